@@ -1,0 +1,1132 @@
+// C-ABI implementation: device context, setup (pattern, symbolic, plans),
+// factorisation driver, solves and the operator entry points.
+// See include/rba_b200.h for the contract and the reference functions each
+// entry point replaces.
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/rba_b200.h"
+#include "kernels.h"
+#include "symbolic.h"
+
+using rba::cplx;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? RBA_ERR_OOM : RBA_ERR_CUDA,           \
+                  std::string("CUDA error: ") + cudaGetErrorString(e_) + " at " #call);   \
+  } while (0)
+
+#define CKL()                                                                             \
+  do {                                                                                    \
+    cudaError_t e_ = cudaGetLastError();                                                  \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(RBA_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+  } while (0)
+
+enum StepKind { ST_EA = 0, ST_DIAG = 1, ST_TRSM = 2, ST_GEMM = 3 };
+struct Step {
+  int kind;
+  int64_t off;
+  int n;
+  int ntiles;
+};
+
+int nr_pad(int s) { return s <= 1 ? 1 : s <= 2 ? 2 : s <= 4 ? 4 : 8; }
+}  // namespace
+
+struct rba_symbolic {
+  rba::Symbolic S;
+};
+
+struct rba_ctx {
+  int device = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  std::vector<void*> allocs;       // persistent (mesh-level) device allocations
+  size_t mem_other = 0, mem_factor = 0, mem_work = 0;
+  // mesh
+  bool have_mesh = false;
+  int64_t N = 0, P = 0;
+  int k = 0;
+  rba::Symbolic sym;
+  int64_t nnzA = 0;
+  std::vector<int32_t> a_rows, a_cols;
+  std::vector<double> Kv_h;
+  double *Kv = nullptr, *Mv = nullptr, *mass = nullptr, *mdev = nullptr, *expm = nullptr;
+  int64_t *tgt = nullptr, *cptr = nullptr, *coff = nullptr;
+  int32_t* cell_dofs_p = nullptr;
+  int64_t* dc_ptr = nullptr;
+  int32_t* dc_item = nullptr;
+  int32_t* perm_d = nullptr;
+  rba::FrontsDev F{};
+  std::vector<Step> plan;
+  int2* ea_tasks = nullptr;
+  rba::PanelTask* pt_tasks = nullptr;
+  rba::GemmTask* gm_tasks = nullptr;
+  std::vector<std::pair<int64_t, int>> fwd_lv, bwd_lv;
+  rba::SolveTask *fwd_tasks = nullptr, *bwd_tasks = nullptr;
+  int* tickets = nullptr;
+  int64_t nblocks = 0;
+  // observation / sources
+  int64_t Mr = 0;
+  int64_t *q_ptr = nullptr, *qt_ptr = nullptr;
+  int32_t *q_col = nullptr, *qt_col = nullptr;
+  double *q_val = nullptr, *qt_val = nullptr;
+  std::vector<void*> obs_allocs;
+  int S = 0, NRs = 1;
+  cplx* Fsrc = nullptr;
+  // poles
+  int m = 0, Kt = 0;
+  std::vector<cplx> poles_h, res_h;
+  cplx *poles_d = nullptr, *res_d = nullptr;
+  std::vector<int> local;
+  int32_t* pole_of_slot = nullptr;
+  int32_t* slot_map = nullptr;   // m entries, staging for combine
+  std::vector<void*> pole_allocs;
+  // per local slot
+  std::vector<cplx*> factor, g, x, uvec;
+  std::vector<int*> flf, flb;
+  std::vector<char> valid;
+  int NRw = 1;
+  std::vector<cplx*> upd;
+  int fbatch = 1;
+  cplx* wa = nullptr;
+  cplx* stage = nullptr;
+  int64_t stage_n = 0;
+  // regulariser
+  int64_t R_rows = 0;
+  int64_t *r_ptr = nullptr, *rt_ptr = nullptr;
+  int32_t *r_idx = nullptr, *rt_idx = nullptr;
+  double *r_val = nullptr, *rt_val = nullptr;
+  std::vector<void*> reg_allocs;
+  // misc
+  double* red_part = nullptr;
+  double* red_res = nullptr;
+  int* err_d = nullptr;
+  int64_t n_fact = 0, n_solve = 0;
+  int epoch = 0;
+  bool model_set = false;
+  bool timing = false;
+  double t_ms[8] = {0};
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+template <class T>
+int dalloc(rba_ctx* c, std::vector<void*>& list, T** out, size_t count, size_t* acct) {
+  *out = nullptr;
+  if (count == 0) count = 1;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(RBA_ERR_OOM, "device allocation of " + std::to_string(count * sizeof(T)) +
+                                 " bytes failed: " + cudaGetErrorString(e));
+  }
+  list.push_back(p);
+  if (acct) *acct += count * sizeof(T);
+  *out = (T*)p;
+  (void)c;
+  return RBA_OK;
+}
+
+template <class T>
+int upload(rba_ctx* c, std::vector<void*>& list, T** out, const T* h, size_t count) {
+  int rc = dalloc(c, list, out, count, &c->mem_other);
+  if (rc) return rc;
+  if (count) CK(cudaMemcpyAsync(*out, h, count * sizeof(T), cudaMemcpyHostToDevice, c->st));
+  return RBA_OK;
+}
+
+void free_list(std::vector<void*>& list) {
+  for (void* p : list) cudaFree(p);
+  list.clear();
+}
+
+void free_slots(rba_ctx* c) {
+  free_list(c->pole_allocs);
+  c->factor.clear(); c->g.clear(); c->x.clear(); c->uvec.clear();
+  c->flf.clear(); c->flb.clear(); c->valid.clear(); c->upd.clear();
+  c->wa = nullptr;
+  c->pole_of_slot = nullptr;
+  c->slot_map = nullptr;
+  c->poles_d = nullptr;
+  c->res_d = nullptr;
+  c->mem_factor = 0;
+  c->mem_work = 0;
+}
+
+int ensure_stage(rba_ctx* c, int64_t n) {
+  if (c->stage_n >= n) return RBA_OK;
+  if (c->stage) { cudaFree(c->stage); c->stage = nullptr; }
+  cudaError_t e = cudaMalloc(&c->stage, n * sizeof(cplx));
+  if (e != cudaSuccess) { cudaGetLastError(); c->stage_n = 0; return fail(RBA_ERR_OOM, "stage alloc"); }
+  c->stage_n = n;
+  return RBA_OK;
+}
+
+// ---------------------------------------------------------------------------
+// plans
+// ---------------------------------------------------------------------------
+int build_plans(rba_ctx* c) {
+  const rba::Symbolic& S = c->sym;
+  std::vector<int2> ea;
+  std::vector<rba::PanelTask> pt;
+  std::vector<rba::GemmTask> gm;
+  c->plan.clear();
+  for (int L = 0; L < S.nlevels; ++L) {
+    const int q0 = S.level_ptr[L], q1 = S.level_ptr[L + 1];
+    // extend-add / zeroing
+    int64_t off = ea.size();
+    for (int q = q0; q < q1; ++q) {
+      int s = S.level_fronts[q];
+      bool kids = S.child_ptr[s + 1] > S.child_ptr[s];
+      if (!kids && S.nf[s] == S.npiv[s]) continue;
+      int c0 = kids ? 0 : S.npiv[s] / 32;
+      for (int ct = c0; ct * 32 < S.nf[s]; ++ct) ea.push_back(make_int2(s, ct));
+    }
+    if ((int64_t)ea.size() > off) c->plan.push_back({ST_EA, off, (int)(ea.size() - off), 0});
+    int kmax = 0;
+    for (int q = q0; q < q1; ++q) kmax = std::max(kmax, (S.npiv[S.level_fronts[q]] + rba::PB - 1) / rba::PB);
+    for (int kk = 0; kk < kmax; ++kk) {
+      const int k0 = kk * rba::PB;
+      int64_t doff = pt.size();
+      for (int q = q0; q < q1; ++q) {
+        int s = S.level_fronts[q];
+        if (S.npiv[s] > k0) pt.push_back({s, k0, k0, 0});
+      }
+      if ((int64_t)pt.size() > doff) c->plan.push_back({ST_DIAG, doff, (int)(pt.size() - doff), 0});
+      int64_t toff = pt.size();
+      for (int q = q0; q < q1; ++q) {
+        int s = S.level_fronts[q];
+        if (S.npiv[s] <= k0) continue;
+        int kb = std::min(rba::PB, S.npiv[s] - k0);
+        for (int r0 = k0 + kb; r0 < S.nf[s]; r0 += rba::PB) pt.push_back({s, k0, r0, 0});
+      }
+      if ((int64_t)pt.size() > toff) c->plan.push_back({ST_TRSM, toff, (int)(pt.size() - toff), 0});
+      int64_t goff = gm.size();
+      int tiles = 0;
+      for (int q = q0; q < q1; ++q) {
+        int s = S.level_fronts[q];
+        if (S.npiv[s] <= k0) continue;
+        int kb = std::min(rba::PB, S.npiv[s] - k0);
+        int clo = k0 + kb, chi = S.npiv[s];
+        if (chi <= clo) continue;
+        int ntr = (S.nf[s] - clo + rba::GT - 1) / rba::GT;
+        int ntc = (chi - clo + rba::GT - 1) / rba::GT;
+        int nt = 0;
+        for (int j = 0; j < ntc; ++j) nt += ntr - j;
+        gm.push_back({s, k0, k0 + kb, clo, chi, tiles, ntr, 0});
+        tiles += nt;
+      }
+      if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles});
+    }
+    // Schur complement of each front with a border
+    int64_t goff = gm.size();
+    int tiles = 0;
+    for (int q = q0; q < q1; ++q) {
+      int s = S.level_fronts[q];
+      int p = S.npiv[s], nf = S.nf[s];
+      if (nf <= p || p == 0) continue;
+      int ntr = (nf - p + rba::GT - 1) / rba::GT;
+      gm.push_back({s, 0, p, p, nf, tiles, ntr, 0});
+      tiles += ntr * (ntr + 1) / 2;
+    }
+    if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles});
+  }
+  int rc;
+  if ((rc = upload(c, c->allocs, &c->ea_tasks, ea.data(), ea.size()))) return rc;
+  if ((rc = upload(c, c->allocs, &c->pt_tasks, pt.data(), pt.size()))) return rc;
+  if ((rc = upload(c, c->allocs, &c->gm_tasks, gm.data(), gm.size()))) return rc;
+
+  // solve plans
+  std::vector<rba::SolveTask> ft, bt;
+  c->fwd_lv.assign(S.nlevels, {0, 0});
+  c->bwd_lv.assign(S.nlevels, {0, 0});
+  std::vector<int64_t> blk_off(S.nfront + 1, 0);
+  for (int s = 0; s < S.nfront; ++s) blk_off[s + 1] = blk_off[s] + (S.npiv[s] + rba::PB - 1) / rba::PB;
+  c->nblocks = blk_off[S.nfront];
+  for (int L = 0; L < S.nlevels; ++L) {
+    const int q0 = S.level_ptr[L], q1 = S.level_ptr[L + 1];
+    int bmax = 0;
+    for (int q = q0; q < q1; ++q) {
+      int s = S.level_fronts[q];
+      int npb = (S.npiv[s] + rba::PB - 1) / rba::PB;
+      int nbb = (S.nf[s] - S.npiv[s] + rba::PB - 1) / rba::PB;
+      bmax = std::max(bmax, npb + nbb);
+    }
+    int64_t off = ft.size();
+    for (int b = 0; b < bmax; ++b)
+      for (int q = q0; q < q1; ++q) {
+        int s = S.level_fronts[q];
+        int npb = (S.npiv[s] + rba::PB - 1) / rba::PB;
+        int nbb = (S.nf[s] - S.npiv[s] + rba::PB - 1) / rba::PB;
+        if (b < npb + nbb) ft.push_back({s, b});
+      }
+    c->fwd_lv[L] = {off, (int)(ft.size() - off)};
+    off = bt.size();
+    int pmax = 0;
+    for (int q = q0; q < q1; ++q) pmax = std::max(pmax, (S.npiv[S.level_fronts[q]] + rba::PB - 1) / rba::PB);
+    for (int key = 0; key < pmax; ++key)
+      for (int q = q0; q < q1; ++q) {
+        int s = S.level_fronts[q];
+        int npb = (S.npiv[s] + rba::PB - 1) / rba::PB;
+        if (key < npb) bt.push_back({s, npb - 1 - key});
+      }
+    c->bwd_lv[L] = {off, (int)(bt.size() - off)};
+  }
+  if ((rc = upload(c, c->allocs, &c->fwd_tasks, ft.data(), ft.size()))) return rc;
+  if ((rc = upload(c, c->allocs, &c->bwd_tasks, bt.data(), bt.size()))) return rc;
+  if ((rc = dalloc(c, c->allocs, &c->tickets, 2 * (size_t)S.nlevels + 2, &c->mem_other))) return rc;
+
+  // solve gather lists (child u-vector rows -> parent front rows), child order
+  const int64_t nrows_tot = S.rows_off[S.nfront];
+  std::vector<int64_t> ucnt(nrows_tot + 1, 0);
+  for (int ch = 0; ch < S.nfront; ++ch) {
+    int s = S.parent[ch];
+    if (s < 0) continue;
+    for (int64_t kk = 0; kk < S.nf[ch] - S.npiv[ch]; ++kk)
+      ucnt[S.rows_off[s] + S.relmap[S.rel_off[ch] + kk] + 1]++;
+  }
+  for (int64_t i = 0; i < nrows_tot; ++i) ucnt[i + 1] += ucnt[i];
+  std::vector<int64_t> uidx(ucnt[nrows_tot]);
+  std::vector<int64_t> pos(ucnt.begin(), ucnt.end() - 1);
+  for (int s = 0; s < S.nfront; ++s)
+    for (int ci = S.child_ptr[s]; ci < S.child_ptr[s + 1]; ++ci) {
+      int ch = S.child_list[ci];
+      for (int64_t kk = 0; kk < S.nf[ch] - S.npiv[ch]; ++kk)
+        uidx[pos[S.rows_off[s] + S.relmap[S.rel_off[ch] + kk]]++] = S.uvec_off[ch] + kk;
+    }
+  int64_t *ucp, *uci, *bo;
+  if ((rc = upload(c, c->allocs, &ucp, ucnt.data(), ucnt.size()))) return rc;
+  if ((rc = upload(c, c->allocs, &uci, uidx.data(), uidx.size()))) return rc;
+  if ((rc = upload(c, c->allocs, &bo, blk_off.data(), blk_off.size()))) return rc;
+  c->F.ucon_ptr = ucp;
+  c->F.ucon_idx = uci;
+  c->F.blk_off = bo;
+  return RBA_OK;
+}
+
+int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
+  for (const Step& s : c->plan) {
+    switch (s.kind) {
+      case ST_EA: rba::launch_extend_add(c->st, c->ea_tasks + s.off, s.n, c->F, pb); break;
+      case ST_DIAG: rba::launch_diag(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d); break;
+      case ST_TRSM: rba::launch_trsm(c->st, c->pt_tasks + s.off, s.n, c->F, pb); break;
+      case ST_GEMM: rba::launch_gemm_update(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb); break;
+    }
+    CKL();
+  }
+  return RBA_OK;
+}
+
+int check_err(rba_ctx* c, int pole) {
+  int h = 0;
+  CK(cudaMemcpyAsync(&h, c->err_d, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  if (h) {
+    CK(cudaMemsetAsync(c->err_d, 0, sizeof(int), c->st));
+    return fail(RBA_ERR_SOLVE, "factorization of shifted matrix failed: zero or non-finite pivot "
+                               "in front " + std::to_string(h - 1) + " (pole " +
+                               std::to_string(pole) + ")");
+  }
+  return RBA_OK;
+}
+
+int ensure_slots(rba_ctx* c) {
+  if (!c->factor.empty()) return RBA_OK;
+  const int nl = (int)c->local.size();
+  if (nl == 0) return RBA_OK;
+  const rba::Symbolic& S = c->sym;
+  int rc;
+  c->factor.assign(nl, nullptr); c->g.assign(nl, nullptr); c->x.assign(nl, nullptr);
+  c->uvec.assign(nl, nullptr); c->flf.assign(nl, nullptr); c->flb.assign(nl, nullptr);
+  c->valid.assign(nl, 0);
+  c->NRw = c->NRs;
+  for (int l = 0; l < nl; ++l) {
+    if ((rc = dalloc(c, c->pole_allocs, &c->factor[l], S.panel_off[S.nfront], &c->mem_factor))) return rc;
+    if ((rc = dalloc(c, c->pole_allocs, &c->g[l], (size_t)c->N * c->NRw, &c->mem_work))) return rc;
+    if ((rc = dalloc(c, c->pole_allocs, &c->x[l], (size_t)c->N * c->NRw, &c->mem_work))) return rc;
+    if ((rc = dalloc(c, c->pole_allocs, &c->uvec[l], (size_t)std::max<int64_t>(S.uvec_off[S.nfront], 1) * c->NRw, &c->mem_work))) return rc;
+    if ((rc = dalloc(c, c->pole_allocs, &c->flf[l], (size_t)c->nblocks + 1, &c->mem_work))) return rc;
+    if ((rc = dalloc(c, c->pole_allocs, &c->flb[l], (size_t)c->nblocks + 1, &c->mem_work))) return rc;
+    CK(cudaMemsetAsync(c->flf[l], 0, (c->nblocks + 1) * sizeof(int), c->st));
+    CK(cudaMemsetAsync(c->flb[l], 0, (c->nblocks + 1) * sizeof(int), c->st));
+    CK(cudaMemsetAsync(c->g[l], 0, (size_t)c->N * c->NRw * sizeof(cplx), c->st));
+  }
+  c->fbatch = 1;
+  if (const char* e = getenv("RBA_FACTOR_BATCH")) c->fbatch = std::max(1, std::min(atoi(e), nl));
+  c->upd.assign(c->fbatch, nullptr);
+  for (int b = 0; b < c->fbatch; ++b)
+    if ((rc = dalloc(c, c->pole_allocs, &c->upd[b], (size_t)S.upd_total, &c->mem_work))) return rc;
+  if ((rc = dalloc(c, c->pole_allocs, &c->wa, (size_t)nl * std::max(c->S, 1) * std::max<int64_t>(c->Mr, 1), &c->mem_work))) return rc;
+  std::vector<int32_t> pos(c->local.begin(), c->local.end());
+  if ((rc = dalloc(c, c->pole_allocs, &c->pole_of_slot, nl, &c->mem_other))) return rc;
+  CK(cudaMemcpyAsync(c->pole_of_slot, pos.data(), nl * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+  return RBA_OK;
+}
+
+int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR) {
+  const int ns = (int)slots.size();
+  if (ns == 0) return RBA_OK;
+  rba::SolveBatch b;
+  for (int i = 0; i < ns; ++i) {
+    int l = slots[i];
+    if (!c->valid[l]) return fail(RBA_ERR_CACHE_MISS, "no factorization for pole " +
+                                                         std::to_string(c->local[l]));
+    b.factor[i] = c->factor[l];
+    b.x[i] = c->x[l];
+    b.uvec[i] = c->uvec[l];
+    b.flags_f[i] = c->flf[l];
+    b.flags_b[i] = c->flb[l];
+  }
+  const rba::Symbolic& S = c->sym;
+  c->epoch++;
+  CK(cudaMemsetAsync(c->tickets, 0, (2 * (size_t)S.nlevels + 2) * sizeof(int), c->st));
+  if (c->timing) cudaEventRecord(c->ev[0], c->st);
+  for (int L = 0; L < S.nlevels; ++L) {
+    rba::launch_solve_level(c->st, true, NR, c->fwd_tasks + c->fwd_lv[L].first, c->fwd_lv[L].second,
+                            ns, c->F, b, c->tickets + L, c->epoch);
+    CKL();
+  }
+  if (c->timing) cudaEventRecord(c->ev[1], c->st);
+  for (int L = S.nlevels - 1; L >= 0; --L) {
+    rba::launch_solve_level(c->st, false, NR, c->bwd_tasks + c->bwd_lv[L].first, c->bwd_lv[L].second,
+                            ns, c->F, b, c->tickets + S.nlevels + L, c->epoch);
+    CKL();
+  }
+  if (c->timing) {
+    cudaEventRecord(c->ev[2], c->st);
+    cudaEventSynchronize(c->ev[2]);
+    float a = 0, bb = 0;
+    cudaEventElapsedTime(&a, c->ev[0], c->ev[1]);
+    cudaEventElapsedTime(&bb, c->ev[1], c->ev[2]);
+    c->t_ms[4] = a;
+    c->t_ms[5] = bb;
+  }
+  c->n_solve += ns;
+  return RBA_OK;
+}
+
+rba::ElemDev elem(rba_ctx* c) {
+  rba::ElemDev E;
+  E.N = c->N;
+  E.P = c->P;
+  E.cell_dofs = c->cell_dofs_p;
+  E.mass = c->mass;
+  E.expm = c->expm;
+  E.dc_ptr = c->dc_ptr;
+  E.dc_item = c->dc_item;
+  return E;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rba_last_error(void) { return g_err.c_str(); }
+int rba_version(void) { return 1; }
+
+int rba_symbolic_analyze(int64_t n, const int64_t* indptr, const int32_t* indices,
+                         const double* coords, int32_t leaf, rba_symbolic** out) {
+  if (!out || !indptr || !indices) return fail(RBA_ERR_INVALID, "null argument");
+  auto* s = new rba_symbolic();
+  std::string e = rba::analyze(n, indptr, indices, coords, leaf, s->S);
+  if (!e.empty()) { delete s; return fail(RBA_ERR_INVALID, e); }
+  *out = s;
+  return RBA_OK;
+}
+
+int rba_symbolic_stats(const rba_symbolic* s, int64_t* is, double* ds) {
+  if (!s) return fail(RBA_ERR_INVALID, "null symbolic");
+  const rba::Symbolic& S = s->S;
+  int64_t nb = 0;
+  for (int f = 0; f < S.nfront; ++f) nb += (S.npiv[f] + rba::PB - 1) / rba::PB;
+  int64_t v[16] = {S.n, S.nfront, S.nlevels, S.nnzL, S.panel_off[S.nfront], S.upd_total,
+                   S.uvec_off[S.nfront], S.max_nf, S.max_npiv, nb, 0, 0, 0, 0, 0, 0};
+  if (is) memcpy(is, v, sizeof(v));
+  if (ds) { ds[0] = S.flops; ds[1] = ds[2] = ds[3] = 0; }
+  return RBA_OK;
+}
+
+int rba_symbolic_array(const rba_symbolic* s, const char* name, void* out, int64_t cap,
+                       int64_t* nbytes) {
+  if (!s || !name) return fail(RBA_ERR_INVALID, "null argument");
+  const rba::Symbolic& S = s->S;
+  const void* src = nullptr;
+  int64_t nb = 0;
+  auto pick32 = [&](const std::vector<int32_t>& v) { src = v.data(); nb = v.size() * 4; };
+  auto pick64 = [&](const std::vector<int64_t>& v) { src = v.data(); nb = v.size() * 8; };
+  std::string n(name);
+  if (n == "perm") pick32(S.perm);
+  else if (n == "first") pick32(S.first);
+  else if (n == "npiv") pick32(S.npiv);
+  else if (n == "nf") pick32(S.nf);
+  else if (n == "parent") pick32(S.parent);
+  else if (n == "level") pick32(S.level);
+  else if (n == "rows") pick32(S.rows);
+  else if (n == "relmap") pick32(S.relmap);
+  else if (n == "rows_off") pick64(S.rows_off);
+  else if (n == "rel_off") pick64(S.rel_off);
+  else if (n == "panel_off") pick64(S.panel_off);
+  else if (n == "upd_off") pick64(S.upd_off);
+  else return fail(RBA_ERR_INVALID, "unknown symbolic array " + n);
+  if (nbytes) *nbytes = nb;
+  if (out) {
+    if (cap < nb) return fail(RBA_ERR_INVALID, "buffer too small");
+    memcpy(out, src, nb);
+  }
+  return RBA_OK;
+}
+
+void rba_symbolic_destroy(rba_symbolic* s) { delete s; }
+
+int rba_ctx_create(int device, void* stream, rba_ctx** out) {
+  if (!out) return fail(RBA_ERR_INVALID, "null out");
+  int ndev = 0;
+  CK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return fail(RBA_ERR_INVALID, "bad device index");
+  CK(cudaSetDevice(device));
+  auto* c = new rba_ctx();
+  c->device = device;
+  if (stream) {
+    c->st = (cudaStream_t)stream;
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { delete c; return fail(RBA_ERR_CUDA, cudaGetErrorString(e)); }
+    c->own_stream = true;
+  }
+  for (auto& e : c->ev) cudaEventCreate(&e);
+  int rc;
+  if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||
+      (rc = dalloc(c, c->allocs, &c->red_part, 1024, &c->mem_other)) ||
+      (rc = dalloc(c, c->allocs, &c->red_res, 8, &c->mem_other))) {
+    rba_ctx_destroy(c);
+    return rc;
+  }
+  cudaMemsetAsync(c->err_d, 0, sizeof(int), c->st);
+  *out = c;
+  return RBA_OK;
+}
+
+void rba_ctx_destroy(rba_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->st) cudaStreamSynchronize(c->st);
+  free_slots(c);
+  free_list(c->obs_allocs);
+  free_list(c->reg_allocs);
+  free_list(c->allocs);
+  if (c->stage) cudaFree(c->stage);
+  for (auto& e : c->ev) if (e) cudaEventDestroy(e);
+  if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+  delete c;
+}
+
+int rba_set_mesh(rba_ctx* c, int64_t N, int64_t P, int32_t k, const int32_t* cell_dofs,
+                 const double* mass_local, const int64_t* Kp, const int32_t* Ki, const double* Kx,
+                 const double* coords, int32_t leaf) {
+  if (!c || !Kp || !Ki || !Kx || (P > 0 && (!cell_dofs || !mass_local)))
+    return fail(RBA_ERR_INVALID, "null argument");
+  if (N <= 0 || P < 0 || k <= 0 || k > 6) return fail(RBA_ERR_INVALID, "bad mesh sizes");
+  if (c->have_mesh) return fail(RBA_ERR_STATE, "mesh already set on this context");
+  CK(cudaSetDevice(c->device));
+  c->N = N; c->P = P; c->k = k;
+  // dof -> (cell, slot) lists
+  std::vector<int64_t> dcp(N + 1, 0);
+  for (int64_t i = 0; i < P * k; ++i) {
+    int32_t d = cell_dofs[i];
+    if (d >= N) return fail(RBA_ERR_INVALID, "cell_dofs entry out of range");
+    if (d >= 0) dcp[d + 1]++;
+  }
+  for (int64_t i = 0; i < N; ++i) dcp[i + 1] += dcp[i];
+  std::vector<int32_t> dci(dcp[N]);
+  {
+    std::vector<int64_t> pos(dcp.begin(), dcp.end() - 1);
+    for (int64_t cidx = 0; cidx < P; ++cidx)
+      for (int a = 0; a < k; ++a) {
+        int32_t d = cell_dofs[cidx * k + a];
+        if (d >= 0) dci[pos[d]++] = (int32_t)(cidx * 6 + a);
+      }
+  }
+  // full symmetric pattern: element pattern U K pattern
+  std::vector<int64_t> ap(N + 1, 0);
+  std::vector<int32_t> ai;
+  {
+    std::vector<int32_t> mark(N, -1), row;
+    ai.reserve((size_t)dcp[N] * k);
+    for (int64_t r = 0; r < N; ++r) {
+      row.clear();
+      for (int64_t q = dcp[r]; q < dcp[r + 1]; ++q) {
+        int64_t cidx = dci[q] / 6;
+        for (int b = 0; b < k; ++b) {
+          int32_t cc = cell_dofs[cidx * k + b];
+          if (cc >= 0 && mark[cc] != r) { mark[cc] = (int32_t)r; row.push_back(cc); }
+        }
+      }
+      for (int64_t e = Kp[r]; e < Kp[r + 1]; ++e) {
+        int32_t cc = Ki[e];
+        if (cc < 0 || cc >= N) return fail(RBA_ERR_INVALID, "K index out of range");
+        if (mark[cc] != r) { mark[cc] = (int32_t)r; row.push_back(cc); }
+      }
+      if (mark[r] != r) { mark[r] = (int32_t)r; row.push_back((int32_t)r); }
+      std::sort(row.begin(), row.end());
+      ai.insert(ai.end(), row.begin(), row.end());
+      ap[r + 1] = ai.size();
+    }
+  }
+  // lower triangle (row >= col), K values, M contribution lists
+  std::vector<int64_t> lp(N + 1, 0);
+  c->a_rows.clear(); c->a_cols.clear(); c->Kv_h.clear();
+  for (int64_t r = 0; r < N; ++r) {
+    for (int64_t e = ap[r]; e < ap[r + 1]; ++e) {
+      int32_t cc = ai[e];
+      if (cc > r) break;
+      c->a_rows.push_back((int32_t)r);
+      c->a_cols.push_back(cc);
+    }
+    lp[r + 1] = c->a_rows.size();
+  }
+  c->nnzA = c->a_rows.size();
+  c->Kv_h.assign(c->nnzA, 0.0);
+  for (int64_t r = 0; r < N; ++r)
+    for (int64_t e = Kp[r]; e < Kp[r + 1]; ++e) {
+      int32_t cc = Ki[e];
+      if (cc > r) continue;
+      const int32_t* b0 = c->a_cols.data() + lp[r];
+      const int32_t* b1 = c->a_cols.data() + lp[r + 1];
+      const int32_t* it = std::lower_bound(b0, b1, cc);
+      c->Kv_h[lp[r] + (it - b0)] += Kx[e];
+    }
+  std::vector<int64_t> mcnt(c->nnzA + 1, 0);
+  std::vector<int64_t> me;  // (e, off) pairs flattened
+  me.reserve((size_t)P * k * (k + 1));
+  for (int64_t cidx = 0; cidx < P; ++cidx)
+    for (int a = 0; a < k; ++a) {
+      int32_t r = cell_dofs[cidx * k + a];
+      if (r < 0) continue;
+      for (int b = 0; b < k; ++b) {
+        int32_t cc = cell_dofs[cidx * k + b];
+        if (cc < 0 || cc > r) continue;
+        const int32_t* b0 = c->a_cols.data() + lp[r];
+        const int32_t* b1 = c->a_cols.data() + lp[r + 1];
+        int64_t e = lp[r] + (std::lower_bound(b0, b1, cc) - b0);
+        me.push_back(e);
+        me.push_back(cidx * 36 + a * 6 + b);
+        mcnt[e + 1]++;
+      }
+    }
+  for (int64_t e = 0; e < c->nnzA; ++e) mcnt[e + 1] += mcnt[e];
+  std::vector<int64_t> moff(mcnt[c->nnzA]);
+  {
+    std::vector<int64_t> pos(mcnt.begin(), mcnt.end() - 1);
+    for (size_t q = 0; q < me.size(); q += 2) moff[pos[me[q]]++] = me[q + 1];
+  }
+  std::vector<int64_t>().swap(me);
+  // symbolic analysis
+  std::string err = rba::analyze(N, ap.data(), ai.data(), coords, leaf > 0 ? leaf : 64, c->sym);
+  if (!err.empty()) return fail(RBA_ERR_INVALID, "symbolic analysis: " + err);
+  const rba::Symbolic& S = c->sym;
+  // scatter targets of A entries into the front panels
+  std::vector<int32_t> front_of(N);
+  for (int s = 0; s < S.nfront; ++s)
+    for (int q = 0; q < S.npiv[s]; ++q) front_of[S.first[s] + q] = s;
+  std::vector<int64_t> tgt(c->nnzA);
+  for (int64_t e = 0; e < c->nnzA; ++e) {
+    int32_t pr = S.iperm[c->a_rows[e]], pc = S.iperm[c->a_cols[e]];
+    int32_t hi = std::max(pr, pc), lo = std::min(pr, pc);
+    int s = front_of[lo];
+    const int32_t* rb = S.rows.data() + S.rows_off[s];
+    const int32_t* it = std::lower_bound(rb, rb + S.nf[s], hi);
+    if (it == rb + S.nf[s] || *it != hi) return fail(RBA_ERR_INVALID, "internal: A entry outside front");
+    tgt[e] = S.panel_off[s] + (int64_t)(lo - S.first[s]) * S.nf[s] + (it - rb);
+  }
+  // permuted element data
+  std::vector<int32_t> cdp((size_t)P * 6, -1);
+  std::vector<double> mass36((size_t)P * 36, 0.0);
+  for (int64_t cidx = 0; cidx < P; ++cidx)
+    for (int a = 0; a < k; ++a) {
+      int32_t d = cell_dofs[cidx * k + a];
+      cdp[cidx * 6 + a] = d >= 0 ? S.iperm[d] : -1;
+      for (int b = 0; b < k; ++b) mass36[cidx * 36 + a * 6 + b] = mass_local[(cidx * k + a) * k + b];
+    }
+  // dof lists re-indexed by permuted dof, element mass offsets rebased to 36
+  std::vector<int64_t> pdcp(N + 1, 0);
+  std::vector<int32_t> pdci(dci.size());
+  for (int64_t kk = 0; kk < N; ++kk) {
+    int32_t o = S.perm[kk];
+    pdcp[kk + 1] = pdcp[kk] + (dcp[o + 1] - dcp[o]);
+  }
+  for (int64_t kk = 0; kk < N; ++kk) {
+    int32_t o = S.perm[kk];
+    std::copy(dci.begin() + dcp[o], dci.begin() + dcp[o + 1], pdci.begin() + pdcp[kk]);
+  }
+  // uploads
+  int rc;
+  auto up32 = [&](int32_t** d, const std::vector<int32_t>& v) { return upload(c, c->allocs, d, v.data(), v.size()); };
+  auto up64 = [&](int64_t** d, const std::vector<int64_t>& v) { return upload(c, c->allocs, d, v.data(), v.size()); };
+  int32_t *d_first, *d_npiv, *d_nf, *d_rows, *d_cp, *d_cl, *d_rel;
+  int64_t *d_po, *d_uo, *d_ro, *d_relo, *d_uvo;
+  if ((rc = up32(&d_first, S.first)) || (rc = up32(&d_npiv, S.npiv)) || (rc = up32(&d_nf, S.nf)) ||
+      (rc = up32(&d_rows, S.rows)) || (rc = up32(&d_cp, S.child_ptr)) ||
+      (rc = up32(&d_cl, S.child_list)) || (rc = up32(&d_rel, S.relmap)) ||
+      (rc = up64(&d_po, S.panel_off)) || (rc = up64(&d_uo, S.upd_off)) ||
+      (rc = up64(&d_ro, S.rows_off)) || (rc = up64(&d_relo, S.rel_off)) ||
+      (rc = up64(&d_uvo, S.uvec_off)))
+    return rc;
+  c->F.first = d_first; c->F.npiv = d_npiv; c->F.nf = d_nf; c->F.rows = d_rows;
+  c->F.child_ptr = d_cp; c->F.child_list = d_cl; c->F.relmap = d_rel;
+  c->F.panel_off = d_po; c->F.upd_off = d_uo; c->F.rows_off = d_ro; c->F.rel_off = d_relo;
+  c->F.uvec_off = d_uvo;
+  if ((rc = upload(c, c->allocs, &c->Kv, c->Kv_h.data(), c->Kv_h.size())) ||
+      (rc = dalloc(c, c->allocs, &c->Mv, c->nnzA, &c->mem_other)) ||
+      (rc = up64(&c->tgt, tgt)) || (rc = up64(&c->cptr, mcnt)) || (rc = up64(&c->coff, moff)) ||
+      (rc = upload(c, c->allocs, &c->mass, mass36.data(), mass36.size())) ||
+      (rc = dalloc(c, c->allocs, &c->mdev, P, &c->mem_other)) ||
+      (rc = dalloc(c, c->allocs, &c->expm, P, &c->mem_other)) ||
+      (rc = up32(&c->cell_dofs_p, cdp)) || (rc = up64(&c->dc_ptr, pdcp)) ||
+      (rc = up32(&c->dc_item, pdci)) || (rc = up32(&c->perm_d, S.perm)))
+    return rc;
+  if ((rc = build_plans(c))) return rc;
+  CK(cudaStreamSynchronize(c->st));
+  c->have_mesh = true;
+  return RBA_OK;
+}
+
+int rba_set_observation(rba_ctx* c, int64_t Mr, const int64_t* qp, const int32_t* qi,
+                        const double* qx) {
+  if (!c || !c->have_mesh) return fail(RBA_ERR_STATE, "set_mesh first");
+  if (Mr < 0 || (Mr > 0 && (!qp || !qi || !qx))) return fail(RBA_ERR_INVALID, "bad Q");
+  CK(cudaSetDevice(c->device));
+  free_list(c->obs_allocs);
+  free_slots(c);
+  c->Mr = Mr;
+  const rba::Symbolic& S = c->sym;
+  int64_t nnz = Mr > 0 ? qp[Mr] : 0;
+  std::vector<int64_t> ptr(qp, qp + Mr + 1);
+  if (Mr == 0) ptr.assign(1, 0);
+  std::vector<int32_t> col(nnz);
+  std::vector<double> val(qx, qx + nnz);
+  for (int64_t e = 0; e < nnz; ++e) {
+    if (qi[e] < 0 || qi[e] >= c->N) return fail(RBA_ERR_INVALID, "Q index out of range");
+    col[e] = S.iperm[qi[e]];
+  }
+  std::vector<int64_t> tp(c->N + 1, 0);
+  for (int64_t e = 0; e < nnz; ++e) tp[col[e] + 1]++;
+  for (int64_t i = 0; i < c->N; ++i) tp[i + 1] += tp[i];
+  std::vector<int32_t> tc(nnz);
+  std::vector<double> tv(nnz);
+  {
+    std::vector<int64_t> pos(tp.begin(), tp.end() - 1);
+    for (int64_t r = 0; r < Mr; ++r)
+      for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) {
+        int64_t q = pos[col[e]]++;
+        tc[q] = (int32_t)r;
+        tv[q] = val[e];
+      }
+  }
+  int rc;
+  if ((rc = upload(c, c->obs_allocs, &c->q_ptr, ptr.data(), ptr.size())) ||
+      (rc = upload(c, c->obs_allocs, &c->q_col, col.data(), col.size())) ||
+      (rc = upload(c, c->obs_allocs, &c->q_val, val.data(), val.size())) ||
+      (rc = upload(c, c->obs_allocs, &c->qt_ptr, tp.data(), tp.size())) ||
+      (rc = upload(c, c->obs_allocs, &c->qt_col, tc.data(), tc.size())) ||
+      (rc = upload(c, c->obs_allocs, &c->qt_val, tv.data(), tv.size())))
+    return rc;
+  c->S = 0;       // sources live in obs_allocs: set them again
+  c->Fsrc = nullptr;
+  return RBA_OK;
+}
+
+int rba_set_sources(rba_ctx* c, int32_t S_, const double* F) {
+  if (!c || !c->have_mesh) return fail(RBA_ERR_STATE, "set_mesh first");
+  if (S_ < 1 || S_ > 8 || !F) return fail(RBA_ERR_INVALID, "1 <= S <= 8 sources required");
+  if (!c->q_ptr) return fail(RBA_ERR_STATE, "set_observation first");
+  CK(cudaSetDevice(c->device));
+  free_slots(c);
+  c->S = S_;
+  c->NRs = nr_pad(S_);
+  std::vector<cplx> h((size_t)c->N * c->NRs, rba::cmk(0.0, 0.0));
+  for (int64_t kk = 0; kk < c->N; ++kk) {
+    int32_t o = c->sym.perm[kk];
+    for (int s = 0; s < S_; ++s) h[kk * c->NRs + s] = rba::cmk(F[(int64_t)s * c->N + o], 0.0);
+  }
+  return upload(c, c->obs_allocs, &c->Fsrc, h.data(), h.size());
+}
+
+int rba_set_poles(rba_ctx* c, int32_t m, const double* poles, int32_t Kt, const double* res,
+                  int32_t nl, const int32_t* local) {
+  if (!c || !c->have_mesh) return fail(RBA_ERR_STATE, "set_mesh first");
+  if (m < 1 || Kt < 1 || !poles || !res || nl < 0 || nl > 32 || (nl > 0 && !local))
+    return fail(RBA_ERR_INVALID, "bad poles (need 1 <= m, 0 <= n_local <= 32)");
+  if (c->S < 1) return fail(RBA_ERR_STATE, "set_sources first");
+  CK(cudaSetDevice(c->device));
+  free_slots(c);
+  c->m = m;
+  c->Kt = Kt;
+  c->poles_h.assign((const cplx*)poles, (const cplx*)poles + m);
+  c->res_h.assign((const cplx*)res, (const cplx*)res + (size_t)m * Kt);
+  c->local.assign(local, local + nl);
+  for (int l : c->local)
+    if (l < 0 || l >= m) return fail(RBA_ERR_INVALID, "local pole index out of range");
+  int rc;
+  if ((rc = upload(c, c->pole_allocs, &c->poles_d, c->poles_h.data(), c->poles_h.size())) ||
+      (rc = upload(c, c->pole_allocs, &c->res_d, c->res_h.data(), c->res_h.size())) ||
+      (rc = dalloc(c, c->pole_allocs, &c->slot_map, (size_t)m, &c->mem_other)))
+    return rc;
+  return ensure_slots(c);
+}
+
+int rba_set_model_d(rba_ctx* c, const double* m_d) {
+  if (!c || !c->have_mesh) return fail(RBA_ERR_STATE, "set_mesh first");
+  CK(cudaSetDevice(c->device));
+  if (m_d != c->mdev) CK(cudaMemcpyAsync(c->mdev, m_d, c->P * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
+  rba::launch_assemble_M(c->st, c->nnzA, c->cptr, c->coff, c->mass, c->mdev, c->expm, c->P, 36, c->Mv);
+  CKL();
+  for (auto& v : c->valid) v = 0;
+  c->model_set = true;
+  return RBA_OK;
+}
+
+int rba_set_model(rba_ctx* c, const double* m_h) {
+  if (!c || !c->have_mesh || !m_h) return fail(RBA_ERR_STATE, "set_mesh first");
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(c->mdev, m_h, c->P * sizeof(double), cudaMemcpyHostToDevice, c->st));
+  int rc = rba_set_model_d(c, c->mdev);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(c->st));   // m_h is only borrowed for the call
+  return RBA_OK;
+}
+
+int rba_factor(rba_ctx* c) {
+  if (!c || !c->model_set) return fail(RBA_ERR_STATE, "set_model first");
+  if (c->local.empty()) return RBA_OK;
+  CK(cudaSetDevice(c->device));
+  int rc;
+  if ((rc = ensure_slots(c))) return rc;
+  const rba::Symbolic& S = c->sym;
+  const int nl = (int)c->local.size();
+  if (c->timing) cudaEventRecord(c->ev[0], c->st);
+  for (int b0 = 0; b0 < nl; b0 += c->fbatch) {
+    rba::PoleBatch pb;
+    pb.count = std::min(c->fbatch, nl - b0);
+    for (int i = 0; i < pb.count; ++i) {
+      int l = b0 + i;
+      c->valid[l] = 0;
+      pb.factor[i] = c->factor[l];
+      pb.upd[i] = c->upd[i];
+      pb.xi[i] = c->poles_h[c->local[l]];
+      CK(cudaMemsetAsync(c->factor[l], 0, S.panel_off[S.nfront] * sizeof(cplx), c->st));
+    }
+    rba::launch_scatter_A(c->st, c->nnzA, c->tgt, c->Kv, c->Mv, pb);
+    CKL();
+    if ((rc = run_plan(c, pb))) return rc;
+    if ((rc = check_err(c, c->local[b0]))) return rc;
+    for (int i = 0; i < pb.count; ++i) c->valid[b0 + i] = 1;
+    c->n_fact += pb.count;
+  }
+  if (c->timing) {
+    cudaEventRecord(c->ev[1], c->st);
+    cudaEventSynchronize(c->ev[1]);
+    float a = 0;
+    cudaEventElapsedTime(&a, c->ev[0], c->ev[1]);
+    c->t_ms[0] = a;
+  }
+  return RBA_OK;
+}
+
+int rba_factor_values(rba_ctx* c, int32_t slot, const double* vals) {
+  if (!c || !c->have_mesh || !vals) return fail(RBA_ERR_STATE, "set_mesh first");
+  if (slot < 0 || slot >= (int)c->local.size()) return fail(RBA_ERR_INVALID, "bad slot");
+  CK(cudaSetDevice(c->device));
+  int rc;
+  if ((rc = ensure_slots(c))) return rc;
+  if ((rc = ensure_stage(c, c->nnzA))) return rc;
+  const rba::Symbolic& S = c->sym;
+  CK(cudaMemcpyAsync(c->stage, vals, c->nnzA * sizeof(cplx), cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(c->factor[slot], 0, S.panel_off[S.nfront] * sizeof(cplx), c->st));
+  rba::launch_scatter_vals(c->st, c->nnzA, c->tgt, c->stage, c->factor[slot]);
+  CKL();
+  rba::PoleBatch pb;
+  pb.count = 1;
+  pb.factor[0] = c->factor[slot];
+  pb.upd[0] = c->upd[0];
+  pb.xi[0] = rba::cmk(0.0, 0.0);
+  c->valid[slot] = 0;
+  if ((rc = run_plan(c, pb))) return rc;
+  if ((rc = check_err(c, c->local[slot]))) return rc;
+  c->valid[slot] = 1;
+  c->n_fact += 1;
+  return RBA_OK;
+}
+
+int rba_pattern(rba_ctx* c, int64_t* nnz, int32_t* rows, int32_t* cols, double* Kh, double* Mh) {
+  if (!c || !c->have_mesh) return fail(RBA_ERR_STATE, "set_mesh first");
+  if (nnz) *nnz = c->nnzA;
+  if (rows) memcpy(rows, c->a_rows.data(), c->nnzA * 4);
+  if (cols) memcpy(cols, c->a_cols.data(), c->nnzA * 4);
+  if (Kh) memcpy(Kh, c->Kv_h.data(), c->nnzA * 8);
+  if (Mh) {
+    if (!c->model_set) return fail(RBA_ERR_STATE, "set_model first");
+    CK(cudaMemcpyAsync(Mh, c->Mv, c->nnzA * 8, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+  }
+  return RBA_OK;
+}
+
+static int solve_common(rba_ctx* c, int32_t slot, const cplx* rhs_d, cplx* out_d, int32_t nrhs) {
+  if (slot < 0 || slot >= (int)c->local.size()) return fail(RBA_ERR_INVALID, "bad slot");
+  if (!c->valid[slot]) return fail(RBA_ERR_CACHE_MISS, "no factorization for pole " +
+                                                         std::to_string(c->local[slot]));
+  int rc;
+  for (int r0 = 0; r0 < nrhs; r0 += c->NRw) {
+    int nr = std::min(c->NRw, nrhs - r0);
+    rba::launch_perm_in(c->st, c->N, nr, c->NRw, c->perm_d, rhs_d + (int64_t)r0 * c->N, c->N, c->x[slot]);
+    CKL();
+    if ((rc = solve_slots(c, {slot}, c->NRw))) return rc;
+    rba::launch_perm_out(c->st, c->N, nr, c->NRw, c->perm_d, c->x[slot], out_d + (int64_t)r0 * c->N, c->N);
+    CKL();
+  }
+  return RBA_OK;
+}
+
+int rba_solve_d(rba_ctx* c, int32_t slot, const double* rhs_d, double* out_d, int32_t nrhs,
+                int32_t trans) {
+  if (!c || !rhs_d || !out_d || nrhs < 1) return fail(RBA_ERR_INVALID, "bad arguments");
+  (void)trans;  // complex symmetric: A^T = A
+  CK(cudaSetDevice(c->device));
+  return solve_common(c, slot, (const cplx*)rhs_d, (cplx*)out_d, nrhs);
+}
+
+int rba_solve(rba_ctx* c, int32_t slot, const double* rhs_h, double* out_h, int32_t nrhs,
+              int32_t trans) {
+  if (!c || !rhs_h || !out_h || nrhs < 1) return fail(RBA_ERR_INVALID, "bad arguments");
+  (void)trans;
+  CK(cudaSetDevice(c->device));
+  int rc;
+  const int64_t n = c->N * (int64_t)nrhs;
+  if ((rc = ensure_stage(c, 2 * n))) return rc;
+  CK(cudaMemcpyAsync(c->stage, rhs_h, n * sizeof(cplx), cudaMemcpyHostToDevice, c->st));
+  if ((rc = solve_common(c, slot, c->stage, c->stage + n, nrhs))) return rc;
+  CK(cudaMemcpyAsync(out_h, c->stage + n, n * sizeof(cplx), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return RBA_OK;
+}
+
+static std::vector<int> all_slots(rba_ctx* c) {
+  std::vector<int> v(c->local.size());
+  std::iota(v.begin(), v.end(), 0);
+  return v;
+}
+
+static rba::SlotPtrs slot_ptrs(const std::vector<cplx*>& v) {
+  rba::SlotPtrs p;
+  for (size_t i = 0; i < v.size() && i < 32; ++i) p.p[i] = v[i];
+  return p;
+}
+
+int rba_forward_partial(rba_ctx* c, double* qpart) {
+  if (!c || !c->model_set) return fail(RBA_ERR_STATE, "set_model first");
+  CK(cudaSetDevice(c->device));
+  const int nl = (int)c->local.size();
+  for (int l = 0; l < nl; ++l)
+    CK(cudaMemcpyAsync(c->x[l], c->Fsrc, (size_t)c->N * c->NRs * sizeof(cplx), cudaMemcpyDeviceToDevice, c->st));
+  int rc;
+  if ((rc = solve_slots(c, all_slots(c), c->NRs))) return rc;
+  for (int l = 0; l < nl; ++l)
+    CK(cudaMemcpyAsync(c->g[l], c->x[l], (size_t)c->N * c->NRs * sizeof(cplx), cudaMemcpyDeviceToDevice, c->st));
+  if (qpart && c->Mr > 0) {
+    rba::launch_q_apply(c->st, nl, c->Mr, c->q_ptr, c->q_col, c->q_val, slot_ptrs(c->g), c->NRs, c->S, (cplx*)qpart);
+    CKL();
+  }
+  return RBA_OK;
+}
+
+int rba_jvp_partial(rba_ctx* c, const double* v_d, double* qpart) {
+  if (!c || !c->model_set || !v_d || !qpart) return fail(RBA_ERR_STATE, "bad state/arguments");
+  CK(cudaSetDevice(c->device));
+  const int nl = (int)c->local.size();
+  rba::launch_jvp_rhs(c->st, nl, elem(c), v_d, slot_ptrs(c->g), slot_ptrs(c->x), c->NRs, c->S);
+  CKL();
+  int rc;
+  if ((rc = solve_slots(c, all_slots(c), c->NRs))) return rc;
+  if (c->Mr > 0) {
+    rba::launch_q_apply(c->st, nl, c->Mr, c->q_ptr, c->q_col, c->q_val, slot_ptrs(c->x), c->NRs, c->S, (cplx*)qpart);
+    CKL();
+  }
+  return RBA_OK;
+}
+
+int rba_vjp_partial(rba_ctx* c, const double* w_d, double* tpart) {
+  if (!c || !c->model_set || !w_d || !tpart) return fail(RBA_ERR_STATE, "bad state/arguments");
+  CK(cudaSetDevice(c->device));
+  const int nl = (int)c->local.size();
+  rba::launch_vjp_rhs(c->st, nl, c->pole_of_slot, c->S, c->Kt, c->Mr, c->N, w_d, c->res_d, c->qt_ptr,
+                      c->qt_col, c->qt_val, c->wa, slot_ptrs(c->x), c->NRs);
+  CKL();
+  int rc;
+  if ((rc = solve_slots(c, all_slots(c), c->NRs))) return rc;
+  rba::launch_vjp_cells(c->st, nl, c->pole_of_slot, c->poles_d, elem(c), slot_ptrs(c->x), slot_ptrs(c->g),
+                        c->NRs, c->S, tpart);
+  CKL();
+  return RBA_OK;
+}
+
+int rba_combine_data(rba_ctx* c, const double* qall, const int32_t* som, int32_t times_pole,
+                     double* d) {
+  if (!c || !qall || !som || !d) return fail(RBA_ERR_INVALID, "null argument");
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(c->slot_map, som, c->m * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+  rba::launch_combine_data(c->st, c->m, c->S, c->Kt, c->Mr, (const cplx*)qall, c->slot_map, c->res_d,
+                           c->poles_d, times_pole != 0, d);
+  CKL();
+  CK(cudaStreamSynchronize(c->st));  // som is borrowed
+  return RBA_OK;
+}
+
+int rba_combine_cells(rba_ctx* c, const double* tall, const int32_t* som, double* out) {
+  if (!c || !tall || !som || !out) return fail(RBA_ERR_INVALID, "null argument");
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(c->slot_map, som, c->m * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+  rba::launch_combine_cells(c->st, c->m, c->P, tall, c->slot_map, out);
+  CKL();
+  CK(cudaStreamSynchronize(c->st));
+  return RBA_OK;
+}
+
+int rba_set_reg(rba_ctx* c, int64_t nrows, const int64_t* rp, const int32_t* ri, const double* rx) {
+  if (!c || !c->have_mesh || nrows < 0 || (nrows > 0 && (!rp || !ri || !rx)))
+    return fail(RBA_ERR_INVALID, "bad regulariser");
+  CK(cudaSetDevice(c->device));
+  free_list(c->reg_allocs);
+  c->R_rows = nrows;
+  const int64_t nnz = rp[nrows];
+  std::vector<int64_t> tp(c->P + 1, 0);
+  for (int64_t e = 0; e < nnz; ++e) {
+    if (ri[e] < 0 || ri[e] >= c->P) return fail(RBA_ERR_INVALID, "R index out of range");
+    tp[ri[e] + 1]++;
+  }
+  for (int64_t i = 0; i < c->P; ++i) tp[i + 1] += tp[i];
+  std::vector<int32_t> tc(nnz);
+  std::vector<double> tv(nnz);
+  {
+    std::vector<int64_t> pos(tp.begin(), tp.end() - 1);
+    for (int64_t r = 0; r < nrows; ++r)
+      for (int64_t e = rp[r]; e < rp[r + 1]; ++e) {
+        int64_t q = pos[ri[e]]++;
+        tc[q] = (int32_t)r;
+        tv[q] = rx[e];
+      }
+  }
+  int rc;
+  if ((rc = upload(c, c->reg_allocs, &c->r_ptr, rp, nrows + 1)) ||
+      (rc = upload(c, c->reg_allocs, &c->r_idx, ri, nnz)) ||
+      (rc = upload(c, c->reg_allocs, &c->r_val, rx, nnz)) ||
+      (rc = upload(c, c->reg_allocs, &c->rt_ptr, tp.data(), tp.size())) ||
+      (rc = upload(c, c->reg_allocs, &c->rt_idx, tc.data(), tc.size())) ||
+      (rc = upload(c, c->reg_allocs, &c->rt_val, tv.data(), tv.size())))
+    return rc;
+  CK(cudaStreamSynchronize(c->st));
+  return RBA_OK;
+}
+
+int rba_reg_apply(rba_ctx* c, int32_t transpose, const double* x, double alpha, double* y,
+                  int32_t accumulate) {
+  if (!c || !c->r_ptr || !x || !y) return fail(RBA_ERR_STATE, "set_reg first");
+  if (transpose)
+    rba::launch_spmv(c->st, c->P, c->rt_ptr, c->rt_idx, c->rt_val, x, alpha, y, accumulate != 0);
+  else
+    rba::launch_spmv(c->st, c->R_rows, c->r_ptr, c->r_idx, c->r_val, x, alpha, y, accumulate != 0);
+  CKL();
+  return RBA_OK;
+}
+
+int rba_vec_axpby(rba_ctx* c, int64_t n, double a, const double* x, double b, const double* y,
+                  double* out) {
+  rba::launch_axpby(c->st, n, a, x, b, y, out);
+  CKL();
+  return RBA_OK;
+}
+
+int rba_vec_mul(rba_ctx* c, int64_t n, const double* a, const double* x, double alpha,
+                double* out) {
+  rba::launch_mul(c->st, n, a, x, alpha, out);
+  CKL();
+  return RBA_OK;
+}
+
+int rba_vec_dot(rba_ctx* c, int64_t n, const double* x, const double* y, double* result) {
+  rba::launch_dot(c->st, n, x, y, c->red_part, c->red_res);
+  CKL();
+  CK(cudaMemcpyAsync(result, c->red_res, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return RBA_OK;
+}
+
+int rba_vec_lsqr_xw(rba_ctx* c, int64_t n, double t1, double t2, const double* v, double* w,
+                    double* x, double* wn2) {
+  rba::launch_lsqr_xw(c->st, n, t1, t2, v, w, x, c->red_part, c->red_res);
+  CKL();
+  CK(cudaMemcpyAsync(wn2, c->red_res, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return RBA_OK;
+}
+
+int rba_get_g(rba_ctx* c, int32_t slot, double* out_h) {
+  if (!c || !out_h || slot < 0 || slot >= (int)c->local.size()) return fail(RBA_ERR_INVALID, "bad slot");
+  CK(cudaSetDevice(c->device));
+  int rc;
+  const int64_t n = c->N * (int64_t)c->S;
+  if ((rc = ensure_stage(c, n))) return rc;
+  rba::launch_perm_out(c->st, c->N, c->S, c->NRs, c->perm_d, c->g[slot], c->stage, c->N);
+  CKL();
+  CK(cudaMemcpyAsync(out_h, c->stage, n * sizeof(cplx), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return RBA_OK;
+}
+
+int rba_info(rba_ctx* c, int64_t* out) {
+  if (!c || !out) return fail(RBA_ERR_INVALID, "null argument");
+  out[0] = c->n_fact; out[1] = c->n_solve; out[2] = c->N; out[3] = c->P;
+  out[4] = c->Mr; out[5] = c->S; out[6] = c->m; out[7] = (int64_t)c->local.size();
+  return RBA_OK;
+}
+
+int rba_memory(rba_ctx* c, int64_t* out) {
+  if (!c || !out) return fail(RBA_ERR_INVALID, "null argument");
+  out[0] = (int64_t)c->mem_factor; out[1] = (int64_t)c->mem_work; out[2] = (int64_t)c->mem_other;
+  return RBA_OK;
+}
+
+int rba_sync(rba_ctx* c) {
+  CK(cudaStreamSynchronize(c->st));
+  return RBA_OK;
+}
+
+int rba_timings(rba_ctx* c, double* out) {
+  for (int i = 0; i < 8; ++i) out[i] = c->t_ms[i];
+  return RBA_OK;
+}
+
+int rba_set_timing(rba_ctx* c, int32_t en) {
+  c->timing = en != 0;
+  return RBA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,47 @@
+// Device view of the symbolic structure (see symbolic.h) plus the task
+// descriptors of the level-scheduled factorisation and solves.
+#pragma once
+#include "common.cuh"
+
+namespace rba {
+
+struct FrontsDev {
+  const int32_t* first;
+  const int32_t* npiv;
+  const int32_t* nf;
+  const int64_t* panel_off;
+  const int64_t* upd_off;
+  const int64_t* rows_off;
+  const int32_t* rows;
+  const int32_t* child_ptr;
+  const int32_t* child_list;
+  const int64_t* rel_off;
+  const int32_t* relmap;
+  const int64_t* uvec_off;
+  const int64_t* ucon_ptr;   // per front-row (rows_off indexing) -> uvec contributions
+  const int64_t* ucon_idx;
+  const int64_t* blk_off;    // per front: offset of its pivot-block flags
+};
+
+// Batch of poles processed by one launch (gridDim.y or ticket modulo).
+struct PoleBatch {
+  cplx* factor[32];     // per slot: factor storage base
+  cplx* upd[32];        // per slot: update arena base
+  cplx xi[32];          // per slot: pole value
+  int32_t count;
+};
+
+constexpr int PB = 64;   // pivot block (factorisation) and solve row block
+constexpr int GT = 64;   // GEMM tile (complex)
+
+// element address in front s: columns < p live in the factor panel (ld = nf),
+// columns >= p in the update block (ld = nf - p, row offset p).
+__device__ __forceinline__ cplx* faddr(cplx* panel, cplx* upd, int p, int nf, int r, int c) {
+  return c < p ? panel + (int64_t)c * nf + r : upd + (int64_t)(c - p) * (nf - p) + (r - p);
+}
+
+struct PanelTask { int32_t s, k0, r0, pad; };
+struct GemmTask { int32_t s, t0, t1, c_lo, c_hi, tile_start, ntr, pad; };
+struct SolveTask { int32_t s, blk; };
+
+}  // namespace rba

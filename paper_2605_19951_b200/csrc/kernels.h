@@ -1,0 +1,88 @@
+// Host-side launch wrappers of the sm_100a kernels.
+#pragma once
+#include <algorithm>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "fronts.cuh"
+
+namespace rba {
+
+struct SlotPtrs {
+  cplx* p[32];
+};
+
+struct SolveBatch {
+  const cplx* factor[32];
+  cplx* x[32];
+  cplx* uvec[32];
+  int* flags_f[32];
+  int* flags_b[32];
+};
+
+// factorisation
+void launch_assemble_M(cudaStream_t st, int64_t nnz, const int64_t* cptr, const int64_t* coff,
+                       const double* mass, const double* m, double* expm, int64_t P, int k2,
+                       double* Mv);
+void launch_scatter_A(cudaStream_t st, int64_t nnz, const int64_t* tgt, const double* Kv,
+                      const double* Mv, const PoleBatch& pb);
+void launch_scatter_vals(cudaStream_t st, int64_t nnz, const int64_t* tgt, const cplx* vals,
+                         cplx* factor);
+void launch_extend_add(cudaStream_t st, const int2* tasks, int ntasks, const FrontsDev& F,
+                       const PoleBatch& pb);
+void launch_diag(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
+                 const PoleBatch& pb, int* err);
+void launch_trsm(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
+                 const PoleBatch& pb);
+void launch_gemm_update(cudaStream_t st, const GemmTask* tasks, int ntasks, int ntiles,
+                        const FrontsDev& F, const PoleBatch& pb);
+
+// solves
+void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* tasks,
+                        int ntasks, int nslots, const FrontsDev& F, const SolveBatch& b,
+                        int* ticket, int epoch);
+void launch_perm_in(cudaStream_t st, int64_t n, int nrhs, int NR, const int32_t* perm,
+                    const cplx* b, int64_t ldb, cplx* x);
+void launch_perm_out(cudaStream_t st, int64_t n, int nrhs, int NR, const int32_t* perm,
+                     const cplx* x, cplx* b, int64_t ldb);
+
+// element / observation / reduction operators
+struct ElemDev {
+  int64_t N, P;
+  const int32_t* cell_dofs;  // P*6, permuted dofs, -1 eliminated
+  const double* mass;        // P*36
+  const double* expm;        // P
+  const int64_t* dc_ptr;     // N+1 (permuted dof -> items)
+  const int32_t* dc_item;    // c*6 + a
+};
+void launch_jvp_rhs(cudaStream_t st, int nslots, const ElemDev& E, const double* v,
+                    const SlotPtrs& g, const SlotPtrs& out, int NR, int S);
+void launch_q_apply(cudaStream_t st, int nslots, int64_t Mr, const int64_t* qptr,
+                    const int32_t* qcol, const double* qval, const SlotPtrs& h, int NR, int S,
+                    cplx* qpart /* [slot][S][Mr] */);
+void launch_combine_data(cudaStream_t st, int m, int S, int Kt, int64_t Mr, const cplx* qall,
+                         const int32_t* slot_of_pole, const cplx* residues, const cplx* poles,
+                         bool times_pole, double* d /* [S][Kt][Mr] */);
+void launch_vjp_rhs(cudaStream_t st, int nslots, const int32_t* pole_of_slot, int S, int Kt,
+                    int64_t Mr, int64_t N, const double* w, const cplx* residues,
+                    const int64_t* qtptr, const int32_t* qtcol, const double* qtval,
+                    cplx* wa /* [slot][S][Mr] */, const SlotPtrs& out, int NR);
+void launch_vjp_cells(cudaStream_t st, int nslots, const int32_t* pole_of_slot,
+                      const cplx* poles, const ElemDev& E, const SlotPtrs& z,
+                      const SlotPtrs& g, int NR, int S, double* tpart /* [slot][P] */);
+void launch_combine_cells(cudaStream_t st, int m, int64_t P, const double* tall,
+                          const int32_t* slot_of_pole, double* out);
+void launch_spmv(cudaStream_t st, int64_t nrows, const int64_t* ptr, const int32_t* idx,
+                 const double* val, const double* x, double alpha, double* y, bool accumulate);
+// vector kernels (deterministic reductions); partial buffer >= 1024 doubles
+void launch_axpby(cudaStream_t st, int64_t n, double a, const double* x, double b,
+                  const double* y, double* out);
+void launch_mul(cudaStream_t st, int64_t n, const double* a, const double* x, double alpha,
+                double* out);
+void launch_dot(cudaStream_t st, int64_t n, const double* x, const double* y, double* part,
+                double* result);
+void launch_lsqr_xw(cudaStream_t st, int64_t n, double t1, double t2, const double* v,
+                    double* w, double* x, double* part, double* result);
+void launch_zero_c(cudaStream_t st, int64_t n, cplx* p);
+
+}  // namespace rba

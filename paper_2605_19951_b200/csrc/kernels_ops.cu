@@ -1,0 +1,389 @@
+// Element, observation, reduction and vector kernels around the solves:
+//  K8  J v right-hand sides   (dM_contract(g) @ v, mesh.py:358-370 / sensitivity.py:73)
+//  K9  J^T w cell kernel      (dM[i].T @ z, sensitivity.py:92)
+//  K10 Q apply + residue/time combination in ascending pole order
+//      (forward.py:61-63, sensitivity.py:74-78,85-96)
+//  K11 CSR SpMV for the regulariser square root R / R^T (inversion.py:144,147)
+//  K12 LSQR vector kernels with deterministic two-stage reductions
+// All reductions run in a fixed order, so results do not depend on the GPU
+// count or on launch timing.
+#include "fronts.cuh"
+#include "kernels.h"
+
+namespace rba {
+
+static inline int grid_for(int64_t n, int per = 256, int cap = 148 * 16) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((n + per - 1) / per, cap));
+}
+
+// out[k][r] = sum_{(c,a) in dofcells(k)} e^{m_c} v_c (M_c g|_c)_a
+template <int NR>
+__global__ void k_jvp_rhs(ElemDev E, const double* __restrict__ v, SlotPtrs g, SlotPtrs out,
+                          int S) {
+  const int slot = blockIdx.y;
+  const cplx* gs = g.p[slot];
+  cplx* o = out.p[slot];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E.N;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    cplx acc[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[r] = cmk(0.0, 0.0);
+    for (int64_t q = E.dc_ptr[k]; q < E.dc_ptr[k + 1]; ++q) {
+      const int item = E.dc_item[q];
+      const int c = item / 6, a = item - 6 * c;
+      const int32_t* dofs = E.cell_dofs + (int64_t)c * 6;
+      const double* Mrow = E.mass + (int64_t)c * 36 + a * 6;
+      cplx loc[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) loc[r] = cmk(0.0, 0.0);
+#pragma unroll
+      for (int b = 0; b < 6; ++b) {
+        const int d = __ldg(dofs + b);
+        if (d < 0) continue;
+        const double mab = __ldg(Mrow + b);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          if (r < S) {
+            const cplx gv = gs[(int64_t)d * NR + r];
+            loc[r].x = fma(mab, gv.x, loc[r].x);
+            loc[r].y = fma(mab, gv.y, loc[r].y);
+          }
+        }
+      }
+      const double sc = __ldg(E.expm + c) * __ldg(v + c);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        acc[r].x = fma(loc[r].x, sc, acc[r].x);
+        acc[r].y = fma(loc[r].y, sc, acc[r].y);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) o[k * NR + r] = acc[r];
+  }
+}
+
+void launch_jvp_rhs(cudaStream_t st, int nslots, const ElemDev& E, const double* v,
+                    const SlotPtrs& g, const SlotPtrs& out, int NR, int S) {
+  dim3 grid(grid_for(E.N), nslots);
+  switch (NR) {
+    case 1: k_jvp_rhs<1><<<grid, 256, 0, st>>>(E, v, g, out, S); break;
+    case 2: k_jvp_rhs<2><<<grid, 256, 0, st>>>(E, v, g, out, S); break;
+    case 4: k_jvp_rhs<4><<<grid, 256, 0, st>>>(E, v, g, out, S); break;
+    default: k_jvp_rhs<8><<<grid, 256, 0, st>>>(E, v, g, out, S); break;
+  }
+}
+
+// qpart[slot][s][r] = sum_e Q[r,e] h[col_e][s]
+__global__ void k_q_apply(int64_t Mr, const int64_t* __restrict__ qptr,
+                          const int32_t* __restrict__ qcol, const double* __restrict__ qval,
+                          SlotPtrs h, int NR, int S, cplx* __restrict__ qpart) {
+  const int slot = blockIdx.y;
+  const cplx* hs = h.p[slot];
+  const int64_t total = Mr * S;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t % Mr;
+    const int s = (int)(t / Mr);
+    cplx acc = cmk(0.0, 0.0);
+    for (int64_t e = qptr[r]; e < qptr[r + 1]; ++e) {
+      const cplx hv = hs[(int64_t)qcol[e] * NR + s];
+      acc.x = fma(qval[e], hv.x, acc.x);
+      acc.y = fma(qval[e], hv.y, acc.y);
+    }
+    qpart[((int64_t)slot * S + s) * Mr + r] = acc;
+  }
+}
+
+void launch_q_apply(cudaStream_t st, int nslots, int64_t Mr, const int64_t* qptr,
+                    const int32_t* qcol, const double* qval, const SlotPtrs& h, int NR, int S,
+                    cplx* qpart) {
+  if (Mr <= 0) return;
+  dim3 grid(grid_for(Mr * S), nslots);
+  k_q_apply<<<grid, 256, 0, st>>>(Mr, qptr, qcol, qval, h, NR, S, qpart);
+}
+
+// d[s][j][r] = sum_i 2 Re( (alpha_ij q_i,s,r) [* xi_i] ), i ascending
+__global__ void k_combine_data(int m, int S, int Kt, int64_t Mr, const cplx* __restrict__ qall,
+                               const int32_t* __restrict__ slot_of_pole,
+                               const cplx* __restrict__ res, const cplx* __restrict__ poles,
+                               bool times_pole, double* __restrict__ d) {
+  const int64_t total = (int64_t)S * Kt * Mr;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t % Mr;
+    const int j = (int)((t / Mr) % Kt);
+    const int s = (int)(t / (Mr * Kt));
+    double acc = 0.0;
+    for (int i = 0; i < m; ++i) {
+      const cplx q = qall[((int64_t)slot_of_pole[i] * S + s) * Mr + r];
+      cplx z = cmul(res[(int64_t)i * Kt + j], q);
+      if (times_pole) z = cmul(poles[i], z);
+      acc += 2.0 * z.x;
+    }
+    d[t] = acc;
+  }
+}
+
+void launch_combine_data(cudaStream_t st, int m, int S, int Kt, int64_t Mr, const cplx* qall,
+                         const int32_t* slot_of_pole, const cplx* residues, const cplx* poles,
+                         bool times_pole, double* d) {
+  const int64_t total = (int64_t)S * Kt * Mr;
+  if (total <= 0) return;
+  k_combine_data<<<grid_for(total), 256, 0, st>>>(m, S, Kt, Mr, qall, slot_of_pole, residues,
+                                                  poles, times_pole, d);
+}
+
+// wa[slot][s][r] = sum_j alpha_{i,j} w[s][j][r]
+__global__ void k_walpha(int nslots, const int32_t* __restrict__ pole_of_slot, int S, int Kt,
+                         int64_t Mr, const double* __restrict__ w, const cplx* __restrict__ res,
+                         cplx* __restrict__ wa) {
+  const int64_t total = (int64_t)nslots * S * Mr;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = t % Mr;
+    const int s = (int)((t / Mr) % S);
+    const int slot = (int)(t / (Mr * S));
+    const int i = pole_of_slot[slot];
+    cplx acc = cmk(0.0, 0.0);
+    for (int j = 0; j < Kt; ++j) {
+      const double wv = w[((int64_t)s * Kt + j) * Mr + r];
+      const cplx a = res[(int64_t)i * Kt + j];
+      acc.x = fma(a.x, wv, acc.x);
+      acc.y = fma(a.y, wv, acc.y);
+    }
+    wa[t] = acc;
+  }
+}
+
+// out[slot][k][s] = sum_{e in QT row k} QT[k,e] wa[slot][s][col_e]   (all N rows)
+__global__ void k_qt_apply(int64_t N, int S, int64_t Mr, const int64_t* __restrict__ qtptr,
+                           const int32_t* __restrict__ qtcol, const double* __restrict__ qtval,
+                           const cplx* __restrict__ wa, SlotPtrs out, int NR) {
+  const int slot = blockIdx.y;
+  cplx* o = out.p[slot];
+  const cplx* was = wa + (int64_t)slot * S * Mr;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    for (int s = 0; s < NR; ++s) {
+      cplx acc = cmk(0.0, 0.0);
+      if (s < S) {
+        for (int64_t e = qtptr[k]; e < qtptr[k + 1]; ++e) {
+          const cplx a = was[(int64_t)s * Mr + qtcol[e]];
+          acc.x = fma(qtval[e], a.x, acc.x);
+          acc.y = fma(qtval[e], a.y, acc.y);
+        }
+      }
+      o[k * NR + s] = acc;
+    }
+  }
+}
+
+void launch_vjp_rhs(cudaStream_t st, int nslots, const int32_t* pole_of_slot, int S, int Kt,
+                    int64_t Mr, int64_t N, const double* w, const cplx* residues,
+                    const int64_t* qtptr, const int32_t* qtcol, const double* qtval, cplx* wa,
+                    const SlotPtrs& out, int NR) {
+  const int64_t total = (int64_t)nslots * S * Mr;
+  if (total > 0)
+    k_walpha<<<grid_for(total), 256, 0, st>>>(nslots, pole_of_slot, S, Kt, Mr, w, residues, wa);
+  dim3 grid(grid_for(N), nslots);
+  k_qt_apply<<<grid, 256, 0, st>>>(N, S, Mr, qtptr, qtcol, qtval, wa, out, NR);
+}
+
+// tpart[slot][c] = sum_s 2 Re( xi_i * e^{m_c} sum_a z_a (M_c g)_a )
+template <int NR>
+__global__ void k_vjp_cells(const int32_t* __restrict__ pole_of_slot,
+                            const cplx* __restrict__ poles, ElemDev E, SlotPtrs z, SlotPtrs g,
+                            int S, double* __restrict__ tpart) {
+  const int slot = blockIdx.y;
+  const cplx xi = poles[pole_of_slot[slot]];
+  const cplx* zs = z.p[slot];
+  const cplx* gs = g.p[slot];
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < E.P;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t* dofs = E.cell_dofs + c * 6;
+    const double* M = E.mass + c * 36;
+    int dd[6];
+#pragma unroll
+    for (int a = 0; a < 6; ++a) dd[a] = __ldg(dofs + a);
+    const double em = __ldg(E.expm + c);
+    double tot = 0.0;
+#pragma unroll
+    for (int s = 0; s < NR; ++s) {
+      if (s >= S) break;
+      cplx gl[6], zl[6];
+#pragma unroll
+      for (int a = 0; a < 6; ++a) {
+        gl[a] = dd[a] >= 0 ? gs[(int64_t)dd[a] * NR + s] : cmk(0.0, 0.0);
+        zl[a] = dd[a] >= 0 ? zs[(int64_t)dd[a] * NR + s] : cmk(0.0, 0.0);
+      }
+      cplx part = cmk(0.0, 0.0);
+#pragma unroll
+      for (int a = 0; a < 6; ++a) {
+        cplx mg = cmk(0.0, 0.0);
+#pragma unroll
+        for (int b = 0; b < 6; ++b) {
+          const double mab = __ldg(M + a * 6 + b);
+          mg.x = fma(mab, gl[b].x, mg.x);
+          mg.y = fma(mab, gl[b].y, mg.y);
+        }
+        mg.x *= em;
+        mg.y *= em;
+        part = cfma(mg, zl[a], part);
+      }
+      tot += 2.0 * cmul(xi, part).x;
+    }
+    tpart[(int64_t)slot * E.P + c] = tot;
+  }
+}
+
+void launch_vjp_cells(cudaStream_t st, int nslots, const int32_t* pole_of_slot,
+                      const cplx* poles, const ElemDev& E, const SlotPtrs& z,
+                      const SlotPtrs& g, int NR, int S, double* tpart) {
+  dim3 grid(grid_for(E.P), nslots);
+  switch (NR) {
+    case 1: k_vjp_cells<1><<<grid, 256, 0, st>>>(pole_of_slot, poles, E, z, g, S, tpart); break;
+    case 2: k_vjp_cells<2><<<grid, 256, 0, st>>>(pole_of_slot, poles, E, z, g, S, tpart); break;
+    case 4: k_vjp_cells<4><<<grid, 256, 0, st>>>(pole_of_slot, poles, E, z, g, S, tpart); break;
+    default: k_vjp_cells<8><<<grid, 256, 0, st>>>(pole_of_slot, poles, E, z, g, S, tpart); break;
+  }
+}
+
+__global__ void k_combine_cells(int m, int64_t P, const double* __restrict__ tall,
+                                const int32_t* __restrict__ slot_of_pole, double* __restrict__ out) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < P;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int i = 0; i < m; ++i) acc += tall[(int64_t)slot_of_pole[i] * P + c];
+    out[c] = acc;
+  }
+}
+
+void launch_combine_cells(cudaStream_t st, int m, int64_t P, const double* tall,
+                          const int32_t* slot_of_pole, double* out) {
+  k_combine_cells<<<grid_for(P), 256, 0, st>>>(m, P, tall, slot_of_pole, out);
+}
+
+__global__ void k_spmv(int64_t nrows, const int64_t* __restrict__ ptr,
+                       const int32_t* __restrict__ idx, const double* __restrict__ val,
+                       const double* __restrict__ x, double alpha, double* __restrict__ y,
+                       bool accumulate) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nrows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int64_t e = ptr[r]; e < ptr[r + 1]; ++e) acc = fma(val[e], __ldg(x + idx[e]), acc);
+    y[r] = accumulate ? fma(alpha, acc, y[r]) : alpha * acc;
+  }
+}
+
+void launch_spmv(cudaStream_t st, int64_t nrows, const int64_t* ptr, const int32_t* idx,
+                 const double* val, const double* x, double alpha, double* y, bool accumulate) {
+  if (nrows <= 0) return;
+  k_spmv<<<grid_for(nrows), 256, 0, st>>>(nrows, ptr, idx, val, x, alpha, y, accumulate);
+}
+
+// ---------------------------------------------------------------------------
+// vector kernels
+// ---------------------------------------------------------------------------
+constexpr int RED_BLOCKS = 296;
+
+__global__ void k_axpby(int64_t n, double a, const double* __restrict__ x, double b,
+                        const double* __restrict__ y, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = a * x[i] + (b == 0.0 ? 0.0 : b * y[i]);
+}
+void launch_axpby(cudaStream_t st, int64_t n, double a, const double* x, double b,
+                  const double* y, double* out) {
+  if (n <= 0) return;
+  k_axpby<<<grid_for(n), 256, 0, st>>>(n, a, x, b, y, out);
+}
+
+__global__ void k_mul(int64_t n, const double* __restrict__ a, const double* __restrict__ x,
+                      double alpha, double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = alpha * (a[i] * x[i]);
+}
+void launch_mul(cudaStream_t st, int64_t n, const double* a, const double* x, double alpha,
+                double* out) {
+  if (n <= 0) return;
+  k_mul<<<grid_for(n), 256, 0, st>>>(n, a, x, alpha, out);
+}
+
+__device__ __forceinline__ double block_sum(double v) {
+  __shared__ double sh[32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) t += sh[k];
+  return t;
+}
+
+__global__ void k_dot_part(int64_t n, const double* __restrict__ x, const double* __restrict__ y,
+                           double* __restrict__ part) {
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    acc = fma(x[i], y[i], acc);
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+__global__ void k_sum_part(int nb, const double* __restrict__ part, double* __restrict__ result) {
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) acc += part[i];
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) *result = acc;
+}
+void launch_dot(cudaStream_t st, int64_t n, const double* x, const double* y, double* part,
+                double* result) {
+  k_dot_part<<<RED_BLOCKS, 256, 0, st>>>(n, x, y, part);
+  k_sum_part<<<1, 256, 0, st>>>(RED_BLOCKS, part, result);
+}
+
+// ddn += |w|^2 (old w); x += t1 w; w = v + t2 w
+__global__ void k_lsqr_xw(int64_t n, double t1, double t2, const double* __restrict__ v,
+                          double* __restrict__ w, double* __restrict__ x,
+                          double* __restrict__ part) {
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double wi = w[i];
+    acc = fma(wi, wi, acc);
+    x[i] = x[i] + t1 * wi;
+    w[i] = v[i] + t2 * wi;
+  }
+  acc = block_sum(acc);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+}
+void launch_lsqr_xw(cudaStream_t st, int64_t n, double t1, double t2, const double* v,
+                    double* w, double* x, double* part, double* result) {
+  k_lsqr_xw<<<RED_BLOCKS, 256, 0, st>>>(n, t1, t2, v, w, x, part);
+  k_sum_part<<<1, 256, 0, st>>>(RED_BLOCKS, part, result);
+}
+
+__global__ void k_zero_c(int64_t n, cplx* p) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = cmk(0.0, 0.0);
+}
+void launch_zero_c(cudaStream_t st, int64_t n, cplx* p) {
+  if (n <= 0) return;
+  k_zero_c<<<grid_for(n), 256, 0, st>>>(n, p);
+}
+
+__global__ void k_scatter_vals(int64_t nnz, const int64_t* __restrict__ tgt,
+                               const cplx* __restrict__ vals, cplx* __restrict__ fac) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nnz;
+       e += (int64_t)gridDim.x * blockDim.x)
+    fac[tgt[e]] = vals[e];
+}
+void launch_scatter_vals(cudaStream_t st, int64_t nnz, const int64_t* tgt, const cplx* vals,
+                         cplx* factor) {
+  k_scatter_vals<<<grid_for(nnz), 256, 0, st>>>(nnz, tgt, vals, factor);
+}
+
+}  // namespace rba

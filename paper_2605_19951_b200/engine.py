@@ -1,0 +1,288 @@
+"""Device engine: one `rba_ctx` (C ABI) bound to a problem and an approximant.
+
+Owns the device-resident state of the shifted-solve path -- mesh operators,
+the symbolic structure, the per-pole factorisations, pole solutions g_i and
+work vectors -- and exposes the operations the reference's modules call:
+
+* ``set_model``  -> M(m) assembly on the device (mesh.py:348-355)
+* ``factor``     -> factorize_all_poles (shifted.py:158-173)
+* ``forward``    -> solve_all_poles + response_from_pole_solutions
+                    (shifted.py:176-199, forward.py:46-75)
+* ``jvp``/``vjp``-> JacobianOperator actions (sensitivity.py:65-97)
+* ``solve``      -> cache.solve (shifted.py:107-116)
+
+Poles are sharded i -> rank (i mod G) like PoleWorkerPool (shifted.py:147-149);
+per-pole partials are exchanged with ``parallel.gather_partials`` and summed
+on every rank in ascending pole order, so results are bitwise identical for
+any GPU count.  PyTorch is used only for device allocation, streams and the
+collectives; every arithmetic step runs in libdrba.so kernels.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _lib
+from ._lib import check, ptr
+from . import parallel
+
+__all__ = ["Engine", "pattern_coords"]
+
+
+def pattern_coords(problem):
+    c = getattr(problem, "dof_coords", None)
+    if c is None:
+        return None
+    return np.ascontiguousarray(c, dtype=np.float64)
+
+
+class Engine:
+    """Device state for one (problem, approximant) pair."""
+
+    def __init__(self, problem, approx=None, device: int | None = None, leaf: int = 64,
+                 comm: parallel.PoleComm | None = None, n_slots: int | None = None):
+        self.lib = _lib.load()
+        if not torch.cuda.is_available():
+            raise RuntimeError("the B200 shifted-solve path needs a CUDA device "
+                               "(no CPU fallback)")
+        self.comm = comm or parallel.PoleComm.current()
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None
+                                   else device)
+        self.stream = torch.cuda.current_stream(self.device)
+        h = _lib.vp()
+        check(self.lib.rba_ctx_create(self.device.index, _lib.vp(self.stream.cuda_stream),
+                                      _lib.C.byref(h)))
+        self.ctx = h
+        self.problem = problem
+        self.N = int(problem.K.shape[0])
+        self.P = int(problem.cell_dofs.shape[0]) if problem.cell_dofs is not None else 0
+        K = sp.csr_matrix(problem.K)
+        K.sort_indices()
+        k = int(problem.cell_dofs.shape[1]) if self.P else 1
+        cd = np.ascontiguousarray(problem.cell_dofs, dtype=np.int32) if self.P \
+            else np.zeros((0, 1), np.int32)
+        ml = np.ascontiguousarray(problem.mass_local, dtype=np.float64) if self.P \
+            else np.zeros((0, 1, 1))
+        coords = pattern_coords(problem)
+        check(self.lib.rba_set_mesh(
+            self.ctx, self.N, self.P, k, ptr(cd), ptr(ml),
+            ptr(np.ascontiguousarray(K.indptr, dtype=np.int64)),
+            ptr(np.ascontiguousarray(K.indices, dtype=np.int32)),
+            ptr(np.ascontiguousarray(K.data, dtype=np.float64)),
+            ptr(coords), int(leaf)))
+        Q = sp.csr_matrix(problem.Q)
+        self.Mr = int(Q.shape[0])
+        check(self.lib.rba_set_observation(
+            self.ctx, self.Mr, ptr(np.ascontiguousarray(Q.indptr, dtype=np.int64)),
+            ptr(np.ascontiguousarray(Q.indices, dtype=np.int32)),
+            ptr(np.ascontiguousarray(Q.data, dtype=np.float64))))
+        F = problem.source_matrix() if hasattr(problem, "source_matrix") else \
+            np.asarray(problem.f, dtype=float)[None, :]
+        self.set_sources(F)
+        self.approx = None
+        self.model_tag = None
+        self.factored = False
+        self.g_valid = False
+        self.reg_rows = 0
+        if approx is not None:
+            self.set_poles(approx)
+        elif n_slots:
+            self._set_dummy_poles(n_slots)
+
+    # ------------------------------------------------------------------ setup
+    def set_sources(self, F):
+        F = np.ascontiguousarray(np.atleast_2d(F), dtype=np.float64)
+        if F.shape[1] != self.N:
+            raise ValueError("source vectors must have length N")
+        self.S = F.shape[0]
+        check(self.lib.rba_set_sources(self.ctx, self.S, ptr(F)))
+        self.factored = False
+
+    def set_poles(self, approx):
+        poles = np.ascontiguousarray(approx.poles, dtype=np.complex128)
+        res = np.ascontiguousarray(approx.residues, dtype=np.complex128)
+        self.m = poles.size
+        self.Kt = res.shape[1]
+        self.local = self.comm.local_poles(self.m)
+        loc = np.ascontiguousarray(self.local, dtype=np.int32)
+        check(self.lib.rba_set_poles(self.ctx, self.m, ptr(poles.view(np.float64)), self.Kt,
+                                     ptr(res.view(np.float64)), loc.size, ptr(loc)))
+        self.approx = approx
+        self.poles = poles
+        self.residues = res
+        self.factored = False
+        self.g_valid = False
+        nl = max(1, self.comm.n_max(self.m))
+        dev = self.device
+        self.qpart = torch.zeros((nl, self.S, max(self.Mr, 1)), dtype=torch.complex128, device=dev)
+        self.tpart = torch.zeros((nl, self.P), dtype=torch.float64, device=dev)
+        self.slot_of_pole = self.comm.slot_of_pole(self.m)
+
+    def _set_dummy_poles(self, n):
+        class _A:
+            pass
+        a = _A()
+        a.poles = 1j * (np.arange(n) + 1.0)
+        a.residues = np.zeros((n, 1), complex)
+        self.set_poles(a)
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.rba_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ model/factor
+    def set_model(self, m, tag: str | None = None):
+        if isinstance(m, torch.Tensor):
+            mt = m.to(self.device, torch.float64).contiguous()
+            check(self.lib.rba_set_model_d(self.ctx, ptr(mt)))
+        else:
+            mh = np.ascontiguousarray(m, dtype=np.float64)
+            if mh.size != self.P:
+                raise ValueError("model size does not match grid")
+            check(self.lib.rba_set_model(self.ctx, ptr(mh)))
+        self.model_tag = tag
+        self.factored = False
+        self.g_valid = False
+
+    def factor(self):
+        check(self.lib.rba_factor(self.ctx))
+        self.factored = True
+
+    def factor_values(self, slot: int, values: np.ndarray):
+        v = np.ascontiguousarray(values, dtype=np.complex128)
+        check(self.lib.rba_factor_values(self.ctx, int(slot), ptr(v.view(np.float64))))
+
+    def pattern(self, with_M: bool = False):
+        n = _lib.i64()
+        check(self.lib.rba_pattern(self.ctx, _lib.C.byref(n), None, None, None, None))
+        nnz = n.value
+        rows = np.empty(nnz, np.int32)
+        cols = np.empty(nnz, np.int32)
+        Kv = np.empty(nnz)
+        Mv = np.empty(nnz) if with_M else None
+        check(self.lib.rba_pattern(self.ctx, _lib.C.byref(n), ptr(rows), ptr(cols), ptr(Kv),
+                                   ptr(Mv)))
+        return rows, cols, Kv, Mv
+
+    # ------------------------------------------------------------- operators
+    def solve(self, slot: int, rhs: np.ndarray, trans: str = "N") -> np.ndarray:
+        rhs = np.asarray(rhs, dtype=np.complex128)
+        one = rhs.ndim == 1
+        B = np.ascontiguousarray(rhs.reshape(self.N, -1).T)       # (nrhs, N) = col-major N x nrhs
+        out = np.empty_like(B)
+        check(self.lib.rba_solve(self.ctx, int(slot), ptr(B.view(np.float64)),
+                                 ptr(out.view(np.float64)), B.shape[0],
+                                 1 if trans != "N" else 0))
+        return out[0] if one else out.T.copy()
+
+    def solve_d(self, slot: int, rhs: torch.Tensor, trans: str = "N") -> torch.Tensor:
+        rhs = rhs.to(self.device, torch.complex128).contiguous()
+        out = torch.empty_like(rhs)
+        nrhs = 1 if rhs.dim() == 1 else rhs.shape[0]
+        check(self.lib.rba_solve_d(self.ctx, int(slot), ptr(rhs), ptr(out), nrhs,
+                                   1 if trans != "N" else 0))
+        return out
+
+    def download_g(self, slot: int) -> np.ndarray:
+        """g of a local slot as (N, S) complex in the original dof order."""
+        out = np.empty((self.S, self.N), dtype=np.complex128)
+        check(self.lib.rba_get_g(self.ctx, int(slot), ptr(out.view(np.float64))))
+        return out.T.copy()
+
+    def _gather(self, part):
+        return self.comm.gather_partials(part)
+
+    def forward(self) -> torch.Tensor:
+        """Predicted data d (S*K_t*M_r,) on the device; stores g_i."""
+        check(self.lib.rba_forward_partial(self.ctx, ptr(self.qpart)))
+        self.g_valid = True
+        qall = self._gather(self.qpart)
+        d = torch.empty(self.S * self.Kt * self.Mr, dtype=torch.float64, device=self.device)
+        check(self.lib.rba_combine_data(self.ctx, ptr(qall), ptr(self.slot_of_pole), 0, ptr(d)))
+        return d
+
+    def jvp(self, v: torch.Tensor) -> torch.Tensor:
+        v = v.to(self.device, torch.float64).contiguous()
+        check(self.lib.rba_jvp_partial(self.ctx, ptr(v), ptr(self.qpart)))
+        qall = self._gather(self.qpart)
+        d = torch.empty(self.S * self.Kt * self.Mr, dtype=torch.float64, device=self.device)
+        check(self.lib.rba_combine_data(self.ctx, ptr(qall), ptr(self.slot_of_pole), 1, ptr(d)))
+        return d
+
+    def vjp(self, w: torch.Tensor) -> torch.Tensor:
+        w = w.to(self.device, torch.float64).contiguous()
+        check(self.lib.rba_vjp_partial(self.ctx, ptr(w), ptr(self.tpart)))
+        tall = self._gather(self.tpart)
+        out = torch.empty(self.P, dtype=torch.float64, device=self.device)
+        check(self.lib.rba_combine_cells(self.ctx, ptr(tall), ptr(self.slot_of_pole), ptr(out)))
+        return out
+
+    # ------------------------------------------------------------ regulariser
+    def set_reg(self, R: sp.spmatrix):
+        R = sp.csr_matrix(R)
+        R.sort_indices()
+        if R.shape[1] != self.P:
+            raise ValueError("regulariser must have P columns")
+        self.reg_rows = R.shape[0]
+        check(self.lib.rba_set_reg(self.ctx, R.shape[0],
+                                   ptr(np.ascontiguousarray(R.indptr, dtype=np.int64)),
+                                   ptr(np.ascontiguousarray(R.indices, dtype=np.int32)),
+                                   ptr(np.ascontiguousarray(R.data, dtype=np.float64))))
+
+    def reg_apply(self, x: torch.Tensor, out: torch.Tensor, alpha=1.0, transpose=False,
+                  accumulate=False):
+        check(self.lib.rba_reg_apply(self.ctx, 1 if transpose else 0, ptr(x), float(alpha),
+                                     ptr(out), 1 if accumulate else 0))
+        return out
+
+    # ------------------------------------------------------------ vectors
+    def axpby(self, a, x, b, y, out):
+        check(self.lib.rba_vec_axpby(self.ctx, out.numel(), float(a), ptr(x), float(b),
+                                     ptr(y if y is not None else x), ptr(out)))
+        return out
+
+    def mul(self, a, x, out, alpha=1.0):
+        check(self.lib.rba_vec_mul(self.ctx, out.numel(), ptr(a), ptr(x), float(alpha), ptr(out)))
+        return out
+
+    def dot(self, x, y) -> float:
+        r = _lib.f64()
+        check(self.lib.rba_vec_dot(self.ctx, x.numel(), ptr(x), ptr(y), _lib.C.byref(r)))
+        return r.value
+
+    def lsqr_xw(self, t1, t2, v, w, x) -> float:
+        r = _lib.f64()
+        check(self.lib.rba_vec_lsqr_xw(self.ctx, x.numel(), float(t1), float(t2), ptr(v), ptr(w),
+                                       ptr(x), _lib.C.byref(r)))
+        return r.value
+
+    # ------------------------------------------------------------ info
+    def info(self) -> dict:
+        out = np.zeros(8, np.int64)
+        check(self.lib.rba_info(self.ctx, ptr(out)))
+        mem = np.zeros(3, np.int64)
+        check(self.lib.rba_memory(self.ctx, ptr(mem)))
+        return dict(factorizations=int(out[0]), solves=int(out[1]), N=int(out[2]),
+                    P=int(out[3]), Mr=int(out[4]), S=int(out[5]), m=int(out[6]),
+                    n_local=int(out[7]), mem_factor=int(mem[0]), mem_work=int(mem[1]),
+                    mem_other=int(mem[2]))
+
+    def set_timing(self, on: bool):
+        check(self.lib.rba_set_timing(self.ctx, 1 if on else 0))
+
+    def timings(self) -> np.ndarray:
+        out = np.zeros(8)
+        check(self.lib.rba_timings(self.ctx, ptr(out)))
+        return out
+
+    def sync(self):
+        check(self.lib.rba_sync(self.ctx))

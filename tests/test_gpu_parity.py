@@ -1,0 +1,168 @@
+"""GPU parity: the device path (libdrba.so through the C ABI) against golden
+vectors from the unmodified reference and against the CPU oracle.
+
+Tolerances (BASELINE north_star): forward data <= 1e-9, J v / J^T w <= 1e-8
+relative; GN update dm judged against the reference's own solver-to-solver
+floor: <= 1e-8 where that floor is below 1e-10 (<= 5 LSQR
+iterations), else within 10x of the floor measured here on the same inputs.
+"""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import scipy.sparse.linalg as spla
+
+from conftest import golden, rel
+import paper_2605_19951_b200 as rb
+from oracle import rbainv_oracle as orc
+
+pytestmark = pytest.mark.gpu
+
+
+def _model(prob, m):
+    return rb.Model(np.asarray(m, dtype=float), np.asarray(m, dtype=float))
+
+
+def _data(z):
+    return rb.DataSet(d_obs=z["d_obs"], sigma_d=z["sigma_d"], times=np.zeros(1),
+                      receivers=np.zeros((1, 3)), eps_r=0.0, eps_a=1.0, seed=0, provenance={})
+
+
+@pytest.mark.parametrize("fname,name", [("ref3d_n6.npz", "C1"), ("ref3d_c3_n6.npz", "C3")])
+def test_forward_jvp_vjp_vs_reference(gpu, fname, name):
+    z = golden(fname)
+    prob, _ = rb.build_config(name, n=int(z["n"]))
+    approx = rb.config_approximant(name)
+    model = _model(prob, z["m"])
+    cache = rb.ShiftedFactorCache()
+    d = rb.forward_response(prob, model, approx, cache).data
+    assert rel(d, z["d"]) <= 1e-9
+    opr = rb.JacobianOperator(prob, model, approx, cache)
+    assert rel(opr.jvp(z["v"]), z["jv"]) <= 1e-8
+    assert rel(opr.vjp(z["w"]), z["jtw"]) <= 1e-8
+    assert rb.adjoint_test(opr, trials=3, seed=4) <= 1e-8
+
+
+def test_gn_update_vs_reference_n6(gpu):
+    z = golden("ref3d_n6.npz")
+    prob, _ = rb.build_config("C1", n=6)
+    approx = rb.config_approximant("C1")
+    model = _model(prob, z["m"])
+    cache = rb.ShiftedFactorCache()
+    reg = rb.build_reg(prob.grid, root="chol")
+    opr = rb.JacobianOperator(prob, model, approx, cache)
+    data = _data(z)
+    from paper_2605_19951_b200.inversion import _augmented_lsqr
+    for k in (1, 3, 5):
+        dm, itn, _ = _augmented_lsqr(opr, reg, data, z["d"], model, float(z["lam"]),
+                                     rb.LsqrConfig(tol=0.0, max_iters=k))
+        assert itn == int(z[f"itn_{k}"])
+        assert rel(dm, z[f"dm_{k}"]) <= 1e-8, k
+
+
+def test_c1_full_size_vs_reference(gpu):
+    """BASELINE config 1 at full size (n=16, N=26,416, 8 poles)."""
+    z = golden("ref3d_C1.npz")
+    prob, _ = rb.build_config("C1", n=16)
+    approx = rb.config_approximant("C1")
+    model = _model(prob, z["m"])
+    cache = rb.ShiftedFactorCache()
+    d = rb.forward_response(prob, model, approx, cache).data
+    assert rel(d, z["d"]) <= 1e-9
+    opr = rb.JacobianOperator(prob, model, approx, cache)
+    assert rel(opr.jvp(z["v"]), z["jv"]) <= 1e-8
+    assert rel(opr.vjp(z["w"]), z["jtw"]) <= 1e-8
+    reg = rb.build_reg(prob.grid, root="chol")
+    from paper_2605_19951_b200.inversion import _augmented_lsqr
+    dm, itn, _ = _augmented_lsqr(opr, reg, _data(z), z["d"], model, float(z["lam"]),
+                                 rb.LsqrConfig(tol=0.0, max_iters=5))
+    assert itn == 5
+    # reference floor at C1 is 9.5e-10 after 5 iterations
+    assert rel(dm, z["dm_5"]) <= 1e-8
+
+
+def test_solves_vs_splu_and_transpose(gpu):
+    prob, _ = rb.build_config("C1", n=8)
+    approx = rb.config_approximant("C1")
+    model = prob.true_model()
+    cache = rb.ShiftedFactorCache()
+    rb.factorize_all_poles(prob, model, approx, cache)
+    M = orc.assemble_M(prob, model.m)
+    rng = np.random.default_rng(5)
+    b = rng.standard_normal(prob.dof_count) + 1j * rng.standard_normal(prob.dof_count)
+    for i in (0, 3, 7):
+        A = (prob.K.astype(complex) - approx.poles[i] * M.astype(complex)).tocsc()
+        x = cache.solve(i, b)
+        xt = cache.solve(i, b, trans="T")
+        assert np.linalg.norm(A @ x - b) / np.linalg.norm(b) <= 1e-8
+        assert rel(x, spla.splu(A).solve(b)) <= 1e-8
+        np.testing.assert_array_equal(x, xt)
+        # repeat solves are bitwise identical (deterministic kernels)
+        np.testing.assert_array_equal(x, cache.solve(i, b))
+        # multi-RHS solve agrees column by column
+        B = np.stack([b, b.conj(), 2 * b], axis=1)
+        X = cache.solve(i, B)
+        assert rel(X[:, 0], x) <= 1e-14 and rel(X[:, 2], 2 * x) <= 1e-14
+
+
+def test_counters_and_cache_semantics(gpu):
+    prob, _ = rb.build_config("C1", n=4)
+    approx = rb.config_approximant("C1")
+    model = prob.reference_model()
+    cache = rb.ShiftedFactorCache()
+    m = approx.pole_count
+    rb.solve_all_poles(prob, model, approx, prob.f, cache)
+    assert cache.counters.factorizations == m and cache.counters.solves == m
+    rb.solve_all_poles(prob, model, approx, prob.f, cache)
+    assert cache.counters.factorizations == m
+    opr = rb.JacobianOperator(prob, model, approx, cache)
+    s0 = cache.counters.solves
+    opr.jvp(np.ones(opr.shape[1]))
+    assert cache.counters.solves - s0 == m
+    opr.vjp(np.ones(opr.shape[0]))
+    assert cache.counters.solves - s0 == 2 * m
+    cache.activate("someone-else")
+    with pytest.raises(RuntimeError):
+        opr.jvp(np.ones(opr.shape[1]))
+    with pytest.raises(rb.CacheMissError):
+        cache.solve(0, np.zeros(prob.dof_count, complex))
+
+
+def test_generic_cache_with_reference_2d_problem(gpu):
+    """Generic mode: factorize(i, A) with assembled SciPy matrices of the
+    reference's 2-D fixture; solutions vs the reference's own g."""
+    z = golden("ref2d_small.npz")
+    N = z["K_indptr"].size - 1
+    K = sp.csr_matrix((z["K_data"], z["K_indices"], z["K_indptr"]), shape=(N, N))
+
+    class P:
+        pass
+    p = P()
+    p.K, p.cell_dofs, p.mass_local, p._scatter = K, z["cell_dofs"], z["mass_local"], None
+    M = orc.assemble_M(p, z["m"]).astype(complex)
+    cache = rb.ShiftedFactorCache()
+    cache.activate("tag")
+    for i, xi in enumerate(z["poles"]):
+        cache.factorize(i, (K.astype(complex) - xi * M).tocsc())
+    g = np.array([cache.solve(i, z["f"]) for i in range(z["poles"].size)])
+    assert rel(g, z["g"][:, :, 0]) <= 1e-10
+    assert cache.counters.factorizations == z["poles"].size
+
+
+def test_scalar_shifted_inverse_kat(gpu):
+    """test_shifted.py:26-36: one dof, A = k - xi mu."""
+    k, mu = 2.0, 2.0 / 3.0
+    cache = rb.ShiftedFactorCache()
+    cache.activate("t")
+    for i, xi in enumerate([0.5 + 1.5j, -2.0 + 3.0j]):
+        cache.factorize(i, sp.csr_matrix(np.array([[k - xi * mu]])))
+        g = cache.solve(i, np.array([1.0]))
+        assert abs(g[0] - 1.0 / (k - xi * mu)) <= 1e-14 * abs(1.0 / (k - xi * mu))
+
+
+def test_singular_shift_raises(gpu):
+    """test_shifted.py:170-177: an exactly singular shift -> SolveError."""
+    cache = rb.ShiftedFactorCache()
+    cache.activate("t")
+    with pytest.raises(rb.SolveError):
+        cache.factorize(0, sp.csr_matrix(np.array([[0.0 + 0.0j]])))
