@@ -60,6 +60,13 @@ int rba_symbolic_stats(const rba_symbolic* s, int64_t* istats_h, double* dstats_
 int rba_symbolic_array(const rba_symbolic* s, const char* name, void* out_h,
                        int64_t capacity_bytes, int64_t* nbytes);
 void rba_symbolic_destroy(rba_symbolic* s);
+/* Host-only dry run of rba_set_mesh's preparation (pattern, symbolic,
+ * scatter plan) for validation without a GPU.  out[4]: nnz(lower A),
+ * M contributions, fronts, panel entries. */
+int rba_mesh_prepare(int64_t N, int64_t P, int32_t k, const int32_t* cell_dofs_h,
+                     const double* mass_local_h, const int64_t* K_indptr_h,
+                     const int32_t* K_indices_h, const double* K_data_h, const double* coords_h,
+                     int32_t leaf, int64_t* out_h);
 
 /* ---- context ------------------------------------------------------------ */
 int rba_ctx_create(int device, void* cuda_stream, rba_ctx** out);
@@ -112,6 +119,10 @@ int rba_vjp_partial(rba_ctx* ctx, const double* w_d, double* tpart_d);
 /* g_i of local slot `slot` after rba_forward_partial: column-major N x S
  * complex, original dof order (ForwardResult fields / pole_solutions). */
 int rba_get_g(rba_ctx* ctx, int32_t slot, double* out_h);
+/* Copy the factor storage of a local slot (panel_total complex entries;
+ * per-front nf x npiv column-major panels at symbolic panel_off) -- used by
+ * the structure-level parity tests against the host emulation. */
+int rba_get_factor(rba_ctx* ctx, int32_t slot, double* out_h, int64_t count);
 /* Ordered pole sums (forward.py:61-63; sensitivity.py:77-78,95-96):
  *   data: d[s][j][r] = sum_i 2 Re(alpha_ij q_i [* xi_i])  (times_pole = 1 for J v)
  *   cells: out[c] = sum_i t_i[c]

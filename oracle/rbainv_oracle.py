@@ -78,7 +78,8 @@ class PoleFactors:
     """shifted.py:44-122: SuperLU factor per pole of A_i = K - xi_i M(m),
     keyed by the model tag; counters as CacheCounters (shifted.py:64-70)."""
 
-    def __init__(self):
+    def __init__(self, permc_spec: str = "COLAMD"):
+        self.permc_spec = permc_spec     # SuperLU ordering (reference default: COLAMD)
         self.tag = None
         self.lu = {}
         self.A = {}
@@ -107,7 +108,7 @@ def factorize_all_poles(problem, m, poles, fac: PoleFactors):
     for i in missing:
         A = K - poles[i] * M
         try:
-            fac.lu[i] = spla.splu(A.tocsc())
+            fac.lu[i] = spla.splu(A.tocsc(), permc_spec=fac.permc_spec)
         except Exception as exc:  # shifted.py:55-56
             raise RuntimeError(f"factorization of shifted matrix failed: {exc}") from exc
         fac.A[i] = A.tocsr()
@@ -296,6 +297,20 @@ def gn_step(problem, m, m_ref, poles, residues, R, weights, d_obs, lam, tol, max
     dm, itn, istop = augmented_lsqr(opr, R, weights, d_obs, d_pred, m, m_ref, lam,
                                     tol, max_iters)
     return dm, itn, istop, d_pred
+
+
+def lsqr_floor(problem, m, poles, residues, R, weights, d_obs, lam, iters, orderings=(
+        "COLAMD", "MMD_AT_PLUS_A")):
+    """The reference's own solver-to-solver floor on the GN update:
+    relative difference of dm computed with two SuperLU orderings."""
+    out = []
+    for spec in orderings:
+        fac = PoleFactors(spec)
+        d, g = forward_response(problem, m, poles, residues, fac)
+        J = Jacobian(problem, m, poles, residues, fac, g=g)
+        dm, _, _ = augmented_lsqr(J, R, weights, d_obs, d, m, m, lam, 0.0, iters)
+        out.append(dm)
+    return float(np.linalg.norm(out[0] - out[1]) / np.linalg.norm(out[0])), out[0]
 
 
 def make_dataset(d_clean, eps_r, eps_a=None, seed=0):

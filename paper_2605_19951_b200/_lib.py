@@ -37,6 +37,7 @@ _SIGS = {
     "rba_symbolic_stats": (C.c_int, [vp, vp, vp]),
     "rba_symbolic_array": (C.c_int, [vp, C.c_char_p, vp, i64, C.POINTER(i64)]),
     "rba_symbolic_destroy": (None, [vp]),
+    "rba_mesh_prepare": (C.c_int, [i64, i64, i32, vp, vp, vp, vp, vp, vp, i32, vp]),
     "rba_ctx_create": (C.c_int, [C.c_int, vp, C.POINTER(vp)]),
     "rba_ctx_destroy": (None, [vp]),
     "rba_set_mesh": (C.c_int, [vp, i64, i64, i32, vp, vp, vp, vp, vp, vp, i32]),
@@ -52,6 +53,7 @@ _SIGS = {
     "rba_solve_d": (C.c_int, [vp, i32, vp, vp, i32, i32]),
     "rba_forward_partial": (C.c_int, [vp, vp]),
     "rba_get_g": (C.c_int, [vp, i32, vp]),
+    "rba_get_factor": (C.c_int, [vp, i32, vp, i64]),
     "rba_jvp_partial": (C.c_int, [vp, vp, vp]),
     "rba_vjp_partial": (C.c_int, [vp, vp, vp]),
     "rba_combine_data": (C.c_int, [vp, vp, vp, i32, vp]),

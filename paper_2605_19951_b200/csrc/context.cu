@@ -11,6 +11,7 @@
 
 #include "../../include/rba_b200.h"
 #include "kernels.h"
+#include "mesh_prep.h"
 #include "symbolic.h"
 
 using rba::cplx;
@@ -497,6 +498,23 @@ int rba_symbolic_array(const rba_symbolic* s, const char* name, void* out, int64
 
 void rba_symbolic_destroy(rba_symbolic* s) { delete s; }
 
+int rba_mesh_prepare(int64_t N, int64_t P, int32_t k, const int32_t* cell_dofs,
+                     const double* mass_local, const int64_t* Kp, const int32_t* Ki,
+                     const double* Kx, const double* coords, int32_t leaf, int64_t* out) {
+  if (!Kp || !Ki || !Kx || (P > 0 && (!cell_dofs || !mass_local)))
+    return fail(RBA_ERR_INVALID, "null argument");
+  rba::MeshPrep MP;
+  std::string err = rba::prepare_mesh(N, P, k, cell_dofs, mass_local, Kp, Ki, Kx, coords, leaf, MP);
+  if (!err.empty()) return fail(RBA_ERR_INVALID, err);
+  if (out) {
+    out[0] = MP.nnzA;
+    out[1] = (int64_t)MP.moff.size();
+    out[2] = MP.sym.nfront;
+    out[3] = MP.sym.panel_off[MP.sym.nfront];
+  }
+  return RBA_OK;
+}
+
 int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   if (!out) return fail(RBA_ERR_INVALID, "null out");
   int ndev = 0;
@@ -548,135 +566,24 @@ int rba_set_mesh(rba_ctx* c, int64_t N, int64_t P, int32_t k, const int32_t* cel
   if (c->have_mesh) return fail(RBA_ERR_STATE, "mesh already set on this context");
   CK(cudaSetDevice(c->device));
   c->N = N; c->P = P; c->k = k;
-  // dof -> (cell, slot) lists
-  std::vector<int64_t> dcp(N + 1, 0);
-  for (int64_t i = 0; i < P * k; ++i) {
-    int32_t d = cell_dofs[i];
-    if (d >= N) return fail(RBA_ERR_INVALID, "cell_dofs entry out of range");
-    if (d >= 0) dcp[d + 1]++;
-  }
-  for (int64_t i = 0; i < N; ++i) dcp[i + 1] += dcp[i];
-  std::vector<int32_t> dci(dcp[N]);
+  rba::MeshPrep MP;
   {
-    std::vector<int64_t> pos(dcp.begin(), dcp.end() - 1);
-    for (int64_t cidx = 0; cidx < P; ++cidx)
-      for (int a = 0; a < k; ++a) {
-        int32_t d = cell_dofs[cidx * k + a];
-        if (d >= 0) dci[pos[d]++] = (int32_t)(cidx * 6 + a);
-      }
+    std::string err = rba::prepare_mesh(N, P, k, cell_dofs, mass_local, Kp, Ki, Kx, coords, leaf, MP);
+    if (!err.empty()) return fail(RBA_ERR_INVALID, err);
   }
-  // full symmetric pattern: element pattern U K pattern
-  std::vector<int64_t> ap(N + 1, 0);
-  std::vector<int32_t> ai;
-  {
-    std::vector<int32_t> mark(N, -1), row;
-    ai.reserve((size_t)dcp[N] * k);
-    for (int64_t r = 0; r < N; ++r) {
-      row.clear();
-      for (int64_t q = dcp[r]; q < dcp[r + 1]; ++q) {
-        int64_t cidx = dci[q] / 6;
-        for (int b = 0; b < k; ++b) {
-          int32_t cc = cell_dofs[cidx * k + b];
-          if (cc >= 0 && mark[cc] != r) { mark[cc] = (int32_t)r; row.push_back(cc); }
-        }
-      }
-      for (int64_t e = Kp[r]; e < Kp[r + 1]; ++e) {
-        int32_t cc = Ki[e];
-        if (cc < 0 || cc >= N) return fail(RBA_ERR_INVALID, "K index out of range");
-        if (mark[cc] != r) { mark[cc] = (int32_t)r; row.push_back(cc); }
-      }
-      if (mark[r] != r) { mark[r] = (int32_t)r; row.push_back((int32_t)r); }
-      std::sort(row.begin(), row.end());
-      ai.insert(ai.end(), row.begin(), row.end());
-      ap[r + 1] = ai.size();
-    }
-  }
-  // lower triangle (row >= col), K values, M contribution lists
-  std::vector<int64_t> lp(N + 1, 0);
-  c->a_rows.clear(); c->a_cols.clear(); c->Kv_h.clear();
-  for (int64_t r = 0; r < N; ++r) {
-    for (int64_t e = ap[r]; e < ap[r + 1]; ++e) {
-      int32_t cc = ai[e];
-      if (cc > r) break;
-      c->a_rows.push_back((int32_t)r);
-      c->a_cols.push_back(cc);
-    }
-    lp[r + 1] = c->a_rows.size();
-  }
-  c->nnzA = c->a_rows.size();
-  c->Kv_h.assign(c->nnzA, 0.0);
-  for (int64_t r = 0; r < N; ++r)
-    for (int64_t e = Kp[r]; e < Kp[r + 1]; ++e) {
-      int32_t cc = Ki[e];
-      if (cc > r) continue;
-      const int32_t* b0 = c->a_cols.data() + lp[r];
-      const int32_t* b1 = c->a_cols.data() + lp[r + 1];
-      const int32_t* it = std::lower_bound(b0, b1, cc);
-      c->Kv_h[lp[r] + (it - b0)] += Kx[e];
-    }
-  std::vector<int64_t> mcnt(c->nnzA + 1, 0);
-  std::vector<int64_t> me;  // (e, off) pairs flattened
-  me.reserve((size_t)P * k * (k + 1));
-  for (int64_t cidx = 0; cidx < P; ++cidx)
-    for (int a = 0; a < k; ++a) {
-      int32_t r = cell_dofs[cidx * k + a];
-      if (r < 0) continue;
-      for (int b = 0; b < k; ++b) {
-        int32_t cc = cell_dofs[cidx * k + b];
-        if (cc < 0 || cc > r) continue;
-        const int32_t* b0 = c->a_cols.data() + lp[r];
-        const int32_t* b1 = c->a_cols.data() + lp[r + 1];
-        int64_t e = lp[r] + (std::lower_bound(b0, b1, cc) - b0);
-        me.push_back(e);
-        me.push_back(cidx * 36 + a * 6 + b);
-        mcnt[e + 1]++;
-      }
-    }
-  for (int64_t e = 0; e < c->nnzA; ++e) mcnt[e + 1] += mcnt[e];
-  std::vector<int64_t> moff(mcnt[c->nnzA]);
-  {
-    std::vector<int64_t> pos(mcnt.begin(), mcnt.end() - 1);
-    for (size_t q = 0; q < me.size(); q += 2) moff[pos[me[q]]++] = me[q + 1];
-  }
-  std::vector<int64_t>().swap(me);
-  // symbolic analysis
-  std::string err = rba::analyze(N, ap.data(), ai.data(), coords, leaf > 0 ? leaf : 64, c->sym);
-  if (!err.empty()) return fail(RBA_ERR_INVALID, "symbolic analysis: " + err);
+  c->sym = std::move(MP.sym);
+  c->a_rows = std::move(MP.a_rows);
+  c->a_cols = std::move(MP.a_cols);
+  c->Kv_h = std::move(MP.Kv);
+  c->nnzA = MP.nnzA;
   const rba::Symbolic& S = c->sym;
-  // scatter targets of A entries into the front panels
-  std::vector<int32_t> front_of(N);
-  for (int s = 0; s < S.nfront; ++s)
-    for (int q = 0; q < S.npiv[s]; ++q) front_of[S.first[s] + q] = s;
-  std::vector<int64_t> tgt(c->nnzA);
-  for (int64_t e = 0; e < c->nnzA; ++e) {
-    int32_t pr = S.iperm[c->a_rows[e]], pc = S.iperm[c->a_cols[e]];
-    int32_t hi = std::max(pr, pc), lo = std::min(pr, pc);
-    int s = front_of[lo];
-    const int32_t* rb = S.rows.data() + S.rows_off[s];
-    const int32_t* it = std::lower_bound(rb, rb + S.nf[s], hi);
-    if (it == rb + S.nf[s] || *it != hi) return fail(RBA_ERR_INVALID, "internal: A entry outside front");
-    tgt[e] = S.panel_off[s] + (int64_t)(lo - S.first[s]) * S.nf[s] + (it - rb);
-  }
-  // permuted element data
-  std::vector<int32_t> cdp((size_t)P * 6, -1);
-  std::vector<double> mass36((size_t)P * 36, 0.0);
-  for (int64_t cidx = 0; cidx < P; ++cidx)
-    for (int a = 0; a < k; ++a) {
-      int32_t d = cell_dofs[cidx * k + a];
-      cdp[cidx * 6 + a] = d >= 0 ? S.iperm[d] : -1;
-      for (int b = 0; b < k; ++b) mass36[cidx * 36 + a * 6 + b] = mass_local[(cidx * k + a) * k + b];
-    }
-  // dof lists re-indexed by permuted dof, element mass offsets rebased to 36
-  std::vector<int64_t> pdcp(N + 1, 0);
-  std::vector<int32_t> pdci(dci.size());
-  for (int64_t kk = 0; kk < N; ++kk) {
-    int32_t o = S.perm[kk];
-    pdcp[kk + 1] = pdcp[kk] + (dcp[o + 1] - dcp[o]);
-  }
-  for (int64_t kk = 0; kk < N; ++kk) {
-    int32_t o = S.perm[kk];
-    std::copy(dci.begin() + dcp[o], dci.begin() + dcp[o + 1], pdci.begin() + pdcp[kk]);
-  }
+  std::vector<int64_t>& tgt = MP.tgt;
+  std::vector<int64_t>& mcnt = MP.mcnt;
+  std::vector<int64_t>& moff = MP.moff;
+  std::vector<int32_t>& cdp = MP.cdp;
+  std::vector<double>& mass36 = MP.mass36;
+  std::vector<int64_t>& pdcp = MP.pdcp;
+  std::vector<int32_t>& pdci = MP.pdci;
   // uploads
   int rc;
   auto up32 = [&](int32_t** d, const std::vector<int32_t>& v) { return upload(c, c->allocs, d, v.data(), v.size()); };
@@ -1097,6 +1004,16 @@ int rba_get_g(rba_ctx* c, int32_t slot, double* out_h) {
   rba::launch_perm_out(c->st, c->N, c->S, c->NRs, c->perm_d, c->g[slot], c->stage, c->N);
   CKL();
   CK(cudaMemcpyAsync(out_h, c->stage, n * sizeof(cplx), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return RBA_OK;
+}
+
+int rba_get_factor(rba_ctx* c, int32_t slot, double* out_h, int64_t count) {
+  if (!c || !out_h || slot < 0 || slot >= (int)c->local.size()) return fail(RBA_ERR_INVALID, "bad slot");
+  const int64_t tot = c->sym.panel_off[c->sym.nfront];
+  if (count < tot) return fail(RBA_ERR_INVALID, "buffer too small");
+  CK(cudaSetDevice(c->device));
+  CK(cudaMemcpyAsync(out_h, c->factor[slot], tot * sizeof(cplx), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   return RBA_OK;
 }

@@ -66,18 +66,18 @@ class Engine:
         ml = np.ascontiguousarray(problem.mass_local, dtype=np.float64) if self.P \
             else np.zeros((0, 1, 1))
         coords = pattern_coords(problem)
-        check(self.lib.rba_set_mesh(
-            self.ctx, self.N, self.P, k, ptr(cd), ptr(ml),
-            ptr(np.ascontiguousarray(K.indptr, dtype=np.int64)),
-            ptr(np.ascontiguousarray(K.indices, dtype=np.int32)),
-            ptr(np.ascontiguousarray(K.data, dtype=np.float64)),
-            ptr(coords), int(leaf)))
+        # keep every converted array referenced until the call returns
+        kp = np.ascontiguousarray(K.indptr, dtype=np.int64)
+        ki = np.ascontiguousarray(K.indices, dtype=np.int32)
+        kx = np.ascontiguousarray(K.data, dtype=np.float64)
+        check(self.lib.rba_set_mesh(self.ctx, self.N, self.P, k, ptr(cd), ptr(ml), ptr(kp),
+                                    ptr(ki), ptr(kx), ptr(coords), int(leaf)))
         Q = sp.csr_matrix(problem.Q)
         self.Mr = int(Q.shape[0])
-        check(self.lib.rba_set_observation(
-            self.ctx, self.Mr, ptr(np.ascontiguousarray(Q.indptr, dtype=np.int64)),
-            ptr(np.ascontiguousarray(Q.indices, dtype=np.int32)),
-            ptr(np.ascontiguousarray(Q.data, dtype=np.float64))))
+        qp = np.ascontiguousarray(Q.indptr, dtype=np.int64)
+        qi = np.ascontiguousarray(Q.indices, dtype=np.int32)
+        qx = np.ascontiguousarray(Q.data, dtype=np.float64)
+        check(self.lib.rba_set_observation(self.ctx, self.Mr, ptr(qp), ptr(qi), ptr(qx)))
         F = problem.source_matrix() if hasattr(problem, "source_matrix") else \
             np.asarray(problem.f, dtype=float)[None, :]
         self.set_sources(F)
@@ -233,10 +233,10 @@ class Engine:
         if R.shape[1] != self.P:
             raise ValueError("regulariser must have P columns")
         self.reg_rows = R.shape[0]
-        check(self.lib.rba_set_reg(self.ctx, R.shape[0],
-                                   ptr(np.ascontiguousarray(R.indptr, dtype=np.int64)),
-                                   ptr(np.ascontiguousarray(R.indices, dtype=np.int32)),
-                                   ptr(np.ascontiguousarray(R.data, dtype=np.float64))))
+        rp = np.ascontiguousarray(R.indptr, dtype=np.int64)
+        ri = np.ascontiguousarray(R.indices, dtype=np.int32)
+        rx = np.ascontiguousarray(R.data, dtype=np.float64)
+        check(self.lib.rba_set_reg(self.ctx, R.shape[0], ptr(rp), ptr(ri), ptr(rx)))
 
     def reg_apply(self, x: torch.Tensor, out: torch.Tensor, alpha=1.0, transpose=False,
                   accumulate=False):

@@ -190,6 +190,8 @@ def _values_on_pattern(A: sp.csr_matrix, rows: np.ndarray, cols: np.ndarray) -> 
     A.sum_duplicates()
     n = A.shape[0]
     coo = A.tocoo()
+    if coo.nnz == 0:
+        return np.zeros(rows.size, dtype=complex)
     keys = coo.row.astype(np.int64) * n + coo.col
     order = np.argsort(keys)
     sk = keys[order]

@@ -77,3 +77,28 @@ def test_flop_and_fill_stats_c1():
     assert 5.0e6 < st[3] < 7.5e6
     assert 0.8e10 < S["flops"] < 1.4e10
     assert st[7] == 1096
+
+
+@pytest.mark.parametrize("name,n", [("C1", 6), ("C3", 6)])
+def test_mesh_prepare_dry_run(name, n):
+    """rba_set_mesh's host preparation (pattern, symbolic, scatter plan) runs
+    without a GPU; every lower entry of A must land in a front panel."""
+    from paper_2605_19951_b200 import _lib
+    from paper_2605_19951_b200._lib import ptr
+    lib = _lib.load()
+    prob, _ = rb.build_config(name, n=n)
+    K = sp.csr_matrix(prob.K)
+    K.sort_indices()
+    cd = np.ascontiguousarray(prob.cell_dofs, dtype=np.int32)
+    ml = np.ascontiguousarray(prob.mass_local)
+    kp = np.ascontiguousarray(K.indptr, dtype=np.int64)
+    ki = np.ascontiguousarray(K.indices, dtype=np.int32)
+    kx = np.ascontiguousarray(K.data)
+    co = np.ascontiguousarray(prob.dof_coords)
+    out = np.zeros(4, np.int64)
+    _lib.check(lib.rba_mesh_prepare(K.shape[0], prob.grid.cell_count, 6, ptr(cd), ptr(ml),
+                                    ptr(kp), ptr(ki), ptr(kx), ptr(co), 64, ptr(out)))
+    assert out[0] == (K.nnz + K.shape[0]) // 2
+    # every cell contributes its 21 lower (a, b) pairs with both dofs interior
+    assert out[1] == sum(int(((r >= 0)[:, None] & (r >= 0)[None, :] &
+                              (r[:, None] >= r[None, :])).sum()) for r in prob.cell_dofs)
