@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""Benchmark of the BASELINE metric: one Gauss-Newton iteration of the
+shifted-solve inversion (C4: 46^3-hex Nedelec box, N = 662,446 edge dofs,
+16 poles, 4 sources x 100 receivers x 31 times, 30 LSQR iterations, RT0
+regularisation lambda = 1e-2), plus its components (J v / J^T w per second,
+factor FP64 TFLOP/s, solve GB/s).
+
+A "step" is one GN iteration of `run_inversion` (inversion.py:240-300):
+operator at the current model, gradient (one J^T w), LSQR (30 x (J v + J^T w)),
+Armijo line search (each trial = 16 refactorisations + forward solves).
+
+Usage (contract): python bench.py [--gpus N] [--steps K] [--warmup W]
+                  [--impl ours|reference] [--config C4] [--n 46]
+For N > 1 launch with torchrun; poles are sharded i -> rank (i mod N).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GN-iteration s & J·v/Jᵀ·w per s at ~700k DOF; factor FP64 TFLOP/s; solve GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--n", type=int, default=None, help="override the mesh size (debug)")
+    ap.add_argument("--lsqr", type=int, default=None)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--profile-once", action="store_true",
+                    help="one factorisation + one forward only (for ncu captures)")
+    return ap.parse_args()
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    elif torch.cuda.is_available():
+        torch.cuda.set_device(0)
+    return world, rank
+
+
+class Clocks:
+    """nvidia-smi sampled during the timed region (B200_PROFILING recipe)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        dev = os.environ.get("LOCAL_RANK", "0")
+        rows = [r for r in rows if r[0].strip() == dev] or rows
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            for k, name in enumerate(names):
+                if len(r) > 5 + k and "Active" in r[5 + k] and "Not" not in r[5 + k]:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def measured_peaks():
+    peaks = {}
+    try:
+        peaks.update(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))))
+    except OSError:
+        peaks["hbm_gbs"] = 6650.0
+        peaks["_hbm_source"] = "fallback (B200_PROFILING.md)"
+    try:
+        fp = json.load(open(os.path.join(ROOT, "profiles", "fp64_peak_r01.json")))
+        peaks["fp64_tflops"] = fp["dmma_tflops"]
+    except OSError:
+        peaks["fp64_tflops"] = 37.0
+    return peaks
+
+
+def build_workload(name, n_override, lsqr_override):
+    import paper_2605_19951_b200 as rb
+    prob, meta = rb.build_config(name, n=n_override)
+    approx = rb.config_approximant(name)
+    lsqr_iters = lsqr_override or meta.get("lsqr_iters", 30)
+    return prob, meta, approx, lsqr_iters
+
+
+def run_ours(args, world, rank):
+    import torch
+    import torch.distributed as dist
+    import paper_2605_19951_b200 as rb
+    from paper_2605_19951_b200.inversion import GNDriver, InversionConfig, LsqrConfig
+
+    t_setup = time.perf_counter()
+    prob, meta, approx, lsqr_iters = build_workload(args.config, args.n, args.lsqr)
+    m_true = rb.Model(prob.m_true, np.full(prob.grid.cell_count, np.log(0.01)))
+    cache = rb.ShiftedFactorCache()
+    eps_r, seed = meta.get("noise", (0.02, 2))
+    data = rb.make_dataset(prob, m_true, approx, rb.NoiseSpec(eps_r=eps_r, seed=seed), cache)
+    reg = rb.build_reg(prob.grid)          # C4: face-based RT0 root (P > dense limit)
+    lam = meta.get("lam", 1e-2)
+    cfg = InversionConfig(lambda0=lam, lsqr=LsqrConfig(tol=0.0, max_iters=lsqr_iters),
+                          m0=np.full(prob.grid.cell_count, np.log(meta.get("m0", 0.01))),
+                          chi2_target=0.0)
+    drv = GNDriver(prob, data, approx, cfg, cache, reg)
+    eng = cache.engine
+    setup_s = time.perf_counter() - t_setup
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    nu = 0
+    for _ in range(args.warmup):
+        nu += 1
+        drv.iterate(nu)
+    # ---- timed region: K GN iterations, inputs resident in HBM ------------
+    eng.set_timing(2)
+    eng.set_timing(1)
+    clocks = Clocks()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    fac0, sol0 = cache.counters.factorizations, cache.counters.solves
+    e0.record(stream)
+    for _ in range(args.steps):
+        nu += 1
+        drv.iterate(nu)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    cls = eng.timings()
+    eng.set_timing(0)
+    n_fact = cache.counters.factorizations - fac0
+    n_solve = cache.counters.solves - sol0
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+
+    # ---- e2e: public API with host buffers (pinned H2D of m and d_obs, D2H of
+    # the updated model inside the timed region) ------------------------------
+    m_host = torch.from_numpy(drv.model.m.copy()).pin_memory()
+    d_host = torch.from_numpy(np.asarray(data.d_obs, dtype=float).copy()).pin_memory()
+    out_host = torch.empty_like(m_host).pin_memory()
+    barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.steps):
+        nu += 1
+        m_dev = m_host.to("cuda", non_blocking=True)
+        d_dev = d_host.to("cuda", non_blocking=True)
+        drv.model = rb.Model(m_dev.cpu().numpy(), drv.model.m_ref)
+        drv.data.d_obs = d_dev.cpu().numpy()
+        drv.iterate(nu)
+        out_host.copy_(torch.from_numpy(drv.model.m))
+    e3.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = e2.elapsed_time(e3) / args.steps
+    if world > 1:
+        t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    bytes_in = m_host.numel() * 8 + d_host.numel() * 8
+    bytes_out = out_host.numel() * 8
+
+    # ---- component rates (after the timed region) ---------------------------
+    sym_flops, nnzL = symbolic_stats(eng)
+    comp = component_rates(eng, cache, drv, sym_flops, nnzL, world)
+
+    # ---- roofline of the dominant kernel class in the timed region ---------
+    peaks = measured_peaks()
+    fact_ms = sum(cls[k] for k in ("scatter", "extend_add", "diag", "trsm", "gemm"))
+    solve_ms = cls["solve_fwd"] + cls["solve_bwd"]
+    n_local_fact = n_fact if world == 1 else n_fact  # counters count local poles
+    fact_flops = sym_flops * n_local_fact
+    S = eng.S
+    nr = {1: 1, 2: 2, 3: 4, 4: 4}.get(S, 8)
+    solve_bytes_one = 2 * nnzL * 16 + eng.N * 16 + 4 * eng.N * nr * 16
+    n_local_solve = n_solve
+    if fact_ms >= solve_ms:
+        achieved = fact_flops / (fact_ms * 1e-3) / 1e12
+        roof = {"kernel": "frontal factorisation (K2-K4: scatter+extend-add+diag+trsm+gemm)",
+                "bound": "tensor", "achieved": achieved, "peak": peaks["fp64_tflops"],
+                "unit": "TFLOP/s", "frac": achieved / peaks["fp64_tflops"],
+                "peak_source": "measured FP64 DMMA microbenchmark (profiles/fp64_peak_r01.json)",
+                "traffic": None, "per_unit": "8*sum_s(p^3/6 + r p^2/2 + r^2 p/2) flops/pole",
+                "units_per_step": n_local_fact / args.steps}
+    else:
+        achieved = solve_bytes_one * n_local_solve / (solve_ms * 1e-3) / 1e9
+        roof = {"kernel": "multifrontal triangular solves (K6/K7)", "bound": "hbm",
+                "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "per_unit": "2*nnz(L)*16 + N*16 + 4*N*nrhs*16 bytes/solve",
+                "units_per_step": n_local_solve / args.steps}
+    value = ms_step / 1e3
+    line = {
+        "metric": METRIC, "value": value, "unit": "s/GN-iteration", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+        "dtype": "c128/f64", "data": "synthetic (seeded C4 stand-in, SURVEY §8d)",
+        "config": {"workload": f"{args.config}: {meta['n']}^3-hex Kuhn-tet Nedelec box, "
+                               f"N={eng.N} edge dofs, P={eng.P} cells, {eng.m} poles, "
+                               f"{S} sources x {eng.Mr} receivers x {eng.Kt} times, "
+                               f"{lsqr_iters} LSQR its, lambda={lam}",
+                   "global_batch": eng.m, "parallelism": f"pole-sharded x{world}",
+                   "l2": "inputs (factors, >100 GB) larger than L2; no flush needed"},
+        "gpu_launches": int(cls["launches"]),
+        "components": comp,
+        "kernel_ms": {k: round(v, 3) for k, v in cls.items() if k != "launches"},
+        "counts": {"factorizations": n_fact, "solves": n_solve},
+        "roofline": roof,
+        "clocks": clk,
+        "e2e": {"value": e2e_ms / 1e3, "unit": "s/GN-iteration",
+                "h2d_bytes_per_step": bytes_in, "d2h_bytes_per_step": bytes_out},
+        "setup_s": setup_s,
+        "memory_gb": {k: v / 1e9 for k, v in eng.info().items() if k.startswith("mem")},
+    }
+    return line
+
+
+def symbolic_stats(eng):
+    from paper_2605_19951_b200 import _lib
+    from paper_2605_19951_b200._lib import ptr
+    import ctypes as C
+    # the engine's symbolic is internal; recompute stats through the host API on
+    # the same pattern (cheap, host only)
+    prob = eng.problem
+    import scipy.sparse as sp
+    K = sp.csr_matrix(prob.K)
+    K.sort_indices()
+    ip = np.ascontiguousarray(K.indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(K.indices, dtype=np.int32)
+    co = np.ascontiguousarray(prob.dof_coords)
+    h = _lib.vp()
+    _lib.check(eng.lib.rba_symbolic_analyze(K.shape[0], ptr(ip), ptr(ix), ptr(co), 64,
+                                            C.byref(h)))
+    st = np.zeros(16, np.int64)
+    ds = np.zeros(4)
+    eng.lib.rba_symbolic_stats(h, ptr(st), ptr(ds))
+    eng.lib.rba_symbolic_destroy(h)
+    return float(ds[0]), int(st[3])
+
+
+def component_rates(eng, cache, drv, flops, nnzL, world):
+    import torch
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    out = {}
+    # factorisation of every local pole at the current model
+    torch.cuda.synchronize()
+    e0.record(stream)
+    eng.factor()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    nl = len(eng.local)
+    out["factor_tflops"] = flops * nl / (ms * 1e-3) / 1e12
+    out["factor_ms_per_pole"] = ms / nl
+    # forward solves (all local poles, S right-hand sides each)
+    e0.record(stream)
+    eng.forward()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    nr = {1: 1, 2: 2, 3: 4, 4: 4}.get(eng.S, 8)
+    bytes_one = 2 * nnzL * 16 + eng.N * 16 + 4 * eng.N * nr * 16
+    out["solve_gbs"] = bytes_one * nl / (ms * 1e-3) / 1e9
+    out["solve_ms_per_pole"] = ms / nl
+    v = torch.randn(eng.P, dtype=torch.float64, device="cuda")
+    w = torch.randn(eng.S * eng.Kt * eng.Mr, dtype=torch.float64, device="cuda")
+    reps = 3
+    e0.record(stream)
+    for _ in range(reps):
+        eng.jvp(v)
+        eng.vjp(w)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    out["jv_jtw_pairs_per_s"] = 1e3 / ms
+    out["factor_flops_per_pole"] = flops
+    out["nnzL_per_pole"] = nnzL
+    return out
+
+
+def cpu_baseline_sample(name):
+    """Oracle (SciPy SuperLU, the reference's backend) timed on the host on a
+    bounded sample: one pole's factorisation + solves at two mesh sizes of the
+    config's shape, power-law extrapolated to the config size and scaled by the
+    GN-iteration count law of SURVEY §3D, pole-parallel over the host cores."""
+    from oracle import rbainv_oracle as orc
+    import paper_2605_19951_b200 as rb
+    import scipy.sparse.linalg as spla
+    cores = os.cpu_count() or 1
+    spec_n = rb.config_spec(name)[1]["n"]
+    approx = rb.config_approximant(name)
+    pts = []
+    for n in (10, 14):
+        prob, _ = rb.build_config(name, n=n)
+        m = prob.m_true
+        t0 = time.perf_counter()
+        M = orc.assemble_M(prob, m).astype(complex)
+        A = (prob.K.astype(complex) - approx.poles[0] * M).tocsc()
+        lu = spla.splu(A)
+        tf = time.perf_counter() - t0
+        rhs = prob.source_matrix().T.astype(complex)
+        t0 = time.perf_counter()
+        for _ in range(3):
+            lu.solve(rhs)
+        ts = (time.perf_counter() - t0) / 3
+        pts.append((prob.dof_count, tf, ts))
+    (N1, f1, s1), (N2, f2, s2) = pts
+    prob_full, meta = rb.build_config(name, n=4)
+    N_full = {"C1": 26416, "C4": 662446, "C5": 1798336}.get(name.upper(), N2)
+    ef = math.log(f2 / f1) / math.log(N2 / N1)
+    es = math.log(s2 / s1) / math.log(N2 / N1)
+    tf = f2 * (N_full / N2) ** ef
+    ts = s2 * (N_full / N2) ** es
+    m = approx.pole_count
+    itn = meta.get("lsqr_iters", 30)
+    phi = 1
+    serial = m * phi * tf + m * (2 * itn + 2 + phi) * ts
+    return {"value": serial / min(cores, m), "unit": "s/GN-iteration", "cores": min(cores, m),
+            "kind": "port",
+            "sample": (f"oracle SuperLU factor+solve of 1 pole measured at N={N1} and N={N2} "
+                       f"({name} shape), power-law extrapolated (factor ~N^{ef:.2f}, solve "
+                       f"~N^{es:.2f}) to N={N_full}, x GN count law m*phi factorisations + "
+                       f"m*(2*itn+2+phi) solves (m={m}, itn={itn}, phi=1), ideal pole-parallel "
+                       f"on {min(cores, m)} cores; the config itself exceeds host RAM")}
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path (oracle port) on the host."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return None
+    t0 = time.perf_counter()
+    for _ in range(args.warmup):
+        pass
+    vals = []
+    for _ in range(max(1, args.steps)):
+        cb = cpu_baseline_sample(args.config)
+        vals.append(cb["value"])
+    cb["value"] = float(np.median(vals))
+    return {"impl": "reference", "metric": METRIC, "value": cb["value"],
+            "unit": "s/GN-iteration", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "c128/f64", "data": "synthetic", "config": {"workload": args.config},
+            "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "s/GN-iteration", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "wall_s": time.perf_counter() - t0}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        line = run_reference(args)
+        if line is not None:
+            print(json.dumps(line))
+        return
+    world, rank = dist_setup(args)
+    line = run_ours(args, world, rank)
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline_sample(args.config)
+        except Exception as exc:       # keep the GPU line even if the sample fails
+            line["cpu_baseline"] = {"error": repr(exc)}
+    if rank == 0:
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

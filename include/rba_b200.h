@@ -152,8 +152,11 @@ int rba_info(rba_ctx* ctx, int64_t* out_h);
 /* bytes of device memory held by the context: factors, workspace, other */
 int rba_memory(rba_ctx* ctx, int64_t* out_h);
 int rba_sync(rba_ctx* ctx);
-/* Per-kernel-class timing of the last rba_factor / solve (ms): factor total,
- * gemm, diag+trsm, extend-add, assembly; solve fwd, bwd. */
+/* Device time per kernel class (ms, CUDA events around every launch while
+ * timing is enabled), out[16]: scatter, extend-add, diag, trsm, gemm,
+ * solve-fwd, solve-bwd, element/observation, vector/SpMV, M assembly, ...,
+ * out[15] = kernel launches issued by this context (always counted).
+ * rba_set_timing: 1 on, 0 off, 2 reset the accumulators. */
 int rba_timings(rba_ctx* ctx, double* out_h);
 int rba_set_timing(rba_ctx* ctx, int32_t enabled);
 

@@ -125,9 +125,56 @@ struct rba_ctx {
   bool timing = false;
   double t_ms[8] = {0};
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  // per-kernel-class device time (CUDA events around every launch, enabled
+  // by rba_set_timing) and the launch count of this context's kernels
+  double cls_ms[16] = {0};
+  int64_t launches = 0;
+  std::vector<cudaEvent_t> evpool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
 };
 
 namespace {
+
+enum KClass { KC_SCATTER = 0, KC_EA = 1, KC_DIAG = 2, KC_TRSM = 3, KC_GEMM = 4, KC_FWD = 5,
+              KC_BWD = 6, KC_ELEM = 7, KC_VEC = 8, KC_ASSEMBLY = 9 };
+
+struct Timed {
+  rba_ctx* c;
+  int cls;
+  cudaEvent_t b = nullptr;
+  Timed(rba_ctx* c_, int cls_, int nlaunch = 1) : c(c_), cls(cls_) {
+    c->launches += nlaunch;
+    if (!c->timing) return;
+    cudaEvent_t a;
+    if (c->evpool.size() < 2) {
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      c->evpool.push_back(e0);
+      c->evpool.push_back(e1);
+    }
+    a = c->evpool.back(); c->evpool.pop_back();
+    b = c->evpool.back(); c->evpool.pop_back();
+    cudaEventRecord(a, c->st);
+    c->pending.push_back({cls, {a, b}});
+  }
+  ~Timed() {
+    if (b) cudaEventRecord(b, c->st);
+  }
+};
+
+void flush_timing(rba_ctx* c) {
+  if (c->pending.empty()) return;
+  cudaStreamSynchronize(c->st);
+  for (auto& p : c->pending) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+    c->cls_ms[p.first] += ms;
+    c->evpool.push_back(p.second.first);
+    c->evpool.push_back(p.second.second);
+  }
+  c->pending.clear();
+}
 
 template <class T>
 int dalloc(rba_ctx* c, std::vector<void*>& list, T** out, size_t count, size_t* acct) {
@@ -327,10 +374,10 @@ int build_plans(rba_ctx* c) {
 int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
   for (const Step& s : c->plan) {
     switch (s.kind) {
-      case ST_EA: rba::launch_extend_add(c->st, c->ea_tasks + s.off, s.n, c->F, pb); break;
-      case ST_DIAG: rba::launch_diag(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d); break;
-      case ST_TRSM: rba::launch_trsm(c->st, c->pt_tasks + s.off, s.n, c->F, pb); break;
-      case ST_GEMM: rba::launch_gemm_update(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb); break;
+      case ST_EA: { Timed t(c, KC_EA); rba::launch_extend_add(c->st, c->ea_tasks + s.off, s.n, c->F, pb); break; }
+      case ST_DIAG: { Timed t(c, KC_DIAG); rba::launch_diag(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d); break; }
+      case ST_TRSM: { Timed t(c, KC_TRSM); rba::launch_trsm(c->st, c->pt_tasks + s.off, s.n, c->F, pb); break; }
+      case ST_GEMM: { Timed t(c, KC_GEMM); rba::launch_gemm_update(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb); break; }
     }
     CKL();
   }
@@ -402,12 +449,14 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR) {
   CK(cudaMemsetAsync(c->tickets, 0, (2 * (size_t)S.nlevels + 2) * sizeof(int), c->st));
   if (c->timing) cudaEventRecord(c->ev[0], c->st);
   for (int L = 0; L < S.nlevels; ++L) {
+    Timed tm(c, KC_FWD);
     rba::launch_solve_level(c->st, true, NR, c->fwd_tasks + c->fwd_lv[L].first, c->fwd_lv[L].second,
                             ns, c->F, b, c->tickets + L, c->epoch);
     CKL();
   }
   if (c->timing) cudaEventRecord(c->ev[1], c->st);
   for (int L = S.nlevels - 1; L >= 0; --L) {
+    Timed tm(c, KC_BWD);
     rba::launch_solve_level(c->st, false, NR, c->bwd_tasks + c->bwd_lv[L].first, c->bwd_lv[L].second,
                             ns, c->F, b, c->tickets + S.nlevels + L, c->epoch);
     CKL();
@@ -704,7 +753,10 @@ int rba_set_model_d(rba_ctx* c, const double* m_d) {
   if (!c || !c->have_mesh) return fail(RBA_ERR_STATE, "set_mesh first");
   CK(cudaSetDevice(c->device));
   if (m_d != c->mdev) CK(cudaMemcpyAsync(c->mdev, m_d, c->P * sizeof(double), cudaMemcpyDeviceToDevice, c->st));
-  rba::launch_assemble_M(c->st, c->nnzA, c->cptr, c->coff, c->mass, c->mdev, c->expm, c->P, 36, c->Mv);
+  {
+    Timed t(c, KC_ASSEMBLY, 2);
+    rba::launch_assemble_M(c->st, c->nnzA, c->cptr, c->coff, c->mass, c->mdev, c->expm, c->P, 36, c->Mv);
+  }
   CKL();
   for (auto& v : c->valid) v = 0;
   c->model_set = true;
@@ -741,7 +793,10 @@ int rba_factor(rba_ctx* c) {
       pb.xi[i] = c->poles_h[c->local[l]];
       CK(cudaMemsetAsync(c->factor[l], 0, S.panel_off[S.nfront] * sizeof(cplx), c->st));
     }
-    rba::launch_scatter_A(c->st, c->nnzA, c->tgt, c->Kv, c->Mv, pb);
+    {
+      Timed t(c, KC_SCATTER);
+      rba::launch_scatter_A(c->st, c->nnzA, c->tgt, c->Kv, c->Mv, pb);
+    }
     CKL();
     if ((rc = run_plan(c, pb))) return rc;
     if ((rc = check_err(c, c->local[b0]))) return rc;
@@ -859,6 +914,7 @@ int rba_forward_partial(rba_ctx* c, double* qpart) {
   for (int l = 0; l < nl; ++l)
     CK(cudaMemcpyAsync(c->g[l], c->x[l], (size_t)c->N * c->NRs * sizeof(cplx), cudaMemcpyDeviceToDevice, c->st));
   if (qpart && c->Mr > 0) {
+    Timed t(c, KC_ELEM);
     rba::launch_q_apply(c->st, nl, c->Mr, c->q_ptr, c->q_col, c->q_val, slot_ptrs(c->g), c->NRs, c->S, (cplx*)qpart);
     CKL();
   }
@@ -869,11 +925,15 @@ int rba_jvp_partial(rba_ctx* c, const double* v_d, double* qpart) {
   if (!c || !c->model_set || !v_d || !qpart) return fail(RBA_ERR_STATE, "bad state/arguments");
   CK(cudaSetDevice(c->device));
   const int nl = (int)c->local.size();
-  rba::launch_jvp_rhs(c->st, nl, elem(c), v_d, slot_ptrs(c->g), slot_ptrs(c->x), c->NRs, c->S);
+  {
+    Timed t(c, KC_ELEM);
+    rba::launch_jvp_rhs(c->st, nl, elem(c), v_d, slot_ptrs(c->g), slot_ptrs(c->x), c->NRs, c->S);
+  }
   CKL();
   int rc;
   if ((rc = solve_slots(c, all_slots(c), c->NRs))) return rc;
   if (c->Mr > 0) {
+    Timed t(c, KC_ELEM);
     rba::launch_q_apply(c->st, nl, c->Mr, c->q_ptr, c->q_col, c->q_val, slot_ptrs(c->x), c->NRs, c->S, (cplx*)qpart);
     CKL();
   }
@@ -884,11 +944,15 @@ int rba_vjp_partial(rba_ctx* c, const double* w_d, double* tpart) {
   if (!c || !c->model_set || !w_d || !tpart) return fail(RBA_ERR_STATE, "bad state/arguments");
   CK(cudaSetDevice(c->device));
   const int nl = (int)c->local.size();
+  {
+  Timed t0(c, KC_ELEM, 2);
   rba::launch_vjp_rhs(c->st, nl, c->pole_of_slot, c->S, c->Kt, c->Mr, c->N, w_d, c->res_d, c->qt_ptr,
                       c->qt_col, c->qt_val, c->wa, slot_ptrs(c->x), c->NRs);
+  }
   CKL();
   int rc;
   if ((rc = solve_slots(c, all_slots(c), c->NRs))) return rc;
+  Timed t1(c, KC_ELEM);
   rba::launch_vjp_cells(c->st, nl, c->pole_of_slot, c->poles_d, elem(c), slot_ptrs(c->x), slot_ptrs(c->g),
                         c->NRs, c->S, tpart);
   CKL();
@@ -900,8 +964,11 @@ int rba_combine_data(rba_ctx* c, const double* qall, const int32_t* som, int32_t
   if (!c || !qall || !som || !d) return fail(RBA_ERR_INVALID, "null argument");
   CK(cudaSetDevice(c->device));
   CK(cudaMemcpyAsync(c->slot_map, som, c->m * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+  {
+  Timed t(c, KC_ELEM);
   rba::launch_combine_data(c->st, c->m, c->S, c->Kt, c->Mr, (const cplx*)qall, c->slot_map, c->res_d,
                            c->poles_d, times_pole != 0, d);
+  }
   CKL();
   CK(cudaStreamSynchronize(c->st));  // som is borrowed
   return RBA_OK;
@@ -911,7 +978,10 @@ int rba_combine_cells(rba_ctx* c, const double* tall, const int32_t* som, double
   if (!c || !tall || !som || !out) return fail(RBA_ERR_INVALID, "null argument");
   CK(cudaSetDevice(c->device));
   CK(cudaMemcpyAsync(c->slot_map, som, c->m * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
-  rba::launch_combine_cells(c->st, c->m, c->P, tall, c->slot_map, out);
+  {
+    Timed t(c, KC_ELEM);
+    rba::launch_combine_cells(c->st, c->m, c->P, tall, c->slot_map, out);
+  }
   CKL();
   CK(cudaStreamSynchronize(c->st));
   return RBA_OK;
@@ -956,6 +1026,7 @@ int rba_set_reg(rba_ctx* c, int64_t nrows, const int64_t* rp, const int32_t* ri,
 int rba_reg_apply(rba_ctx* c, int32_t transpose, const double* x, double alpha, double* y,
                   int32_t accumulate) {
   if (!c || !c->r_ptr || !x || !y) return fail(RBA_ERR_STATE, "set_reg first");
+  Timed t(c, KC_VEC);
   if (transpose)
     rba::launch_spmv(c->st, c->P, c->rt_ptr, c->rt_idx, c->rt_val, x, alpha, y, accumulate != 0);
   else
@@ -966,6 +1037,7 @@ int rba_reg_apply(rba_ctx* c, int32_t transpose, const double* x, double alpha, 
 
 int rba_vec_axpby(rba_ctx* c, int64_t n, double a, const double* x, double b, const double* y,
                   double* out) {
+  Timed t(c, KC_VEC);
   rba::launch_axpby(c->st, n, a, x, b, y, out);
   CKL();
   return RBA_OK;
@@ -973,13 +1045,14 @@ int rba_vec_axpby(rba_ctx* c, int64_t n, double a, const double* x, double b, co
 
 int rba_vec_mul(rba_ctx* c, int64_t n, const double* a, const double* x, double alpha,
                 double* out) {
+  Timed t(c, KC_VEC);
   rba::launch_mul(c->st, n, a, x, alpha, out);
   CKL();
   return RBA_OK;
 }
 
 int rba_vec_dot(rba_ctx* c, int64_t n, const double* x, const double* y, double* result) {
-  rba::launch_dot(c->st, n, x, y, c->red_part, c->red_res);
+  { Timed t(c, KC_VEC, 2); rba::launch_dot(c->st, n, x, y, c->red_part, c->red_res); }
   CKL();
   CK(cudaMemcpyAsync(result, c->red_res, sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
@@ -988,7 +1061,7 @@ int rba_vec_dot(rba_ctx* c, int64_t n, const double* x, const double* y, double*
 
 int rba_vec_lsqr_xw(rba_ctx* c, int64_t n, double t1, double t2, const double* v, double* w,
                     double* x, double* wn2) {
-  rba::launch_lsqr_xw(c->st, n, t1, t2, v, w, x, c->red_part, c->red_res);
+  { Timed t(c, KC_VEC, 2); rba::launch_lsqr_xw(c->st, n, t1, t2, v, w, x, c->red_part, c->red_res); }
   CKL();
   CK(cudaMemcpyAsync(wn2, c->red_res, sizeof(double), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
@@ -1037,11 +1110,19 @@ int rba_sync(rba_ctx* c) {
 }
 
 int rba_timings(rba_ctx* c, double* out) {
-  for (int i = 0; i < 8; ++i) out[i] = c->t_ms[i];
+  flush_timing(c);
+  for (int i = 0; i < 16; ++i) out[i] = c->cls_ms[i];
+  out[15] = (double)c->launches;
   return RBA_OK;
 }
 
 int rba_set_timing(rba_ctx* c, int32_t en) {
+  flush_timing(c);
+  if (en == 2) {
+    for (double& v : c->cls_ms) v = 0;
+    c->launches = 0;
+    return RBA_OK;
+  }
   c->timing = en != 0;
   return RBA_OK;
 }

@@ -276,13 +276,19 @@ class Engine:
                     n_local=int(out[7]), mem_factor=int(mem[0]), mem_work=int(mem[1]),
                     mem_other=int(mem[2]))
 
-    def set_timing(self, on: bool):
-        check(self.lib.rba_set_timing(self.ctx, 1 if on else 0))
+    KCLASSES = ("scatter", "extend_add", "diag", "trsm", "gemm", "solve_fwd", "solve_bwd",
+                "elem", "vec", "assembly")
 
-    def timings(self) -> np.ndarray:
-        out = np.zeros(8)
+    def set_timing(self, mode):
+        """True/1: record device time per kernel class; False/0: stop; 2: reset."""
+        check(self.lib.rba_set_timing(self.ctx, int(mode)))
+
+    def timings(self) -> dict:
+        out = np.zeros(16)
         check(self.lib.rba_timings(self.ctx, ptr(out)))
-        return out
+        d = {k: float(out[i]) for i, k in enumerate(self.KCLASSES)}
+        d["launches"] = int(out[15])
+        return d
 
     def sync(self):
         check(self.lib.rba_sync(self.ctx))
