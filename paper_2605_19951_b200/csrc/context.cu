@@ -128,6 +128,7 @@ struct rba_ctx {
   // per-kernel-class device time (CUDA events around every launch, enabled
   // by rba_set_timing) and the launch count of this context's kernels
   double cls_ms[16] = {0};
+  bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernel
   int64_t launches = 0;
   std::vector<cudaEvent_t> evpool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -377,7 +378,14 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
       case ST_EA: { Timed t(c, KC_EA); rba::launch_extend_add(c->st, c->ea_tasks + s.off, s.n, c->F, pb); break; }
       case ST_DIAG: { Timed t(c, KC_DIAG); rba::launch_diag(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d); break; }
       case ST_TRSM: { Timed t(c, KC_TRSM); rba::launch_trsm(c->st, c->pt_tasks + s.off, s.n, c->F, pb); break; }
-      case ST_GEMM: { Timed t(c, KC_GEMM); rba::launch_gemm_update(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb); break; }
+      case ST_GEMM: {
+        Timed t(c, KC_GEMM);
+        if (c->gemm_dfma)
+          rba::launch_gemm_update(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
+        else
+          rba::launch_gemm_dmma(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
+        break;
+      }
     }
     CKL();
   }
@@ -580,6 +588,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     c->own_stream = true;
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
+  if (const char* e = getenv("RBA_GEMM")) c->gemm_dfma = std::string(e) == "dfma";
   int rc;
   if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||
       (rc = dalloc(c, c->allocs, &c->red_part, 1024, &c->mem_other)) ||

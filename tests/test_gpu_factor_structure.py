@@ -42,3 +42,24 @@ def test_device_fronts_match_emulation(gpu, n):
     b = prob.f.astype(complex)
     x = cache.solve(0, b)
     assert rel(prob.Q @ x, prob.Q @ mf.solve(b, panels, S)) <= 1e-10
+
+
+def test_dmma_gemm_matches_dfma_reference(gpu, monkeypatch):
+    """The FP64 tensor-core (DMMA) trailing update equals the DFMA reference
+    kernel on the same fronts (C1 shape, n=10: multi-block fronts)."""
+    prob, _ = rb.build_config("C1", n=10)
+    approx = rb.config_approximant("C1")
+    model = prob.true_model()
+    out = []
+    for mode in ("dfma", "dmma"):
+        monkeypatch.setenv("RBA_GEMM", mode)
+        cache = rb.ShiftedFactorCache()
+        rb.factorize_all_poles(prob, model, approx, cache)
+        eng = cache.engine
+        S = mf.analyze(prob.K, prob.dof_coords, 64)
+        tot = int(S["panel_off"][-1])
+        buf = np.empty(tot, dtype=np.complex128)
+        _lib.check(eng.lib.rba_get_factor(eng.ctx, 2, ptr(buf.view(np.float64)), tot))
+        out.append(buf)
+        eng.close()
+    assert rel(out[1], out[0]) <= 1e-12
