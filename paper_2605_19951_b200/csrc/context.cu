@@ -377,7 +377,14 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
     switch (s.kind) {
       case ST_EA: { Timed t(c, KC_EA); rba::launch_extend_add(c->st, c->ea_tasks + s.off, s.n, c->F, pb); break; }
       case ST_DIAG: { Timed t(c, KC_DIAG); rba::launch_diag(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d); break; }
-      case ST_TRSM: { Timed t(c, KC_TRSM); rba::launch_trsm(c->st, c->pt_tasks + s.off, s.n, c->F, pb); break; }
+      case ST_TRSM: {
+        Timed t(c, KC_TRSM);
+        if (c->gemm_dfma)
+          rba::launch_trsm(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
+        else
+          rba::launch_trsm_dmma(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
+        break;
+      }
       case ST_GEMM: {
         Timed t(c, KC_GEMM);
         if (c->gemm_dfma)

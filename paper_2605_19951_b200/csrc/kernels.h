@@ -38,6 +38,8 @@ void launch_gemm_update(cudaStream_t st, const GemmTask* tasks, int ntasks, int 
                         const FrontsDev& F, const PoleBatch& pb);
 void launch_gemm_dmma(cudaStream_t st, const GemmTask* tasks, int ntasks, int ntiles,
                       const FrontsDev& F, const PoleBatch& pb);
+void launch_trsm_dmma(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
+                      const PoleBatch& pb);
 
 // solves
 void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* tasks,

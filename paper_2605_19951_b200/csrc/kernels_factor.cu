@@ -119,7 +119,11 @@ void launch_extend_add(cudaStream_t st, const int2* tasks, int ntasks, const Fro
 
 // ---------------------------------------------------------------------------
 // K4a: diagonal block LDL^T (one CTA per front, shared memory), written back
-// in place (unit-lower L below the diagonal, D on the diagonal).
+// in place: unit-lower L below the diagonal, D on the diagonal, and the
+// inverse X = L^{-1} (unit lower) stored TRANSPOSED in the otherwise unused
+// strictly-upper triangle (X[i][j] at row j, column i).  The inverse turns the
+// panel TRSM into a tensor-core GEMM and the solve's diagonal-block
+// substitutions into GEMVs (no sequential chains inside a block).
 // ---------------------------------------------------------------------------
 constexpr int LDS = PB + 1;
 
@@ -157,9 +161,20 @@ __global__ void __launch_bounds__(256) k_diag(const PanelTask* __restrict__ task
     for (int i = j + 1 + tid; i < kb; i += blockDim.x) Dg[i * LDS + j] = cmul(Dg[i * LDS + j], dinv);
     __syncthreads();
   }
+  // X = L^{-1}: one column per thread, forward substitution down the column
+  cplx* Xs = sm + PB * LDS;
+  if (tid < kb) {
+    const int j = tid;
+    for (int i = j + 1; i < kb; ++i) {
+      cplx acc = Dg[i * LDS + j];
+      for (int t = j + 1; t < i; ++t) acc = cfma(Dg[i * LDS + t], Xs[t * LDS + j], acc);
+      Xs[i * LDS + j] = cmk(-acc.x, -acc.y);
+    }
+  }
+  __syncthreads();
   for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
     int i = idx % kb, j = idx / kb;
-    if (i >= j) panel[(int64_t)(k0 + j) * nf + k0 + i] = Dg[i * LDS + j];
+    panel[(int64_t)(k0 + j) * nf + k0 + i] = i >= j ? Dg[i * LDS + j] : Xs[j * LDS + i];
   }
 }
 
@@ -205,7 +220,7 @@ __global__ void __launch_bounds__(256) k_trsm(const PanelTask* __restrict__ task
 void launch_diag(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
                  const PoleBatch& pb, int* err) {
   if (ntasks <= 0) return;
-  size_t smem = PB * LDS * sizeof(cplx);
+  size_t smem = 2 * PB * LDS * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_diag, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -40,22 +40,43 @@ struct Stage {
 };
 }  // namespace
 
+// MODE 0: trailing/Schur update  C[r,c] -= sum_t (L[r,t] d_t) L[c,t]  (r >= c)
+// MODE 1: panel TRSM  L[r, k0+c] = (sum_{t<=c} F[r, k0+t] X[c][t]) / d_c, with
+//         X = L_kk^{-1} read from the diagonal block's upper triangle (k_diag).
+template <int MODE>
 __global__ void __launch_bounds__(NT) k_gemm_dmma(const GemmTask* __restrict__ tasks, int ntasks,
+                                                  const PanelTask* __restrict__ ptasks,
                                                   FrontsDev F, PoleBatch pb) {
   extern __shared__ __align__(16) double smraw[];
   Stage* st = reinterpret_cast<Stage*>(smraw);     // st[0], st[1]
   __shared__ cplx ds[2][TK];
+  __shared__ cplx dinv[GT];
   const int slot = blockIdx.y;
-  const int ti = find_task(tasks, ntasks, blockIdx.x);
-  const GemmTask tk = tasks[ti];
-  int local = blockIdx.x - tk.tile_start;
-  int j = 0;
-  while (local >= tk.ntr - j) { local -= tk.ntr - j; ++j; }
-  const int i = j + local;
+  GemmTask tk;
+  int r0, cc0, cmax, kbase = 0;
+  if (MODE == 0) {
+    const int ti = find_task(tasks, ntasks, blockIdx.x);
+    tk = tasks[ti];
+    int local = blockIdx.x - tk.tile_start;
+    int j = 0;
+    while (local >= tk.ntr - j) { local -= tk.ntr - j; ++j; }
+    const int i = j + local;
+    r0 = tk.c_lo + i * GT;
+    cc0 = tk.c_lo + j * GT;
+    cmax = min(cc0 + GT, tk.c_hi);
+  } else {
+    const PanelTask pt = ptasks[blockIdx.x];
+    const int p_ = F.npiv[pt.s];
+    tk.s = pt.s;
+    tk.t0 = 0;
+    tk.t1 = min(GT, p_ - pt.k0);         // kb
+    kbase = pt.k0;
+    r0 = pt.r0;
+    cc0 = 0;
+    cmax = tk.t1;
+  }
   const int s = tk.s;
   const int nf = F.nf[s], p = F.npiv[s];
-  const int r0 = tk.c_lo + i * GT, cc0 = tk.c_lo + j * GT;
-  const int cmax = min(cc0 + GT, tk.c_hi);
   const cplx* __restrict__ panel = pb.factor[slot] + F.panel_off[s];
   cplx* pw = pb.factor[slot] + F.panel_off[s];
   cplx* upd = pb.upd[slot] + (F.upd_off[s] >= 0 ? F.upd_off[s] : 0);
@@ -84,9 +105,18 @@ __global__ void __launch_bounds__(NT) k_gemm_dmma(const GemmTask* __restrict__ t
       const int t = kt + kk;
       cplx a = cmk(0.0, 0.0), b = cmk(0.0, 0.0);
       if (t < tk.t1) {
-        const cplx* col = panel + (int64_t)t * nf;
-        if (r0 + rr < nf) a = __ldg(col + r0 + rr);
-        if (cc0 + rr < cmax) b = __ldg(col + cc0 + rr);
+        if (MODE == 0) {
+          const cplx* col = panel + (int64_t)t * nf;
+          if (r0 + rr < nf) a = __ldg(col + r0 + rr);
+          if (cc0 + rr < cmax) b = __ldg(col + cc0 + rr);
+        } else {
+          // A = F[r0+rr, kbase+t]; B[c=rr][t] = X[c][t] (t < c), 1 (t == c), 0 (t > c)
+          if (r0 + rr < nf) a = __ldg(panel + (int64_t)(kbase + t) * nf + r0 + rr);
+          if (rr < cmax) {
+            if (t < rr) b = __ldg(panel + (int64_t)(kbase + rr) * nf + kbase + t);
+            else if (t == rr) b = cmk(1.0, 0.0);
+          }
+        }
       }
       pa[q] = a;
       pbv[q] = b;
@@ -95,9 +125,14 @@ __global__ void __launch_bounds__(NT) k_gemm_dmma(const GemmTask* __restrict__ t
   auto dload = [&](int kt, int buf) {
     if (tid < TK) {
       const int t = kt + tid;
-      ds[buf][tid] = t < tk.t1 ? __ldg(panel + (int64_t)t * nf + t) : cmk(0.0, 0.0);
+      ds[buf][tid] = MODE == 1 ? cmk(1.0, 0.0)
+                   : (t < tk.t1 ? __ldg(panel + (int64_t)t * nf + t) : cmk(0.0, 0.0));
     }
   };
+  if (MODE == 1 && tid < GT) {
+    dinv[tid] = tid < cmax ? cinv(__ldg(panel + (int64_t)(kbase + tid) * nf + kbase + tid))
+                           : cmk(0.0, 0.0);
+  }
   auto sstore = [&](int buf) {
     Stage& S = st[buf];
 #pragma unroll
@@ -158,23 +193,39 @@ __global__ void __launch_bounds__(NT) k_gemm_dmma(const GemmTask* __restrict__ t
     }
     __syncthreads();
   }
-  // epilogue: C -= acc  (lower triangle only)
+  if (MODE == 0) {
+    // epilogue: C -= acc  (lower triangle only)
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+      for (int b = 0; b < 4; ++b)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = r0 + wm + a * 8 + g;
-        const int c = cc0 + wn + b * 8 + t4 * 2 + h;
-        if (r < nf && c < cmax && r >= c) {
-          cplx* dst = faddr(pw, upd, p, nf, r, c);
-          cplx v = *dst;
-          v.x -= cre[a][b][h];
-          v.y -= cim[a][b][h];
-          *dst = v;
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + wm + a * 8 + g;
+          const int c = cc0 + wn + b * 8 + t4 * 2 + h;
+          if (r < nf && c < cmax && r >= c) {
+            cplx* dst = faddr(pw, upd, p, nf, r, c);
+            cplx v = *dst;
+            v.x -= cre[a][b][h];
+            v.y -= cim[a][b][h];
+            *dst = v;
+          }
         }
-      }
+  } else {
+    // epilogue: L = (F X^T) D^{-1}, written in place (every A element of this
+    // tile was staged before any write: the K loop ended with a barrier)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + wm + a * 8 + g;
+          const int c = wn + b * 8 + t4 * 2 + h;
+          if (r < nf && c < cmax)
+            pw[(int64_t)(kbase + c) * nf + r] = cmul(cmk(cre[a][b][h], cim[a][b][h]), dinv[c]);
+        }
+  }
 }
 
 void launch_gemm_dmma(cudaStream_t st, const GemmTask* tasks, int ntasks, int ntiles,
@@ -183,11 +234,24 @@ void launch_gemm_dmma(cudaStream_t st, const GemmTask* tasks, int ntasks, int nt
   const size_t smem = 2 * sizeof(Stage);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_dmma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_gemm_dmma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   dim3 grid(ntiles, pb.count);
-  k_gemm_dmma<<<grid, NT, smem, st>>>(tasks, ntasks, F, pb);
+  k_gemm_dmma<0><<<grid, NT, smem, st>>>(tasks, ntasks, nullptr, F, pb);
+}
+
+void launch_trsm_dmma(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
+                      const PoleBatch& pb) {
+  if (ntasks <= 0) return;
+  const size_t smem = 2 * sizeof(Stage);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_dmma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid(ntasks, pb.count);
+  k_gemm_dmma<1><<<grid, NT, smem, st>>>(nullptr, 0, tasks, F, pb);
 }
 
 }  // namespace rba

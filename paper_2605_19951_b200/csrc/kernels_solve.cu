@@ -28,6 +28,12 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// Forward task (front s, row block blk): rows [r0, r0+nr) of the front vector.
+//   pivot block  : y_blk = X_blk (v_blk - sum_{j<blk} L[blk, j] y_j)   (X = L_bb^{-1})
+//   border block : u     = v - sum_{j<npb} L[rows, j] y_j              -> parent
+// Warps split the pivot columns (column c handled by warp c % 8), lanes own
+// rows lane and lane+32, so every L load is a coalesced 2 x 512 B column
+// segment; y is read through L2 (it was produced by other CTAs).
 template <int NR>
 __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks, int nslots,
                                              FrontsDev F, SolveBatchDev sb, int* ticket,
@@ -35,10 +41,8 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
   __shared__ int s_t;
   extern __shared__ cplx dsm[];
   cplx(*v)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm);
-  cplx(*ys)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + PB * NR);
-  cplx(*red)[PB][NR] = reinterpret_cast<cplx(*)[PB][NR]>(dsm + 2 * PB * NR);
-  cplx(*Lb)[PB + 1] = reinterpret_cast<cplx(*)[PB + 1]>(dsm + 6 * PB * NR);
-  const int tid = threadIdx.x;
+  cplx(*red)[PB][NR] = reinterpret_cast<cplx(*)[PB][NR]>(dsm + PB * NR);   // [8][PB][NR]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_t = atomicAdd(ticket, 1);
   __syncthreads();
   const int t = s_t;
@@ -55,10 +59,9 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
   const int r0 = pivot ? blk * PB : p + (blk - npb) * PB;
   const int nr = pivot ? min(PB, p - r0) : min(PB, nf - r0);
   const int jmax = pivot ? blk : npb;
-  const int row = tid & (PB - 1), cg = tid >> 6;
 
-  if (cg == 0 && row < nr) {
-    const int rho = r0 + row;
+  if (tid < nr) {
+    const int rho = r0 + tid;
     cplx val[NR];
 #pragma unroll
     for (int r = 0; r < NR; ++r)
@@ -70,77 +73,88 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
       for (int r = 0; r < NR; ++r) val[r] = cadd(val[r], uvec[u * NR + r]);
     }
 #pragma unroll
-    for (int r = 0; r < NR; ++r) v[row][r] = val[r];
+    for (int r = 0; r < NR; ++r) v[tid][r] = val[r];
   }
-  cplx acc[NR];
+  cplx acc0[NR], acc1[NR];
 #pragma unroll
-  for (int r = 0; r < NR; ++r) acc[r] = cmk(0.0, 0.0);
+  for (int r = 0; r < NR; ++r) acc0[r] = acc1[r] = cmk(0.0, 0.0);
+  const bool ok0 = lane < nr, ok1 = lane + 32 < nr;
+  const cplx* rowp = panel + r0 + lane;
+  if (!pivot && jmax > 0) {
+    // border rows need every pivot block: one wait (block npb-1 implies all)
+    if (lane == 0)
+      while (ld_acquire(flags + jmax - 1) < epoch) __nanosleep(32);
+    __syncwarp();
+  }
   for (int j = 0; j < jmax; ++j) {
-    const int c0 = j * PB, ncol = min(PB, p - c0);
-    if (tid == 0) {
-      while (ld_acquire(flags + j) < epoch) { __nanosleep(64); }
+    if (pivot) {
+      if (lane == 0)
+        while (ld_acquire(flags + j) < epoch) __nanosleep(32);
+      __syncwarp();
     }
-    __syncthreads();
-    for (int q = tid; q < ncol * NR; q += blockDim.x)
-      ys[q / NR][q % NR] = ldcg_c(x + (int64_t)(first + c0) * NR + q);
-    __syncthreads();
-    if (row < nr) {
-      const cplx* col = panel + (int64_t)c0 * nf + r0 + row;
+    const int c0 = j * PB, c1 = min(c0 + PB, p);
 #pragma unroll 4
-      for (int c = cg; c < ncol; c += 4) {
-        const cplx l = __ldg(col + (int64_t)c * nf);
+    for (int c = c0 + warp; c < c1; c += 8) {
+      const cplx* colp = rowp + (int64_t)c * nf;
+      const cplx l0 = ok0 ? __ldg(colp) : cmk(0.0, 0.0);
+      const cplx l1 = ok1 ? __ldg(colp + 32) : cmk(0.0, 0.0);
 #pragma unroll
-        for (int r = 0; r < NR; ++r) acc[r] = cfma(l, ys[c][r], acc[r]);
+      for (int r = 0; r < NR; ++r) {
+        const cplx y = ldcg_c(x + (int64_t)(first + c) * NR + r);
+        acc0[r] = cfma(l0, y, acc0[r]);
+        acc1[r] = cfma(l1, y, acc1[r]);
       }
     }
-    __syncthreads();
   }
 #pragma unroll
-  for (int r = 0; r < NR; ++r) red[cg][row][r] = acc[r];
-  if (pivot) {
-    for (int idx = tid; idx < nr * nr; idx += blockDim.x) {
-      const int i = idx % nr, c = idx / nr;
-      if (i > c) Lb[i][c] = panel[(int64_t)(r0 + c) * nf + r0 + i];
-    }
+  for (int r = 0; r < NR; ++r) {
+    red[warp][lane][r] = acc0[r];
+    red[warp][lane + 32][r] = acc1[r];
   }
   __syncthreads();
-  if (cg == 0 && row < nr) {
+  if (tid < nr) {
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-      cplx sacc = cadd(cadd(red[0][row][r], red[1][row][r]), cadd(red[2][row][r], red[3][row][r]));
-      v[row][r] = csub(v[row][r], sacc);
+      cplx sacc = red[0][tid][r];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) sacc = cadd(sacc, red[w][tid][r]);
+      v[tid][r] = csub(v[tid][r], sacc);
     }
   }
   __syncthreads();
   if (pivot) {
-    // unit-lower solve, threads 0..63 own one row each
-    if (tid < PB) {
-      for (int c = 0; c < nr; ++c) {
-        named_bar(1, PB);
-        if (tid > c && tid < nr) {
+    // y_i = t_i + sum_{c<i} X[i][c] t_c ; X[i][c] sits at (row r0+c, col r0+i)
+    if (tid < nr) {
+      const int i = tid;
+      cplx yv[NR];
 #pragma unroll
-          for (int r = 0; r < NR; ++r) v[tid][r] = cfms(Lb[tid][c], v[c][r], v[tid][r]);
-        }
-      }
-      named_bar(1, PB);
-      if (tid < nr) {
+      for (int r = 0; r < NR; ++r) yv[r] = v[i][r];
+      const cplx* xcol = panel + (int64_t)(r0 + i) * nf + r0;
+#pragma unroll 4
+      for (int c = 0; c < i; ++c) {
+        const cplx xv = __ldg(xcol + c);
 #pragma unroll
-        for (int r = 0; r < NR; ++r) x[(int64_t)(first + r0 + tid) * NR + r] = v[tid][r];
+        for (int r = 0; r < NR; ++r) yv[r] = cfma(xv, v[c][r], yv[r]);
       }
+#pragma unroll
+      for (int r = 0; r < NR; ++r) x[(int64_t)(first + r0 + i) * NR + r] = yv[r];
       __threadfence();
     }
     __syncthreads();
     if (tid == 0) st_release(flags + blk, epoch);
   } else {
-    if (cg == 0 && row < nr) {
-      cplx* u = sb.uvec[slot] + (F.uvec_off[s] + (r0 - p) + row) * NR;
+    if (tid < nr) {
+      cplx* u = sb.uvec[slot] + (F.uvec_off[s] + (r0 - p) + tid) * NR;
 #pragma unroll
-      for (int r = 0; r < NR; ++r) u[r] = v[row][r];
+      for (int r = 0; r < NR; ++r) u[r] = v[tid][r];
     }
   }
 }
 
-// Backward: column block of pivots; x_c = L_cc^{-T} (y_c / d_c - sum_{rows below} L^T x).
+// Backward task (front s, pivot column block cb), blocks processed from the
+// last one down:  x_cb = X^T (y_cb / d_cb - sum_{rho beyond block} L[rho, cb]^T x_rho).
+// 16 warps x 4 columns; lanes stride the rows; X^T from the diagonal block's
+// upper triangle (coalesced across the column threads).
 template <int NR>
 __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks, int nslots,
                                              FrontsDev F, SolveBatchDev sb, int* ticket,
@@ -149,7 +163,6 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   extern __shared__ cplx dsm[];
   cplx(*red)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm);
   cplx(*tv)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + PB * NR);
-  cplx(*Lb)[PB + 1] = reinterpret_cast<cplx(*)[PB + 1]>(dsm + 2 * PB * NR);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_t = atomicAdd(ticket, 1);
   __syncthreads();
@@ -164,23 +177,25 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   int* flags = sb.flags[slot] + F.blk_off[s];
   const int c0 = cb * PB, ncol = min(PB, p - c0);
   const int* rows = F.rows + F.rows_off[s];
-  // warp w owns columns c0 + 4w .. c0 + 4w + 3
   cplx acc[4][NR];
 #pragma unroll
   for (int k = 0; k < 4; ++k)
 #pragma unroll
     for (int r = 0; r < NR; ++r) acc[k][r] = cmk(0.0, 0.0);
   const int cw = 4 * warp;
+  const int nk = max(0, min(4, ncol - cw));
+  const cplx* colp = panel + (int64_t)(c0 + cw) * nf;
   // border rows (ancestor pivots: final)
+#pragma unroll 2
   for (int rho = p + lane; rho < nf; rho += 32) {
-    const int g = rows[rho];
+    const int g = __ldg(rows + rho);
     cplx xv[NR];
 #pragma unroll
     for (int r = 0; r < NR; ++r) xv[r] = ldcg_c(x + (int64_t)g * NR + r);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      if (cw + k < ncol) {
-        const cplx l = __ldg(panel + (int64_t)(c0 + cw + k) * nf + rho);
+      if (k < nk) {
+        const cplx l = __ldg(colp + (int64_t)k * nf + rho);
 #pragma unroll
         for (int r = 0; r < NR; ++r) acc[k][r] = cfma(l, xv[r], acc[k][r]);
       }
@@ -188,26 +203,25 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   }
   // later pivot blocks of this front (produced by earlier tickets)
   for (int rb = npb - 1; rb > cb; --rb) {
-    if (tid == 0) {
-      while (ld_acquire(flags + rb) < epoch) { __nanosleep(64); }
-    }
-    __syncthreads();
+    if (lane == 0)
+      while (ld_acquire(flags + rb) < epoch) __nanosleep(32);
+    __syncwarp();
     const int q0 = rb * PB, q1 = min(q0 + PB, p);
+#pragma unroll 2
     for (int rho = q0 + lane; rho < q1; rho += 32) {
       cplx xv[NR];
 #pragma unroll
       for (int r = 0; r < NR; ++r) xv[r] = ldcg_c(x + (int64_t)(first + rho) * NR + r);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        if (cw + k < ncol) {
-          const cplx l = __ldg(panel + (int64_t)(c0 + cw + k) * nf + rho);
+        if (k < nk) {
+          const cplx l = __ldg(colp + (int64_t)k * nf + rho);
 #pragma unroll
           for (int r = 0; r < NR; ++r) acc[k][r] = cfma(l, xv[r], acc[k][r]);
         }
       }
     }
   }
-  // in-block strictly-lower part handled by the triangular solve below
 #pragma unroll
   for (int k = 0; k < 4; ++k)
 #pragma unroll
@@ -223,36 +237,35 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   if (lane == 0) {
 #pragma unroll
     for (int k = 0; k < 4; ++k)
-      if (cw + k < ncol)
+      if (k < nk)
 #pragma unroll
         for (int r = 0; r < NR; ++r) red[cw + k][r] = acc[k][r];
   }
-  for (int idx = tid; idx < ncol * ncol; idx += blockDim.x) {
-    const int i = idx % ncol, c = idx / ncol;
-    if (i > c) Lb[i][c] = panel[(int64_t)(c0 + c) * nf + c0 + i];
+  __syncthreads();
+  if (tid < ncol) {
+    const cplx d = panel[(int64_t)(c0 + tid) * nf + c0 + tid];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const cplx y = x[(int64_t)(first + c0 + tid) * NR + r];
+      tv[tid][r] = csub(cdiv(y, d), red[tid][r]);
+    }
   }
   __syncthreads();
-  if (tid < PB) {
-    if (tid < ncol) {
-      const cplx d = panel[(int64_t)(c0 + tid) * nf + c0 + tid];
+  // x_c = t_c + sum_{i>c} X[i][c] t_i ; X[i][c] sits at (row c0+c, col c0+i)
+  if (tid < ncol) {
+    const int c = tid;
+    cplx xv[NR];
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const cplx y = x[(int64_t)(first + c0 + tid) * NR + r];
-        tv[tid][r] = csub(cdiv(y, d), red[tid][r]);
-      }
-    }
-    for (int c = ncol - 1; c >= 0; --c) {
-      named_bar(1, PB);
-      if (tid < c) {
+    for (int r = 0; r < NR; ++r) xv[r] = tv[c][r];
+    const cplx* xrow = panel + c0 + c;
+#pragma unroll 4
+    for (int i = c + 1; i < ncol; ++i) {
+      const cplx w = __ldg(xrow + (int64_t)(c0 + i) * nf);
 #pragma unroll
-        for (int r = 0; r < NR; ++r) tv[tid][r] = cfms(Lb[c][tid], tv[c][r], tv[tid][r]);
-      }
+      for (int r = 0; r < NR; ++r) xv[r] = cfma(w, tv[i][r], xv[r]);
     }
-    named_bar(1, PB);
-    if (tid < ncol) {
 #pragma unroll
-      for (int r = 0; r < NR; ++r) x[(int64_t)(first + c0 + tid) * NR + r] = tv[tid][r];
-    }
+    for (int r = 0; r < NR; ++r) x[(int64_t)(first + c0 + c) * NR + r] = xv[r];
     __threadfence();
   }
   __syncthreads();
@@ -262,7 +275,7 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
 template <int NR>
 static void fwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
                    const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch) {
-  const size_t smem = (6 * PB * NR + PB * (PB + 1)) * sizeof(cplx);
+  const size_t smem = (9 * PB * NR) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fwd<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -273,7 +286,7 @@ static void fwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslo
 template <int NR>
 static void bwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
                    const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch) {
-  const size_t smem = (2 * PB * NR + PB * (PB + 1)) * sizeof(cplx);
+  const size_t smem = (2 * PB * NR) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_bwd<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

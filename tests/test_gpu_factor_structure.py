@@ -62,4 +62,6 @@ def test_dmma_gemm_matches_dfma_reference(gpu, monkeypatch):
         _lib.check(eng.lib.rba_get_factor(eng.ctx, 2, ptr(buf.view(np.float64)), tot))
         out.append(buf)
         eng.close()
-    assert rel(out[1], out[0]) <= 1e-12
+    # the DFMA reference path also keeps the substitution TRSM, the DMMA path
+    # uses the inverted diagonal block: rounding-level differences only
+    assert rel(out[1], out[0]) <= 1e-10
