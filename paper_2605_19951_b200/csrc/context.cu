@@ -235,6 +235,8 @@ int ensure_stage(rba_ctx* c, int64_t n) {
 // ---------------------------------------------------------------------------
 int build_plans(rba_ctx* c) {
   const rba::Symbolic& S = c->sym;
+  int panel = 2;                  // 64-column blocks per trailing-update panel
+  if (const char* e = getenv("RBA_PANEL")) panel = std::max(1, atoi(e));
   std::vector<int2> ea;
   std::vector<rba::PanelTask> pt;
   std::vector<rba::GemmTask> gm;
@@ -269,19 +271,31 @@ int build_plans(rba_ctx* c) {
         for (int r0 = k0 + kb; r0 < S.nf[s]; r0 += rba::PB) pt.push_back({s, k0, r0, 0});
       }
       if ((int64_t)pt.size() > toff) c->plan.push_back({ST_TRSM, toff, (int)(pt.size() - toff), 0});
+      // trailing update after block kk: inside a panel of `panel` blocks only
+      // the rest of the panel is updated (K = 64, look-ahead); at the panel's
+      // last block all columns beyond the panel get one update with
+      // K = the whole panel (fewer, fatter tensor-core GEMM passes).
       int64_t goff = gm.size();
       int tiles = 0;
       for (int q = q0; q < q1; ++q) {
         int s = S.level_fronts[q];
-        if (S.npiv[s] <= k0) continue;
-        int kb = std::min(rba::PB, S.npiv[s] - k0);
-        int clo = k0 + kb, chi = S.npiv[s];
+        const int p = S.npiv[s];
+        if (p <= k0) continue;
+        const int kb = std::min(rba::PB, p - k0);
+        const int pstart = (kk / panel) * panel * rba::PB;
+        const int pend = std::min(p, (kk / panel + 1) * panel * rba::PB);
+        int t0, t1, clo, chi;
+        if (k0 + kb < pend) {            // in-panel look-ahead update
+          t0 = k0; t1 = k0 + kb; clo = k0 + kb; chi = pend;
+        } else {                         // end of panel: aggregated update
+          t0 = pstart; t1 = pend; clo = pend; chi = p;
+        }
         if (chi <= clo) continue;
         int ntr = (S.nf[s] - clo + rba::GT - 1) / rba::GT;
         int ntc = (chi - clo + rba::GT - 1) / rba::GT;
         int nt = 0;
         for (int j = 0; j < ntc; ++j) nt += ntr - j;
-        gm.push_back({s, k0, k0 + kb, clo, chi, tiles, ntr, 0});
+        gm.push_back({s, t0, t1, clo, chi, tiles, ntr, 0});
         tiles += nt;
       }
       if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles});

@@ -33,7 +33,9 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 //   border block : u     = v - sum_{j<npb} L[rows, j] y_j              -> parent
 // Warps split the pivot columns (column c handled by warp c % 8), lanes own
 // rows lane and lane+32, so every L load is a coalesced 2 x 512 B column
-// segment; y is read through L2 (it was produced by other CTAs).
+// segment; each warp fetches the y values of its 8 columns of a block with one
+// L2 load per lane (they were produced by other CTAs) and broadcasts them with
+// shuffles.  16 L loads per lane are in flight per block.
 template <int NR>
 __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks, int nslots,
                                              FrontsDev F, SolveBatchDev sb, int* ticket,
@@ -86,25 +88,42 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
       while (ld_acquire(flags + jmax - 1) < epoch) __nanosleep(32);
     __syncwarp();
   }
+  constexpr int YPL = (8 * NR + 31) / 32;   // y values per lane per block
   for (int j = 0; j < jmax; ++j) {
     if (pivot) {
       if (lane == 0)
         while (ld_acquire(flags + j) < epoch) __nanosleep(32);
       __syncwarp();
     }
-    const int c0 = j * PB, c1 = min(c0 + PB, p);
-#pragma unroll 4
-    for (int c = c0 + warp; c < c1; c += 8) {
-      const cplx* colp = rowp + (int64_t)c * nf;
-      const cplx l0 = ok0 ? __ldg(colp) : cmk(0.0, 0.0);
-      const cplx l1 = ok1 ? __ldg(colp + 32) : cmk(0.0, 0.0);
+    const int c0 = j * PB, ncol = min(PB, p - c0);
+    // y of this warp's 8 columns (c0 + warp + 8q), NR each
+    cplx yv[YPL];
+#pragma unroll
+    for (int h = 0; h < YPL; ++h) {
+      const int e = lane + 32 * h;
+      const int q = e / NR, r = e % NR;
+      const int c = warp + 8 * q;
+      yv[h] = (e < 8 * NR && c < ncol) ? ldcg_c(x + (int64_t)(first + c0 + c) * NR + r)
+                                       : cmk(0.0, 0.0);
+    }
+    cplx l0[8], l1[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = warp + 8 * q;
+      const cplx* colp = rowp + (int64_t)(c0 + c) * nf;
+      l0[q] = (c < ncol && ok0) ? __ldg(colp) : cmk(0.0, 0.0);
+      l1[q] = (c < ncol && ok1) ? __ldg(colp + 32) : cmk(0.0, 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
-        const cplx y = ldcg_c(x + (int64_t)(first + c) * NR + r);
-        acc0[r] = cfma(l0, y, acc0[r]);
-        acc1[r] = cfma(l1, y, acc1[r]);
+        const int e = q * NR + r;
+        const cplx y = cmk(__shfl_sync(0xffffffffu, yv[e / 32].x, e % 32),
+                           __shfl_sync(0xffffffffu, yv[e / 32].y, e % 32));
+        acc0[r] = cfma(l0[q], y, acc0[r]);
+        acc1[r] = cfma(l1[q], y, acc1[r]);
       }
-    }
   }
 #pragma unroll
   for (int r = 0; r < NR; ++r) {
@@ -123,21 +142,34 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
   }
   __syncthreads();
   if (pivot) {
-    // y_i = t_i + sum_{c<i} X[i][c] t_c ; X[i][c] sits at (row r0+c, col r0+i)
-    if (tid < nr) {
-      const int i = tid;
-      cplx yv[NR];
+    // y_i = t_i + sum_{c<i} X[i][c] t_c ; X[i][c] sits at (row r0+c, col r0+i).
+    // 4 threads per output row (c = k mod 4), shuffle-reduced.
+    const int i = tid >> 2, k = tid & 3;
+    cplx yv[NR];
 #pragma unroll
-      for (int r = 0; r < NR; ++r) yv[r] = v[i][r];
+    for (int r = 0; r < NR; ++r) yv[r] = cmk(0.0, 0.0);
+    if (i < nr) {
       const cplx* xcol = panel + (int64_t)(r0 + i) * nf + r0;
-#pragma unroll 4
-      for (int c = 0; c < i; ++c) {
+#pragma unroll 8
+      for (int c = k; c < i; c += 4) {
         const cplx xv = __ldg(xcol + c);
 #pragma unroll
         for (int r = 0; r < NR; ++r) yv[r] = cfma(xv, v[c][r], yv[r]);
       }
+    }
 #pragma unroll
-      for (int r = 0; r < NR; ++r) x[(int64_t)(first + r0 + i) * NR + r] = yv[r];
+    for (int r = 0; r < NR; ++r) {
+      double a = yv[r].x, b = yv[r].y;
+      a += __shfl_xor_sync(0xffffffffu, a, 1);
+      b += __shfl_xor_sync(0xffffffffu, b, 1);
+      a += __shfl_xor_sync(0xffffffffu, a, 2);
+      b += __shfl_xor_sync(0xffffffffu, b, 2);
+      yv[r] = cmk(a, b);
+    }
+    if (i < nr && k == 0) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        x[(int64_t)(first + r0 + i) * NR + r] = cadd(v[i][r], yv[r]);
       __threadfence();
     }
     __syncthreads();
@@ -153,8 +185,10 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
 
 // Backward task (front s, pivot column block cb), blocks processed from the
 // last one down:  x_cb = X^T (y_cb / d_cb - sum_{rho beyond block} L[rho, cb]^T x_rho).
-// 16 warps x 4 columns; lanes stride the rows; X^T from the diagonal block's
-// upper triangle (coalesced across the column threads).
+// 16 warps x 4 columns; rows are processed in chunks of CH whose x values are
+// gathered into shared memory first (decoupling the rows[] -> x gather from
+// the L stream); each lane then issues 16 independent L loads per chunk.
+constexpr int CH = 64;
 template <int NR>
 __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks, int nslots,
                                              FrontsDev F, SolveBatchDev sb, int* ticket,
@@ -163,6 +197,7 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   extern __shared__ cplx dsm[];
   cplx(*red)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm);
   cplx(*tv)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + PB * NR);
+  cplx(*xs)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + 2 * PB * NR);     // [CH][NR]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_t = atomicAdd(ticket, 1);
   __syncthreads();
@@ -185,42 +220,46 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   const int cw = 4 * warp;
   const int nk = max(0, min(4, ncol - cw));
   const cplx* colp = panel + (int64_t)(c0 + cw) * nf;
-  // border rows (ancestor pivots: final)
-#pragma unroll 2
-  for (int rho = p + lane; rho < nf; rho += 32) {
-    const int g = __ldg(rows + rho);
-    cplx xv[NR];
-#pragma unroll
-    for (int r = 0; r < NR; ++r) xv[r] = ldcg_c(x + (int64_t)g * NR + r);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (k < nk) {
-        const cplx l = __ldg(colp + (int64_t)k * nf + rho);
-#pragma unroll
-        for (int r = 0; r < NR; ++r) acc[k][r] = cfma(l, xv[r], acc[k][r]);
-      }
+
+  auto chunk = [&](int q0, int q1, bool border) {
+    // gather x of rows [q0, q1) into smem
+    const int n = q1 - q0;
+    for (int e = tid; e < n * NR; e += blockDim.x) {
+      const int i = e / NR, r = e % NR;
+      const int g = border ? __ldg(rows + q0 + i) : first + q0 + i;
+      xs[i][r] = ldcg_c(x + (int64_t)g * NR + r);
     }
-  }
-  // later pivot blocks of this front (produced by earlier tickets)
-  for (int rb = npb - 1; rb > cb; --rb) {
-    if (lane == 0)
-      while (ld_acquire(flags + rb) < epoch) __nanosleep(32);
-    __syncwarp();
-    const int q0 = rb * PB, q1 = min(q0 + PB, p);
-#pragma unroll 2
-    for (int rho = q0 + lane; rho < q1; rho += 32) {
-      cplx xv[NR];
+    __syncthreads();
+    cplx lv[CH / 32][4];
 #pragma unroll
-      for (int r = 0; r < NR; ++r) xv[r] = ldcg_c(x + (int64_t)(first + rho) * NR + r);
+    for (int h = 0; h < CH / 32; ++h) {
+      const int i = lane + 32 * h;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        if (k < nk) {
-          const cplx l = __ldg(colp + (int64_t)k * nf + rho);
+      for (int k = 0; k < 4; ++k)
+        lv[h][k] = (i < n && k < nk) ? __ldg(colp + (int64_t)k * nf + q0 + i) : cmk(0.0, 0.0);
+    }
 #pragma unroll
-          for (int r = 0; r < NR; ++r) acc[k][r] = cfma(l, xv[r], acc[k][r]);
+    for (int h = 0; h < CH / 32; ++h) {
+      const int i = lane + 32 * h;
+      if (i < n) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          const cplx xv = xs[i][r];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[k][r] = cfma(lv[h][k], xv, acc[k][r]);
         }
       }
     }
+    __syncthreads();
+  };
+  // border rows (ancestor pivots: final)
+  for (int q0 = p; q0 < nf; q0 += CH) chunk(q0, min(q0 + CH, nf), true);
+  // later pivot blocks of this front (produced by earlier tickets)
+  for (int rb = npb - 1; rb > cb; --rb) {
+    if (tid == 0)
+      while (ld_acquire(flags + rb) < epoch) __nanosleep(32);
+    __syncthreads();
+    chunk(rb * PB, min(rb * PB + PB, p), false);
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k)
@@ -251,22 +290,38 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
     }
   }
   __syncthreads();
-  // x_c = t_c + sum_{i>c} X[i][c] t_i ; X[i][c] sits at (row c0+c, col c0+i)
-  if (tid < ncol) {
-    const int c = tid;
+  // x_c = t_c + sum_{i>c} X[i][c] t_i ; X[i][c] sits at (row c0+c, col c0+i).
+  // 8 threads per column (i = c+1+k mod 8), shuffle-reduced.
+  {
+    const int c = tid >> 3, k = tid & 7;
     cplx xv[NR];
 #pragma unroll
-    for (int r = 0; r < NR; ++r) xv[r] = tv[c][r];
-    const cplx* xrow = panel + c0 + c;
+    for (int r = 0; r < NR; ++r) xv[r] = cmk(0.0, 0.0);
+    if (c < ncol) {
+      const cplx* xrow = panel + c0 + c;
 #pragma unroll 4
-    for (int i = c + 1; i < ncol; ++i) {
-      const cplx w = __ldg(xrow + (int64_t)(c0 + i) * nf);
+      for (int i = c + 1 + k; i < ncol; i += 8) {
+        const cplx w = __ldg(xrow + (int64_t)(c0 + i) * nf);
 #pragma unroll
-      for (int r = 0; r < NR; ++r) xv[r] = cfma(w, tv[i][r], xv[r]);
+        for (int r = 0; r < NR; ++r) xv[r] = cfma(w, tv[i][r], xv[r]);
+      }
     }
 #pragma unroll
-    for (int r = 0; r < NR; ++r) x[(int64_t)(first + c0 + c) * NR + r] = xv[r];
-    __threadfence();
+    for (int r = 0; r < NR; ++r) {
+      double a = xv[r].x, b = xv[r].y;
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+      }
+      xv[r] = cmk(a, b);
+    }
+    if (c < ncol && k == 0) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        x[(int64_t)(first + c0 + c) * NR + r] = cadd(tv[c][r], xv[r]);
+      __threadfence();
+    }
   }
   __syncthreads();
   if (tid == 0) st_release(flags + cb, epoch);
@@ -286,7 +341,7 @@ static void fwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslo
 template <int NR>
 static void bwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
                    const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch) {
-  const size_t smem = (2 * PB * NR) * sizeof(cplx);
+  const size_t smem = (2 * PB * NR + CH * NR) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_bwd<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
