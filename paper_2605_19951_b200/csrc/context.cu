@@ -235,7 +235,7 @@ int ensure_stage(rba_ctx* c, int64_t n) {
 // ---------------------------------------------------------------------------
 int build_plans(rba_ctx* c) {
   const rba::Symbolic& S = c->sym;
-  int panel = 2;                  // 64-column blocks per trailing-update panel
+  int panel = 4;                  // 64-column blocks per trailing-update panel
   if (const char* e = getenv("RBA_PANEL")) panel = std::max(1, atoi(e));
   std::vector<int2> ea;
   std::vector<rba::PanelTask> pt;
@@ -447,7 +447,7 @@ int ensure_slots(rba_ctx* c) {
     CK(cudaMemsetAsync(c->flb[l], 0, (c->nblocks + 1) * sizeof(int), c->st));
     CK(cudaMemsetAsync(c->g[l], 0, (size_t)c->N * c->NRw * sizeof(cplx), c->st));
   }
-  c->fbatch = 1;
+  c->fbatch = std::min(2, nl);
   if (const char* e = getenv("RBA_FACTOR_BATCH")) c->fbatch = std::max(1, std::min(atoi(e), nl));
   c->upd.assign(c->fbatch, nullptr);
   for (int b = 0; b < c->fbatch; ++b)
