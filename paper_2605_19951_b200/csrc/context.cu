@@ -128,7 +128,8 @@ struct rba_ctx {
   // per-kernel-class device time (CUDA events around every launch, enabled
   // by rba_set_timing) and the launch count of this context's kernels
   double cls_ms[16] = {0};
-  bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernel
+  bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernels
+  int gemm_v = 2;             // RBA_GEMM=v1 selects the first DMMA kernel
   int64_t launches = 0;
   std::vector<cudaEvent_t> evpool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -268,7 +269,8 @@ int build_plans(rba_ctx* c) {
         int s = S.level_fronts[q];
         if (S.npiv[s] <= k0) continue;
         int kb = std::min(rba::PB, S.npiv[s] - k0);
-        for (int r0 = k0 + kb; r0 < S.nf[s]; r0 += rba::PB) pt.push_back({s, k0, r0, 0});
+        const int rstep = c->gemm_v == 2 ? 2 * rba::PB : rba::PB;
+        for (int r0 = k0 + kb; r0 < S.nf[s]; r0 += rstep) pt.push_back({s, k0, r0, 0});
       }
       if ((int64_t)pt.size() > toff) c->plan.push_back({ST_TRSM, toff, (int)(pt.size() - toff), 0});
       // trailing update after block kk: inside a panel of `panel` blocks only
@@ -294,7 +296,7 @@ int build_plans(rba_ctx* c) {
         int ntr = (S.nf[s] - clo + rba::GT - 1) / rba::GT;
         int ntc = (chi - clo + rba::GT - 1) / rba::GT;
         int nt = 0;
-        for (int j = 0; j < ntc; ++j) nt += ntr - j;
+        for (int j = 0; j < ntc; ++j) nt += c->gemm_v == 2 ? (ntr - j + 1) / 2 : ntr - j;
         gm.push_back({s, t0, t1, clo, chi, tiles, ntr, 0});
         tiles += nt;
       }
@@ -309,7 +311,10 @@ int build_plans(rba_ctx* c) {
       if (nf <= p || p == 0) continue;
       int ntr = (nf - p + rba::GT - 1) / rba::GT;
       gm.push_back({s, 0, p, p, nf, tiles, ntr, 0});
-      tiles += ntr * (ntr + 1) / 2;
+      if (c->gemm_v == 2)
+        for (int j = 0; j < ntr; ++j) tiles += (ntr - j + 1) / 2;
+      else
+        tiles += ntr * (ntr + 1) / 2;
     }
     if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles});
   }
@@ -395,16 +400,20 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
         Timed t(c, KC_TRSM);
         if (c->gemm_dfma)
           rba::launch_trsm(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
-        else
+        else if (c->gemm_v == 1)
           rba::launch_trsm_dmma(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
+        else
+          rba::launch_trsm2(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
         break;
       }
       case ST_GEMM: {
         Timed t(c, KC_GEMM);
         if (c->gemm_dfma)
           rba::launch_gemm_update(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
-        else
+        else if (c->gemm_v == 1)
           rba::launch_gemm_dmma(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
+        else
+          rba::launch_gemm2(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
         break;
       }
     }
@@ -447,7 +456,12 @@ int ensure_slots(rba_ctx* c) {
     CK(cudaMemsetAsync(c->flb[l], 0, (c->nblocks + 1) * sizeof(int), c->st));
     CK(cudaMemsetAsync(c->g[l], 0, (size_t)c->N * c->NRw * sizeof(cplx), c->st));
   }
-  c->fbatch = std::min(2, nl);
+  {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t need = (size_t)S.upd_total * sizeof(cplx);
+    c->fbatch = (nl >= 2 && fr > 2 * need + ((size_t)4 << 30)) ? 2 : 1;
+  }
   if (const char* e = getenv("RBA_FACTOR_BATCH")) c->fbatch = std::max(1, std::min(atoi(e), nl));
   c->upd.assign(c->fbatch, nullptr);
   for (int b = 0; b < c->fbatch; ++b)
@@ -609,7 +623,10 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     c->own_stream = true;
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
-  if (const char* e = getenv("RBA_GEMM")) c->gemm_dfma = std::string(e) == "dfma";
+  if (const char* e = getenv("RBA_GEMM")) {
+    c->gemm_dfma = std::string(e) == "dfma";
+    if (std::string(e) == "v1" || c->gemm_dfma) c->gemm_v = 1;
+  }
   int rc;
   if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||
       (rc = dalloc(c, c->allocs, &c->red_part, 1024, &c->mem_other)) ||

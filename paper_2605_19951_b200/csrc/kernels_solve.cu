@@ -185,10 +185,8 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
 
 // Backward task (front s, pivot column block cb), blocks processed from the
 // last one down:  x_cb = X^T (y_cb / d_cb - sum_{rho beyond block} L[rho, cb]^T x_rho).
-// 16 warps x 4 columns; rows are processed in chunks of CH whose x values are
-// gathered into shared memory first (decoupling the rows[] -> x gather from
-// the L stream); each lane then issues 16 independent L loads per chunk.
-constexpr int CH = 64;
+// 16 warps x 4 columns, lanes stride the rows; no block barrier in the main
+// loop (the pivot-block waits are per warp).
 template <int NR>
 __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks, int nslots,
                                              FrontsDev F, SolveBatchDev sb, int* ticket,
@@ -197,7 +195,6 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   extern __shared__ cplx dsm[];
   cplx(*red)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm);
   cplx(*tv)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + PB * NR);
-  cplx(*xs)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + 2 * PB * NR);     // [CH][NR]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_t = atomicAdd(ticket, 1);
   __syncthreads();
@@ -221,45 +218,43 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   const int nk = max(0, min(4, ncol - cw));
   const cplx* colp = panel + (int64_t)(c0 + cw) * nf;
 
-  auto chunk = [&](int q0, int q1, bool border) {
-    // gather x of rows [q0, q1) into smem
-    const int n = q1 - q0;
-    for (int e = tid; e < n * NR; e += blockDim.x) {
-      const int i = e / NR, r = e % NR;
-      const int g = border ? __ldg(rows + q0 + i) : first + q0 + i;
-      xs[i][r] = ldcg_c(x + (int64_t)g * NR + r);
-    }
-    __syncthreads();
-    cplx lv[CH / 32][4];
+  // border rows: pivots of ancestors, final before this launch (L1 is
+  // invalidated at launch, so the read-only path is safe); the 16 warps of
+  // the CTA read the same x rows, which therefore hit in L1.
+#pragma unroll 2
+  for (int rho = p + lane; rho < nf; rho += 32) {
+    const int g = __ldg(rows + rho);
+    cplx lv[4];
 #pragma unroll
-    for (int h = 0; h < CH / 32; ++h) {
-      const int i = lane + 32 * h;
+    for (int k = 0; k < 4; ++k)
+      lv[k] = k < nk ? __ldg(colp + (int64_t)k * nf + rho) : cmk(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const cplx xv = __ldg(x + (int64_t)g * NR + r);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k][r] = cfma(lv[k], xv, acc[k][r]);
+    }
+  }
+  // later pivot blocks of this front (produced by earlier tickets in this
+  // launch): per-warp wait, L2 reads
+  for (int rb = npb - 1; rb > cb; --rb) {
+    if (lane == 0)
+      while (ld_acquire(flags + rb) < epoch) __nanosleep(32);
+    __syncwarp();
+    const int q0 = rb * PB, q1 = min(q0 + PB, p);
+#pragma unroll 2
+    for (int rho = q0 + lane; rho < q1; rho += 32) {
+      cplx lv[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        lv[h][k] = (i < n && k < nk) ? __ldg(colp + (int64_t)k * nf + q0 + i) : cmk(0.0, 0.0);
-    }
+        lv[k] = k < nk ? __ldg(colp + (int64_t)k * nf + rho) : cmk(0.0, 0.0);
 #pragma unroll
-    for (int h = 0; h < CH / 32; ++h) {
-      const int i = lane + 32 * h;
-      if (i < n) {
+      for (int r = 0; r < NR; ++r) {
+        const cplx xv = ldcg_c(x + (int64_t)(first + rho) * NR + r);
 #pragma unroll
-        for (int r = 0; r < NR; ++r) {
-          const cplx xv = xs[i][r];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) acc[k][r] = cfma(lv[h][k], xv, acc[k][r]);
-        }
+        for (int k = 0; k < 4; ++k) acc[k][r] = cfma(lv[k], xv, acc[k][r]);
       }
     }
-    __syncthreads();
-  };
-  // border rows (ancestor pivots: final)
-  for (int q0 = p; q0 < nf; q0 += CH) chunk(q0, min(q0 + CH, nf), true);
-  // later pivot blocks of this front (produced by earlier tickets)
-  for (int rb = npb - 1; rb > cb; --rb) {
-    if (tid == 0)
-      while (ld_acquire(flags + rb) < epoch) __nanosleep(32);
-    __syncthreads();
-    chunk(rb * PB, min(rb * PB + PB, p), false);
   }
 #pragma unroll
   for (int k = 0; k < 4; ++k)
@@ -341,7 +336,7 @@ static void fwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslo
 template <int NR>
 static void bwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
                    const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch) {
-  const size_t smem = (2 * PB * NR + CH * NR) * sizeof(cplx);
+  const size_t smem = (2 * PB * NR) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_bwd<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
