@@ -129,7 +129,7 @@ struct rba_ctx {
   // by rba_set_timing) and the launch count of this context's kernels
   double cls_ms[16] = {0};
   bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernels
-  int gemm_v = 2;             // RBA_GEMM=v1 selects the first DMMA kernel
+  int gemm_v = 1;             // RBA_GEMM=v2 selects the cp.async 128x64 kernel
   int64_t launches = 0;
   std::vector<cudaEvent_t> evpool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -626,6 +626,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   if (const char* e = getenv("RBA_GEMM")) {
     c->gemm_dfma = std::string(e) == "dfma";
     if (std::string(e) == "v1" || c->gemm_dfma) c->gemm_v = 1;
+    if (std::string(e) == "v2") c->gemm_v = 2;
   }
   int rc;
   if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||

@@ -13,6 +13,8 @@
 #include "fronts.cuh"
 #include "kernels.h"
 
+#include <cstdlib>
+
 namespace rba {
 
 namespace {
@@ -43,8 +45,8 @@ struct Stage {
 // MODE 0: trailing/Schur update  C[r,c] -= sum_t (L[r,t] d_t) L[c,t]  (r >= c)
 // MODE 1: panel TRSM  L[r, k0+c] = (sum_{t<=c} F[r, k0+t] X[c][t]) / d_c, with
 //         X = L_kk^{-1} read from the diagonal block's upper triangle (k_diag).
-template <int MODE>
-__global__ void __launch_bounds__(NT) k_gemm_dmma(const GemmTask* __restrict__ tasks, int ntasks,
+template <int MODE, int NW>
+__global__ void __launch_bounds__(32 * NW) k_gemm_dmma(const GemmTask* __restrict__ tasks, int ntasks,
                                                   const PanelTask* __restrict__ ptasks,
                                                   FrontsDev F, PoleBatch pb) {
   extern __shared__ __align__(16) double smraw[];
@@ -80,27 +82,30 @@ __global__ void __launch_bounds__(NT) k_gemm_dmma(const GemmTask* __restrict__ t
   const cplx* __restrict__ panel = pb.factor[slot] + F.panel_off[s];
   cplx* pw = pb.factor[slot] + F.panel_off[s];
   cplx* upd = pb.upd[slot] + (F.upd_off[s] >= 0 ? F.upd_off[s] : 0);
+  constexpr int NTH = 32 * NW;            // threads
+  constexpr int NB = NW == 4 ? 4 : 2;      // 8-wide n-tiles per warp (32 or 16 columns)
+  constexpr int PER = (GT * TK) / NTH;     // staged elements per thread per operand
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;   // warp tile origin
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * (8 * NB);   // warp tile origin
   const int g = lane >> 2, t4 = lane & 3;
 
   // accumulators: [mi][ni] 8x8 tiles, re and im, 2 doubles each
-  double cre[4][4][2], cim[4][4][2];
+  double cre[4][NB][2], cim[4][NB][2];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
+    for (int b = 0; b < NB; ++b) {
       cre[a][b][0] = cre[a][b][1] = 0.0;
       cim[a][b][0] = cim[a][b][1] = 0.0;
     }
 
   // staging: each thread loads 8 A and 8 B complex per chunk:
   // element e = tid + q*NT (q < 8) -> row = e % 64, k = e / 64
-  cplx pa[8], pbv[8];
+  cplx pa[PER], pbv[PER];
   auto gload = [&](int kt) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = tid + q * NT;
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * NTH;
       const int rr = e & (GT - 1), kk = e >> 6;
       const int t = kt + kk;
       cplx a = cmk(0.0, 0.0), b = cmk(0.0, 0.0);
@@ -136,8 +141,8 @@ __global__ void __launch_bounds__(NT) k_gemm_dmma(const GemmTask* __restrict__ t
   auto sstore = [&](int buf) {
     Stage& S = st[buf];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int e = tid + q * NT;
+    for (int q = 0; q < PER; ++q) {
+      const int e = tid + q * NTH;
       const int rr = e & (GT - 1), kk = e >> 6;
       const cplx a = cmul(pa[q], ds[buf][kk]);
       S.are[rr * LDK + kk] = a.x;
@@ -163,7 +168,7 @@ __global__ void __launch_bounds__(NT) k_gemm_dmma(const GemmTask* __restrict__ t
     const Stage& S = st[buf];
 #pragma unroll
     for (int k4 = 0; k4 < TK; k4 += 4) {
-      double ar[4], ai[4], an[4], br[4], bi[4];
+      double ar[4], ai[4], an[4], br[NB], bi[NB];
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
         const int idx = (wm + a * 8 + g) * LDK + k4 + t4;
@@ -172,7 +177,7 @@ __global__ void __launch_bounds__(NT) k_gemm_dmma(const GemmTask* __restrict__ t
         an[a] = -ai[a];
       }
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
+      for (int b = 0; b < NB; ++b) {
         const int idx = (wn + b * 8 + g) * LDK + k4 + t4;
         br[b] = S.bre[idx];
         bi[b] = S.bim[idx];
@@ -180,7 +185,7 @@ __global__ void __launch_bounds__(NT) k_gemm_dmma(const GemmTask* __restrict__ t
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
+        for (int b = 0; b < NB; ++b) {
           dmma(cre[a][b][0], cre[a][b][1], ar[a], br[b]);
           dmma(cre[a][b][0], cre[a][b][1], an[a], bi[b]);
           dmma(cim[a][b][0], cim[a][b][1], ar[a], bi[b]);
@@ -194,30 +199,36 @@ __global__ void __launch_bounds__(NT) k_gemm_dmma(const GemmTask* __restrict__ t
     __syncthreads();
   }
   if (MODE == 0) {
-    // epilogue: C -= acc  (lower triangle only)
+    // epilogue: C -= acc  (lower triangle only).  The 8 C values of one
+    // m-tile row are loaded together before any store (the stores may alias
+    // later loads as far as the compiler knows: batching avoids 32 serial
+    // round trips per thread).
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < 4; ++a) {
+      cplx* dst[NB][2];
+      cplx cv[NB][2];
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
+      for (int b = 0; b < NB; ++b)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int r = r0 + wm + a * 8 + g;
           const int c = cc0 + wn + b * 8 + t4 * 2 + h;
-          if (r < nf && c < cmax && r >= c) {
-            cplx* dst = faddr(pw, upd, p, nf, r, c);
-            cplx v = *dst;
-            v.x -= cre[a][b][h];
-            v.y -= cim[a][b][h];
-            *dst = v;
-          }
+          dst[b][h] = (r < nf && c < cmax && r >= c) ? faddr(pw, upd, p, nf, r, c) : nullptr;
+          cv[b][h] = dst[b][h] ? __ldcg(dst[b][h]) : cmk(0.0, 0.0);
         }
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (dst[b][h]) *dst[b][h] = cmk(cv[b][h].x - cre[a][b][h], cv[b][h].y - cim[a][b][h]);
+    }
   } else {
     // epilogue: L = (F X^T) D^{-1}, written in place (every A element of this
     // tile was staged before any write: the K loop ended with a barrier)
 #pragma unroll
     for (int a = 0; a < 4; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
+      for (int b = 0; b < NB; ++b)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int r = r0 + wm + a * 8 + g;
@@ -228,17 +239,24 @@ __global__ void __launch_bounds__(NT) k_gemm_dmma(const GemmTask* __restrict__ t
   }
 }
 
+int g_dmma_warps = 4;   // RBA_GEMM_WARPS=8 selects 32x16 warp tiles (8 warps/CTA)
+
 void launch_gemm_dmma(cudaStream_t st, const GemmTask* tasks, int ntasks, int ntiles,
                       const FrontsDev& F, const PoleBatch& pb) {
   if (ntasks <= 0 || ntiles <= 0) return;
   const size_t smem = 2 * sizeof(Stage);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_dmma<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_gemm_dmma<0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_gemm_dmma<0, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (const char* e = getenv("RBA_GEMM_WARPS")) g_dmma_warps = atoi(e) == 8 ? 8 : 4;
     attr = true;
   }
   dim3 grid(ntiles, pb.count);
-  k_gemm_dmma<0><<<grid, NT, smem, st>>>(tasks, ntasks, nullptr, F, pb);
+  if (g_dmma_warps == 8)
+    k_gemm_dmma<0, 8><<<grid, 256, smem, st>>>(tasks, ntasks, nullptr, F, pb);
+  else
+    k_gemm_dmma<0, 4><<<grid, 128, smem, st>>>(tasks, ntasks, nullptr, F, pb);
 }
 
 void launch_trsm_dmma(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
@@ -247,11 +265,11 @@ void launch_trsm_dmma(cudaStream_t st, const PanelTask* tasks, int ntasks, const
   const size_t smem = 2 * sizeof(Stage);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_dmma<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_gemm_dmma<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   dim3 grid(ntasks, pb.count);
-  k_gemm_dmma<1><<<grid, NT, smem, st>>>(nullptr, 0, tasks, F, pb);
+  k_gemm_dmma<1, 4><<<grid, 128, smem, st>>>(nullptr, 0, tasks, F, pb);
 }
 
 
