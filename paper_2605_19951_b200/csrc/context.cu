@@ -80,7 +80,11 @@ struct rba_ctx {
   rba::PanelTask* pt_tasks = nullptr;
   rba::GemmTask* gm_tasks = nullptr;
   std::vector<std::pair<int64_t, int>> fwd_lv, bwd_lv;
-  rba::SolveTask *fwd_tasks = nullptr, *bwd_tasks = nullptr;
+  rba::SolveTask *fwd_tasks = nullptr, *bwd_tasks = nullptr, *bwd_all = nullptr;
+  int64_t n_fwd_tasks = 0, n_bwd_tasks = 0;
+  int32_t *parent_d = nullptr, *need_u_d = nullptr;
+  int epoch_limit = 1 << 20;  // flags/counters are monotonic in the epoch; reset before overflow
+  bool fused_sweep = true;    // RBA_SWEEP=levels: one launch per level instead
   int* tickets = nullptr;
   int64_t nblocks = 0;
   // observation / sources
@@ -101,7 +105,7 @@ struct rba_ctx {
   std::vector<void*> pole_allocs;
   // per local slot
   std::vector<cplx*> factor, g, x, uvec;
-  std::vector<int*> flf, flb;
+  std::vector<int*> flf, flb, dnf, dnb;
   std::vector<char> valid;
   int NRw = 1;
   std::vector<cplx*> upd;
@@ -213,6 +217,7 @@ void free_slots(rba_ctx* c) {
   free_list(c->pole_allocs);
   c->factor.clear(); c->g.clear(); c->x.clear(); c->uvec.clear();
   c->flf.clear(); c->flb.clear(); c->valid.clear(); c->upd.clear();
+  c->dnf.clear(); c->dnb.clear();
   c->wa = nullptr;
   c->pole_of_slot = nullptr;
   c->slot_map = nullptr;
@@ -361,6 +366,24 @@ int build_plans(rba_ctx* c) {
   }
   if ((rc = upload(c, c->allocs, &c->fwd_tasks, ft.data(), ft.size()))) return rc;
   if ((rc = upload(c, c->allocs, &c->bwd_tasks, bt.data(), bt.size()))) return rc;
+  {
+    // fused backward: levels top-down in one task list
+    std::vector<rba::SolveTask> ba;
+    for (int L = S.nlevels - 1; L >= 0; --L)
+      ba.insert(ba.end(), bt.begin() + c->bwd_lv[L].first,
+                bt.begin() + c->bwd_lv[L].first + c->bwd_lv[L].second);
+    if ((rc = upload(c, c->allocs, &c->bwd_all, ba.data(), ba.size()))) return rc;
+    c->n_fwd_tasks = ft.size();
+    c->n_bwd_tasks = ba.size();
+    std::vector<int32_t> need(S.nfront, 0);
+    for (int ch = 0; ch < S.nfront; ++ch)
+      if (S.parent[ch] >= 0) need[S.parent[ch]] += (S.nf[ch] - S.npiv[ch] + rba::PB - 1) / rba::PB;
+    if ((rc = upload(c, c->allocs, &c->need_u_d, need.data(), need.size()))) return rc;
+    int mx = 1;
+    for (int s2 = 0; s2 < S.nfront; ++s2) mx = std::max({mx, need[s2], (S.npiv[s2] + rba::PB - 1) / rba::PB});
+    c->epoch_limit = std::max(1, (1 << 30) / mx);
+    if ((rc = upload(c, c->allocs, &c->parent_d, S.parent.data(), S.parent.size()))) return rc;
+  }
   if ((rc = dalloc(c, c->allocs, &c->tickets, 2 * (size_t)S.nlevels + 2, &c->mem_other))) return rc;
 
   // solve gather lists (child u-vector rows -> parent front rows), child order
@@ -443,6 +466,7 @@ int ensure_slots(rba_ctx* c) {
   int rc;
   c->factor.assign(nl, nullptr); c->g.assign(nl, nullptr); c->x.assign(nl, nullptr);
   c->uvec.assign(nl, nullptr); c->flf.assign(nl, nullptr); c->flb.assign(nl, nullptr);
+  c->dnf.assign(nl, nullptr); c->dnb.assign(nl, nullptr);
   c->valid.assign(nl, 0);
   c->NRw = c->NRs;
   for (int l = 0; l < nl; ++l) {
@@ -452,6 +476,10 @@ int ensure_slots(rba_ctx* c) {
     if ((rc = dalloc(c, c->pole_allocs, &c->uvec[l], (size_t)std::max<int64_t>(S.uvec_off[S.nfront], 1) * c->NRw, &c->mem_work))) return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->flf[l], (size_t)c->nblocks + 1, &c->mem_work))) return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->flb[l], (size_t)c->nblocks + 1, &c->mem_work))) return rc;
+    if ((rc = dalloc(c, c->pole_allocs, &c->dnf[l], (size_t)S.nfront + 1, &c->mem_work))) return rc;
+    if ((rc = dalloc(c, c->pole_allocs, &c->dnb[l], (size_t)S.nfront + 1, &c->mem_work))) return rc;
+    CK(cudaMemsetAsync(c->dnf[l], 0, (S.nfront + 1) * sizeof(int), c->st));
+    CK(cudaMemsetAsync(c->dnb[l], 0, (S.nfront + 1) * sizeof(int), c->st));
     CK(cudaMemsetAsync(c->flf[l], 0, (c->nblocks + 1) * sizeof(int), c->st));
     CK(cudaMemsetAsync(c->flb[l], 0, (c->nblocks + 1) * sizeof(int), c->st));
     CK(cudaMemsetAsync(c->g[l], 0, (size_t)c->N * c->NRw * sizeof(cplx), c->st));
@@ -486,23 +514,52 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR) {
     b.uvec[i] = c->uvec[l];
     b.flags_f[i] = c->flf[l];
     b.flags_b[i] = c->flb[l];
+    b.done_f[i] = c->dnf[l];
+    b.done_b[i] = c->dnb[l];
   }
   const rba::Symbolic& S = c->sym;
+  if (c->epoch + 1 >= c->epoch_limit) {
+    for (size_t l = 0; l < c->flf.size(); ++l) {
+      CK(cudaMemsetAsync(c->flf[l], 0, (c->nblocks + 1) * sizeof(int), c->st));
+      CK(cudaMemsetAsync(c->flb[l], 0, (c->nblocks + 1) * sizeof(int), c->st));
+      CK(cudaMemsetAsync(c->dnf[l], 0, (S.nfront + 1) * sizeof(int), c->st));
+      CK(cudaMemsetAsync(c->dnb[l], 0, (S.nfront + 1) * sizeof(int), c->st));
+    }
+    c->epoch = 0;
+  }
   c->epoch++;
   CK(cudaMemsetAsync(c->tickets, 0, (2 * (size_t)S.nlevels + 2) * sizeof(int), c->st));
   if (c->timing) cudaEventRecord(c->ev[0], c->st);
-  for (int L = 0; L < S.nlevels; ++L) {
-    Timed tm(c, KC_FWD);
-    rba::launch_solve_level(c->st, true, NR, c->fwd_tasks + c->fwd_lv[L].first, c->fwd_lv[L].second,
-                            ns, c->F, b, c->tickets + L, c->epoch);
+  if (c->fused_sweep) {
+    {
+      Timed tm(c, KC_FWD);
+      rba::launch_solve_level(c->st, true, NR, c->fwd_tasks, (int)c->n_fwd_tasks, ns, c->F, b,
+                              c->tickets, c->epoch, c->parent_d, c->need_u_d, true);
+    }
     CKL();
-  }
-  if (c->timing) cudaEventRecord(c->ev[1], c->st);
-  for (int L = S.nlevels - 1; L >= 0; --L) {
-    Timed tm(c, KC_BWD);
-    rba::launch_solve_level(c->st, false, NR, c->bwd_tasks + c->bwd_lv[L].first, c->bwd_lv[L].second,
-                            ns, c->F, b, c->tickets + S.nlevels + L, c->epoch);
+    if (c->timing) cudaEventRecord(c->ev[1], c->st);
+    {
+      Timed tm(c, KC_BWD);
+      rba::launch_solve_level(c->st, false, NR, c->bwd_all, (int)c->n_bwd_tasks, ns, c->F, b,
+                              c->tickets + 1, c->epoch, c->parent_d, c->need_u_d, true);
+    }
     CKL();
+  } else {
+    for (int L = 0; L < S.nlevels; ++L) {
+      Timed tm(c, KC_FWD);
+      rba::launch_solve_level(c->st, true, NR, c->fwd_tasks + c->fwd_lv[L].first,
+                              c->fwd_lv[L].second, ns, c->F, b, c->tickets + L, c->epoch,
+                              c->parent_d, c->need_u_d, false);
+      CKL();
+    }
+    if (c->timing) cudaEventRecord(c->ev[1], c->st);
+    for (int L = S.nlevels - 1; L >= 0; --L) {
+      Timed tm(c, KC_BWD);
+      rba::launch_solve_level(c->st, false, NR, c->bwd_tasks + c->bwd_lv[L].first,
+                              c->bwd_lv[L].second, ns, c->F, b, c->tickets + S.nlevels + L,
+                              c->epoch, c->parent_d, c->need_u_d, false);
+      CKL();
+    }
   }
   if (c->timing) {
     cudaEventRecord(c->ev[2], c->st);
@@ -628,6 +685,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     if (std::string(e) == "v1" || c->gemm_dfma) c->gemm_v = 1;
     if (std::string(e) == "v2") c->gemm_v = 2;
   }
+  if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) != "levels";
   int rc;
   if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||
       (rc = dalloc(c, c->allocs, &c->red_part, 1024, &c->mem_other)) ||

@@ -18,6 +18,8 @@ struct SolveBatch {
   cplx* uvec[32];
   int* flags_f[32];
   int* flags_b[32];
+  int* done_f[32];
+  int* done_b[32];
 };
 
 // factorisation
@@ -48,7 +50,8 @@ void launch_trsm2(cudaStream_t st, const PanelTask* tasks, int ntasks, const Fro
 // solves
 void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* tasks,
                         int ntasks, int nslots, const FrontsDev& F, const SolveBatch& b,
-                        int* ticket, int epoch);
+                        int* ticket, int epoch, const int32_t* parent, const int32_t* need_u,
+                        bool fused);
 void launch_perm_in(cudaStream_t st, int64_t n, int nrhs, int NR, const int32_t* perm,
                     const cplx* b, int64_t ldb, cplx* x);
 void launch_perm_out(cudaStream_t st, int64_t n, int nrhs, int NR, const int32_t* perm,

@@ -20,6 +20,14 @@ struct SolveBatchDev {
   cplx* x[32];
   cplx* uvec[32];
   int* flags[32];
+  int* done[32];      // fused sweeps: per-front completion counters (monotonic)
+};
+
+// Cross-front dependencies of the fused (single-launch) sweeps.
+struct SweepDeps {
+  const int32_t* parent;   // front parent (-1 root)
+  const int32_t* need_u;   // forward: border tasks of all children of the front
+  int fused;
 };
 
 __device__ __forceinline__ cplx ldcg_c(const cplx* p) { return __ldcg(p); }
@@ -39,7 +47,7 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 template <int NR>
 __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks, int nslots,
                                              FrontsDev F, SolveBatchDev sb, int* ticket,
-                                             int epoch) {
+                                             int epoch, SweepDeps dep) {
   __shared__ int s_t;
   extern __shared__ cplx dsm[];
   cplx(*v)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm);
@@ -61,6 +69,15 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
   const int r0 = pivot ? blk * PB : p + (blk - npb) * PB;
   const int nr = pivot ? min(PB, p - r0) : min(PB, nf - r0);
   const int jmax = pivot ? blk : npb;
+  if (dep.fused) {
+    // every child's border (u-vector) tasks must have completed
+    const int need = dep.need_u[s];
+    if (need > 0) {
+      if (tid == 0)
+        while (ld_acquire(sb.done[slot] + s) < epoch * need) __nanosleep(64);
+      __syncthreads();
+    }
+  }
 
   if (tid < nr) {
     const int rho = r0 + tid;
@@ -179,6 +196,11 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
       cplx* u = sb.uvec[slot] + (F.uvec_off[s] + (r0 - p) + tid) * NR;
 #pragma unroll
       for (int r = 0; r < NR; ++r) u[r] = v[tid][r];
+      __threadfence();
+    }
+    if (dep.fused) {
+      __syncthreads();
+      if (tid == 0) atomicAdd(sb.done[slot] + dep.parent[s], 1);
     }
   }
 }
@@ -190,7 +212,7 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
 template <int NR>
 __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks, int nslots,
                                              FrontsDev F, SolveBatchDev sb, int* ticket,
-                                             int epoch) {
+                                             int epoch, SweepDeps dep) {
   __shared__ int s_t;
   extern __shared__ cplx dsm[];
   cplx(*red)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm);
@@ -217,6 +239,15 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   const int cw = 4 * warp;
   const int nk = max(0, min(4, ncol - cw));
   const cplx* colp = panel + (int64_t)(c0 + cw) * nf;
+  if (dep.fused && nf > p) {
+    // border rows are final once the parent front is complete (its own tasks
+    // waited for every owner of its border)
+    const int par = dep.parent[s];
+    const int need = (F.npiv[par] + PB - 1) / PB;
+    if (tid == 0)
+      while (ld_acquire(sb.done[slot] + par) < epoch * need) __nanosleep(64);
+    __syncthreads();
+  }
 
   // border rows: pivots of ancestors, final before this launch (L1 is
   // invalidated at launch, so the read-only path is safe); the 16 warps of
@@ -319,35 +350,41 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
     }
   }
   __syncthreads();
-  if (tid == 0) st_release(flags + cb, epoch);
+  if (tid == 0) {
+    st_release(flags + cb, epoch);
+    if (dep.fused) atomicAdd(sb.done[slot] + s, 1);
+  }
 }
 
 template <int NR>
 static void fwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
-                   const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch) {
+                   const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch,
+                   const SweepDeps& dep) {
   const size_t smem = (9 * PB * NR) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fwd<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_fwd<NR><<<ntasks * nslots, 256, smem, st>>>(tasks, nslots, F, sb, ticket, epoch);
+  k_fwd<NR><<<ntasks * nslots, 256, smem, st>>>(tasks, nslots, F, sb, ticket, epoch, dep);
 }
 template <int NR>
 static void bwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
-                   const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch) {
+                   const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch,
+                   const SweepDeps& dep) {
   const size_t smem = (2 * PB * NR) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_bwd<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_bwd<NR><<<ntasks * nslots, 512, smem, st>>>(tasks, nslots, F, sb, ticket, epoch);
+  k_bwd<NR><<<ntasks * nslots, 512, smem, st>>>(tasks, nslots, F, sb, ticket, epoch, dep);
 }
 
 void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* tasks,
                         int ntasks, int nslots, const FrontsDev& F, const SolveBatch& b,
-                        int* ticket, int epoch) {
+                        int* ticket, int epoch, const int32_t* parent, const int32_t* need_u,
+                        bool fused) {
   if (ntasks <= 0) return;
   SolveBatchDev sb;
   for (int i = 0; i < nslots; ++i) {
@@ -355,16 +392,18 @@ void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* 
     sb.x[i] = b.x[i];
     sb.uvec[i] = b.uvec[i];
     sb.flags[i] = forward ? b.flags_f[i] : b.flags_b[i];
+    sb.done[i] = forward ? b.done_f[i] : b.done_b[i];
   }
+  SweepDeps dep{parent, need_u, fused ? 1 : 0};
   switch (nr) {
-    case 1: forward ? fwd_nr<1>(st, tasks, ntasks, nslots, F, sb, ticket, epoch)
-                    : bwd_nr<1>(st, tasks, ntasks, nslots, F, sb, ticket, epoch); break;
-    case 2: forward ? fwd_nr<2>(st, tasks, ntasks, nslots, F, sb, ticket, epoch)
-                    : bwd_nr<2>(st, tasks, ntasks, nslots, F, sb, ticket, epoch); break;
-    case 4: forward ? fwd_nr<4>(st, tasks, ntasks, nslots, F, sb, ticket, epoch)
-                    : bwd_nr<4>(st, tasks, ntasks, nslots, F, sb, ticket, epoch); break;
-    default: forward ? fwd_nr<8>(st, tasks, ntasks, nslots, F, sb, ticket, epoch)
-                     : bwd_nr<8>(st, tasks, ntasks, nslots, F, sb, ticket, epoch); break;
+    case 1: forward ? fwd_nr<1>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep)
+                    : bwd_nr<1>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep); break;
+    case 2: forward ? fwd_nr<2>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep)
+                    : bwd_nr<2>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep); break;
+    case 4: forward ? fwd_nr<4>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep)
+                    : bwd_nr<4>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep); break;
+    default: forward ? fwd_nr<8>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep)
+                     : bwd_nr<8>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep); break;
   }
 }
 

@@ -66,3 +66,23 @@ def test_dmma_gemm_matches_dfma_reference(gpu, monkeypatch):
     # uses the inverted diagonal block: rounding-level differences only
     assert rel(out[1], out[0]) <= 1e-10
     assert rel(out[2], out[0]) <= 1e-10
+
+
+def test_fused_sweep_equals_level_sweeps(gpu, monkeypatch):
+    """The single-launch solve sweeps (cross-front counters) give bitwise the
+    same solutions as one launch per level (same arithmetic order)."""
+    prob, _ = rb.build_config("C3", n=8)
+    approx = rb.config_approximant("C3")
+    model = prob.true_model()
+    outs = []
+    for mode in ("levels", "fused"):
+        monkeypatch.setenv("RBA_SWEEP", mode)
+        cache = rb.ShiftedFactorCache()
+        d = rb.forward_response(prob, model, approx, cache).data
+        opr = rb.JacobianOperator(prob, model, approx, cache)
+        v = np.random.default_rng(1).standard_normal(opr.shape[1])
+        w = np.random.default_rng(2).standard_normal(opr.shape[0])
+        outs.append((d, opr.jvp(v), opr.vjp(w)))
+        cache.engine.close()
+    for a, b in zip(*outs):
+        np.testing.assert_array_equal(a, b)
