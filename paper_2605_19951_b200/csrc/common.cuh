@@ -53,4 +53,16 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Spin until *p >= target.  Dependencies always point to tasks with smaller
+// tickets, so the wait is bounded; as a guard against a logic error a wait
+// longer than ~20 s (at 2 GHz) traps instead of hanging the GPU.
+__device__ __forceinline__ void spin_wait_geq(const int* p, int target) {
+  if (ld_acquire(p) >= target) return;
+  const long long t0 = clock64();
+  while (ld_acquire(p) < target) {
+    __nanosleep(64);
+    if (clock64() - t0 > 40000000000LL) __trap();
+  }
+}
+
 }  // namespace rba

@@ -85,6 +85,7 @@ struct rba_ctx {
   int32_t *parent_d = nullptr, *need_u_d = nullptr;
   int epoch_limit = 1 << 20;  // flags/counters are monotonic in the epoch; reset before overflow
   bool fused_sweep = true;    // RBA_SWEEP=levels: one launch per level instead
+  bool diag_v1 = false;       // RBA_DIAG=v1: unblocked diagonal-block kernel
   int* tickets = nullptr;
   int64_t nblocks = 0;
   // observation / sources
@@ -106,6 +107,7 @@ struct rba_ctx {
   // per local slot
   std::vector<cplx*> factor, g, x, uvec;
   std::vector<int*> flf, flb, dnf, dnb;
+  std::vector<int> slot_epoch;    // solves issued per local slot (flags / counters)
   std::vector<char> valid;
   int NRw = 1;
   std::vector<cplx*> upd;
@@ -217,7 +219,7 @@ void free_slots(rba_ctx* c) {
   free_list(c->pole_allocs);
   c->factor.clear(); c->g.clear(); c->x.clear(); c->uvec.clear();
   c->flf.clear(); c->flb.clear(); c->valid.clear(); c->upd.clear();
-  c->dnf.clear(); c->dnb.clear();
+  c->dnf.clear(); c->dnb.clear(); c->slot_epoch.clear();
   c->wa = nullptr;
   c->pole_of_slot = nullptr;
   c->slot_map = nullptr;
@@ -418,7 +420,14 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
   for (const Step& s : c->plan) {
     switch (s.kind) {
       case ST_EA: { Timed t(c, KC_EA); rba::launch_extend_add(c->st, c->ea_tasks + s.off, s.n, c->F, pb); break; }
-      case ST_DIAG: { Timed t(c, KC_DIAG); rba::launch_diag(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d); break; }
+      case ST_DIAG: {
+        Timed t(c, KC_DIAG);
+        if (c->diag_v1)
+          rba::launch_diag(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d);
+        else
+          rba::launch_diag2(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d);
+        break;
+      }
       case ST_TRSM: {
         Timed t(c, KC_TRSM);
         if (c->gemm_dfma)
@@ -467,6 +476,7 @@ int ensure_slots(rba_ctx* c) {
   c->factor.assign(nl, nullptr); c->g.assign(nl, nullptr); c->x.assign(nl, nullptr);
   c->uvec.assign(nl, nullptr); c->flf.assign(nl, nullptr); c->flb.assign(nl, nullptr);
   c->dnf.assign(nl, nullptr); c->dnb.assign(nl, nullptr);
+  c->slot_epoch.assign(nl, 0);
   c->valid.assign(nl, 0);
   c->NRw = c->NRs;
   for (int l = 0; l < nl; ++l) {
@@ -518,14 +528,16 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR) {
     b.done_b[i] = c->dnb[l];
   }
   const rba::Symbolic& S = c->sym;
-  if (c->epoch + 1 >= c->epoch_limit) {
-    for (size_t l = 0; l < c->flf.size(); ++l) {
+  for (int i = 0; i < ns; ++i) {
+    const int l = slots[i];
+    if (c->slot_epoch[l] + 1 >= c->epoch_limit) {
       CK(cudaMemsetAsync(c->flf[l], 0, (c->nblocks + 1) * sizeof(int), c->st));
       CK(cudaMemsetAsync(c->flb[l], 0, (c->nblocks + 1) * sizeof(int), c->st));
       CK(cudaMemsetAsync(c->dnf[l], 0, (S.nfront + 1) * sizeof(int), c->st));
       CK(cudaMemsetAsync(c->dnb[l], 0, (S.nfront + 1) * sizeof(int), c->st));
+      c->slot_epoch[l] = 0;
     }
-    c->epoch = 0;
+    b.epoch[i] = ++c->slot_epoch[l];
   }
   c->epoch++;
   CK(cudaMemsetAsync(c->tickets, 0, (2 * (size_t)S.nlevels + 2) * sizeof(int), c->st));
@@ -686,6 +698,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     if (std::string(e) == "v2") c->gemm_v = 2;
   }
   if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) != "levels";
+  if (const char* e = getenv("RBA_DIAG")) c->diag_v1 = std::string(e) == "v1";
   int rc;
   if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||
       (rc = dalloc(c, c->allocs, &c->red_part, 1024, &c->mem_other)) ||

@@ -20,6 +20,7 @@ struct SolveBatch {
   int* flags_b[32];
   int* done_f[32];
   int* done_b[32];
+  int epoch[32];
 };
 
 // factorisation
@@ -34,6 +35,8 @@ void launch_extend_add(cudaStream_t st, const int2* tasks, int ntasks, const Fro
                        const PoleBatch& pb);
 void launch_diag(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
                  const PoleBatch& pb, int* err);
+void launch_diag2(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
+                  const PoleBatch& pb, int* err);
 void launch_trsm(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
                  const PoleBatch& pb);
 void launch_gemm_update(cudaStream_t st, const GemmTask* tasks, int ntasks, int ntiles,

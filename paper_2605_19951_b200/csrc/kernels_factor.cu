@@ -178,6 +178,136 @@ __global__ void __launch_bounds__(256) k_diag(const PanelTask* __restrict__ task
   }
 }
 
+// K4a (v2): the same diagonal-block LDL^T + inverse, blocked by 16 so that
+// only ~20 block barriers remain (v1: two per pivot).  Warp 0 factors each
+// 16x16 diagonal sub-block with warp barriers, all threads do the sub-panel
+// TRSM and the trailing update; the inverse is built block-row by block-row
+// (X_ij = -X_ii sum_k L_ik X_kj).
+constexpr int SB = 16;
+
+__global__ void __launch_bounds__(256) k_diag2(const PanelTask* __restrict__ tasks, FrontsDev F,
+                                               PoleBatch pb, int* err) {
+  extern __shared__ cplx sm[];
+  cplx* Dg = sm;                   // [PB][LDS]
+  cplx* Xs = sm + PB * LDS;        // [PB][LDS]
+  cplx* Ts = sm + 2 * PB * LDS;    // [PB][LDS]
+  cplx* dv = sm + 3 * PB * LDS;    // [PB]
+  cplx* di = dv + PB;              // [PB]
+  const int slot = blockIdx.y;
+  const PanelTask tk = tasks[blockIdx.x];
+  const int s = tk.s, k0 = tk.k0;
+  const int nf = F.nf[s], p = F.npiv[s];
+  const int kb = min(PB, p - k0);
+  cplx* panel = pb.factor[slot] + F.panel_off[s];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+    int i = idx % kb, j = idx / kb;
+    if (i >= j) Dg[i * LDS + j] = panel[(int64_t)(k0 + j) * nf + k0 + i];
+  }
+  __syncthreads();
+  const int nsub = (kb + SB - 1) / SB;
+  for (int sbk = 0; sbk < nsub; ++sbk) {
+    const int b0 = sbk * SB, b1 = min(b0 + SB, kb);
+    if (warp == 0) {
+      for (int j = b0; j < b1; ++j) {
+        if (lane == 0) {
+          const cplx d = Dg[j * LDS + j];
+          const bool bad = !(isfinite(d.x) && isfinite(d.y)) || (d.x == 0.0 && d.y == 0.0);
+          if (bad) atomicCAS(err, 0, 1 + s);
+          dv[j] = d;
+          di[j] = cinv(d);
+        }
+        __syncwarp();
+        const cplx dij = di[j];
+        const int rem = b1 - j - 1;
+        for (int q = lane; q < rem * rem; q += 32) {
+          const int c = j + 1 + q / rem, i = j + 1 + q % rem;
+          if (i >= c) Dg[i * LDS + c] = cfms(Dg[i * LDS + j], cmul(Dg[c * LDS + j], dij), Dg[i * LDS + c]);
+        }
+        __syncwarp();
+        for (int i = j + 1 + lane; i < b1; i += 32) Dg[i * LDS + j] = cmul(Dg[i * LDS + j], dij);
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    // sub-panel TRSM: rows [b1, kb), columns [b0, b1)
+    for (int i = b1 + tid; i < kb; i += blockDim.x) {
+      cplx w[SB];
+#pragma unroll
+      for (int jj = 0; jj < SB; ++jj) {
+        if (b0 + jj < b1) {
+          cplx acc = Dg[i * LDS + b0 + jj];
+#pragma unroll
+          for (int tt = 0; tt < jj; ++tt) acc = cfms(w[tt], Dg[(b0 + jj) * LDS + b0 + tt], acc);
+          w[jj] = acc;
+        }
+      }
+#pragma unroll
+      for (int jj = 0; jj < SB; ++jj)
+        if (b0 + jj < b1) Dg[i * LDS + b0 + jj] = cmul(w[jj], di[b0 + jj]);
+    }
+    __syncthreads();
+    // trailing update of [b1, kb)^2 (lower) with the sub-block's columns
+    const int rem = kb - b1;
+    for (int q = tid; q < rem * rem; q += blockDim.x) {
+      const int c = b1 + q / rem, i = b1 + q % rem;
+      if (i >= c) {
+        cplx acc = Dg[i * LDS + c];
+        for (int t = b0; t < b1; ++t) acc = cfms(cmul(Dg[i * LDS + t], dv[t]), Dg[c * LDS + t], acc);
+        Dg[i * LDS + c] = acc;
+      }
+    }
+    __syncthreads();
+  }
+  // X = L^{-1}: diagonal 16x16 blocks (one warp each, one column per lane)
+  if (warp < nsub) {
+    const int b0 = warp * SB, b1 = min(b0 + SB, kb);
+    const int j = b0 + lane;
+    if (j < b1) {
+      for (int i = j + 1; i < b1; ++i) {
+        cplx acc = Dg[i * LDS + j];
+        for (int t = j + 1; t < i; ++t) acc = cfma(Dg[i * LDS + t], Xs[t * LDS + j], acc);
+        Xs[i * LDS + j] = cmk(-acc.x, -acc.y);
+      }
+    }
+  }
+  __syncthreads();
+  for (int bi = 1; bi < nsub; ++bi) {
+    const int i0 = bi * SB, i1 = min(i0 + SB, kb), ni = i1 - i0;
+    for (int q = tid; q < ni * i0; q += blockDim.x) {
+      const int i = i0 + q % ni, j = q / ni;
+      cplx acc = Dg[i * LDS + j];
+      for (int t = j + 1; t < i0; ++t) acc = cfma(Dg[i * LDS + t], Xs[t * LDS + j], acc);
+      Ts[i * LDS + j] = acc;
+    }
+    __syncthreads();
+    for (int q = tid; q < ni * i0; q += blockDim.x) {
+      const int i = i0 + q % ni, j = q / ni;
+      cplx acc = Ts[i * LDS + j];
+      for (int t = i0; t < i; ++t) acc = cfma(Xs[i * LDS + t], Ts[t * LDS + j], acc);
+      Xs[i * LDS + j] = cmk(-acc.x, -acc.y);
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
+    int i = idx % kb, j = idx / kb;
+    panel[(int64_t)(k0 + j) * nf + k0 + i] = i >= j ? Dg[i * LDS + j] : Xs[j * LDS + i];
+  }
+}
+
+void launch_diag2(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
+                  const PoleBatch& pb, int* err) {
+  if (ntasks <= 0) return;
+  size_t smem = (3 * PB * LDS + 2 * PB) * sizeof(cplx);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_diag2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid(ntasks, pb.count);
+  k_diag2<<<grid, 256, smem, st>>>(tasks, F, pb, err);
+}
+
 // K4a': panel TRSM  L_r = F_r L_kk^{-T} D^{-1}  for one 64-row tile per CTA
 // (rows below the diagonal block), reading the factored diagonal block.
 __global__ void __launch_bounds__(256) k_trsm(const PanelTask* __restrict__ tasks, FrontsDev F,

@@ -21,6 +21,7 @@ struct SolveBatchDev {
   cplx* uvec[32];
   int* flags[32];
   int* done[32];      // fused sweeps: per-front completion counters (monotonic)
+  int epoch[32];      // per-slot solve count: flags hold it, counters reach epoch*need
 };
 
 // Cross-front dependencies of the fused (single-launch) sweeps.
@@ -47,7 +48,7 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 template <int NR>
 __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks, int nslots,
                                              FrontsDev F, SolveBatchDev sb, int* ticket,
-                                             int epoch, SweepDeps dep) {
+                                             int /*unused*/, SweepDeps dep) {
   __shared__ int s_t;
   extern __shared__ cplx dsm[];
   cplx(*v)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm);
@@ -57,6 +58,7 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
   __syncthreads();
   const int t = s_t;
   const int slot = t % nslots;
+  const int epoch = sb.epoch[slot];
   const SolveTask tk = tasks[t / nslots];
   const int s = tk.s, blk = tk.blk;
   const int p = F.npiv[s], nf = F.nf[s], first = F.first[s];
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
     const int need = dep.need_u[s];
     if (need > 0) {
       if (tid == 0)
-        while (ld_acquire(sb.done[slot] + s) < epoch * need) __nanosleep(64);
+        spin_wait_geq(sb.done[slot] + s, epoch * need);
       __syncthreads();
     }
   }
@@ -102,14 +104,14 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
   if (!pivot && jmax > 0) {
     // border rows need every pivot block: one wait (block npb-1 implies all)
     if (lane == 0)
-      while (ld_acquire(flags + jmax - 1) < epoch) __nanosleep(32);
+      spin_wait_geq(flags + jmax - 1, epoch);
     __syncwarp();
   }
   constexpr int YPL = (8 * NR + 31) / 32;   // y values per lane per block
   for (int j = 0; j < jmax; ++j) {
     if (pivot) {
       if (lane == 0)
-        while (ld_acquire(flags + j) < epoch) __nanosleep(32);
+        spin_wait_geq(flags + j, epoch);
       __syncwarp();
     }
     const int c0 = j * PB, ncol = min(PB, p - c0);
@@ -212,7 +214,7 @@ __global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks
 template <int NR>
 __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks, int nslots,
                                              FrontsDev F, SolveBatchDev sb, int* ticket,
-                                             int epoch, SweepDeps dep) {
+                                             int /*unused*/, SweepDeps dep) {
   __shared__ int s_t;
   extern __shared__ cplx dsm[];
   cplx(*red)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm);
@@ -222,6 +224,7 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   __syncthreads();
   const int t = s_t;
   const int slot = t % nslots;
+  const int epoch = sb.epoch[slot];
   const SolveTask tk = tasks[t / nslots];
   const int s = tk.s, cb = tk.blk;
   const int p = F.npiv[s], nf = F.nf[s], first = F.first[s];
@@ -245,7 +248,7 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
     const int par = dep.parent[s];
     const int need = (F.npiv[par] + PB - 1) / PB;
     if (tid == 0)
-      while (ld_acquire(sb.done[slot] + par) < epoch * need) __nanosleep(64);
+      spin_wait_geq(sb.done[slot] + par, epoch * need);
     __syncthreads();
   }
 
@@ -270,7 +273,7 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   // launch): per-warp wait, L2 reads
   for (int rb = npb - 1; rb > cb; --rb) {
     if (lane == 0)
-      while (ld_acquire(flags + rb) < epoch) __nanosleep(32);
+      spin_wait_geq(flags + rb, epoch);
     __syncwarp();
     const int q0 = rb * PB, q1 = min(q0 + PB, p);
 #pragma unroll 2
@@ -393,6 +396,7 @@ void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* 
     sb.uvec[i] = b.uvec[i];
     sb.flags[i] = forward ? b.flags_f[i] : b.flags_b[i];
     sb.done[i] = forward ? b.done_f[i] : b.done_b[i];
+    sb.epoch[i] = b.epoch[i];
   }
   SweepDeps dep{parent, need_u, fused ? 1 : 0};
   switch (nr) {

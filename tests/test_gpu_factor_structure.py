@@ -79,6 +79,10 @@ def test_fused_sweep_equals_level_sweeps(gpu, monkeypatch):
         monkeypatch.setenv("RBA_SWEEP", mode)
         cache = rb.ShiftedFactorCache()
         d = rb.forward_response(prob, model, approx, cache).data
+        # single-pole solves advance one slot's sweep counters only; later
+        # all-pole sweeps must not wait on the others (per-slot epochs)
+        for _ in range(2):
+            cache.solve(0, prob.f.astype(complex))
         opr = rb.JacobianOperator(prob, model, approx, cache)
         v = np.random.default_rng(1).standard_normal(opr.shape[1])
         w = np.random.default_rng(2).standard_normal(opr.shape[0])
@@ -86,3 +90,22 @@ def test_fused_sweep_equals_level_sweeps(gpu, monkeypatch):
         cache.engine.close()
     for a, b in zip(*outs):
         np.testing.assert_array_equal(a, b)
+
+
+def test_blocked_diag_matches_unblocked(gpu, monkeypatch):
+    prob, _ = rb.build_config("C1", n=10)
+    approx = rb.config_approximant("C1")
+    model = prob.true_model()
+    outs = []
+    for mode in ("v1", "v2"):
+        monkeypatch.setenv("RBA_DIAG", mode)
+        cache = rb.ShiftedFactorCache()
+        rb.factorize_all_poles(prob, model, approx, cache)
+        eng = cache.engine
+        S = mf.analyze(prob.K, prob.dof_coords, 64)
+        tot = int(S["panel_off"][-1])
+        buf = np.empty(tot, dtype=np.complex128)
+        _lib.check(eng.lib.rba_get_factor(eng.ctx, 1, ptr(buf.view(np.float64)), tot))
+        outs.append(buf)
+        eng.close()
+    assert rel(outs[1], outs[0]) <= 1e-10
