@@ -46,7 +46,7 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 // L2 load per lane (they were produced by other CTAs) and broadcasts them with
 // shuffles.  16 L loads per lane are in flight per block.
 template <int NR>
-__global__ void __launch_bounds__(256) k_fwd(const SolveTask* __restrict__ tasks, int nslots,
+__global__ void __launch_bounds__(256, 2) k_fwd(const SolveTask* __restrict__ tasks, int nslots,
                                              FrontsDev F, SolveBatchDev sb, int* ticket,
                                              int /*unused*/, SweepDeps dep) {
   __shared__ int s_t;
