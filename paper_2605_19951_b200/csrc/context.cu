@@ -84,7 +84,7 @@ struct rba_ctx {
   int64_t n_fwd_tasks = 0, n_bwd_tasks = 0;
   int32_t *parent_d = nullptr, *need_u_d = nullptr;
   int epoch_limit = 1 << 20;  // flags/counters are monotonic in the epoch; reset before overflow
-  bool fused_sweep = true;    // RBA_SWEEP=levels: one launch per level instead
+  bool fused_sweep = false;   // RBA_SWEEP=fused: one launch per sweep (cross-front counters)
   bool diag_v1 = false;       // RBA_DIAG=v1: unblocked diagonal-block kernel
   int* tickets = nullptr;
   int64_t nblocks = 0;
@@ -697,7 +697,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     if (std::string(e) == "v1" || c->gemm_dfma) c->gemm_v = 1;
     if (std::string(e) == "v2") c->gemm_v = 2;
   }
-  if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) != "levels";
+  if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) == "fused";
   if (const char* e = getenv("RBA_DIAG")) c->diag_v1 = std::string(e) == "v1";
   int rc;
   if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||

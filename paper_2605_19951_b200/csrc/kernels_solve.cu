@@ -198,7 +198,7 @@ __global__ void __launch_bounds__(256, 2) k_fwd(const SolveTask* __restrict__ ta
       cplx* u = sb.uvec[slot] + (F.uvec_off[s] + (r0 - p) + tid) * NR;
 #pragma unroll
       for (int r = 0; r < NR; ++r) u[r] = v[tid][r];
-      __threadfence();
+      if (dep.fused) __threadfence();
     }
     if (dep.fused) {
       __syncthreads();
