@@ -79,7 +79,9 @@ struct rba_ctx {
   int2* ea_tasks = nullptr;
   rba::PanelTask* pt_tasks = nullptr;
   rba::GemmTask* gm_tasks = nullptr;
-  std::vector<std::pair<int64_t, int>> fwd_lv, bwd_lv;
+  std::vector<std::pair<int64_t, int>> fwd_lv, bwd_lv, fwdb_lv, bwdb_lv, small_lv;
+  rba::SolveTask *fwdb_tasks = nullptr, *bwdb_tasks = nullptr;
+  int32_t* small_fronts = nullptr;
   rba::SolveTask *fwd_tasks = nullptr, *bwd_tasks = nullptr, *bwd_all = nullptr;
   int64_t n_fwd_tasks = 0, n_bwd_tasks = 0;
   int32_t *parent_d = nullptr, *need_u_d = nullptr;
@@ -331,9 +333,13 @@ int build_plans(rba_ctx* c) {
   if ((rc = upload(c, c->allocs, &c->gm_tasks, gm.data(), gm.size()))) return rc;
 
   // solve plans
-  std::vector<rba::SolveTask> ft, bt;
+  std::vector<rba::SolveTask> ft, bt, ftb, btb;
+  std::vector<int32_t> smallf;
   c->fwd_lv.assign(S.nlevels, {0, 0});
   c->bwd_lv.assign(S.nlevels, {0, 0});
+  c->fwdb_lv.assign(S.nlevels, {0, 0});
+  c->bwdb_lv.assign(S.nlevels, {0, 0});
+  c->small_lv.assign(S.nlevels, {0, 0});
   std::vector<int64_t> blk_off(S.nfront + 1, 0);
   for (int s = 0; s < S.nfront; ++s) blk_off[s + 1] = blk_off[s] + (S.npiv[s] + rba::PB - 1) / rba::PB;
   c->nblocks = blk_off[S.nfront];
@@ -355,6 +361,24 @@ int build_plans(rba_ctx* c) {
         if (b < npb + nbb) ft.push_back({s, b});
       }
     c->fwd_lv[L] = {off, (int)(ft.size() - off)};
+    // split for the per-level path: single-pivot-block fronts go to the
+    // warp-per-front kernels, the rest keep the block-task kernels
+    {
+      int64_t so = smallf.size();
+      for (int q = q0; q < q1; ++q)
+        if (S.npiv[S.level_fronts[q]] <= rba::PB) smallf.push_back(S.level_fronts[q]);
+      c->small_lv[L] = {so, (int)(smallf.size() - so)};
+      int64_t bo = ftb.size();
+      for (int b = 0; b < bmax; ++b)
+        for (int q = q0; q < q1; ++q) {
+          int s = S.level_fronts[q];
+          if (S.npiv[s] <= rba::PB) continue;
+          int npb = (S.npiv[s] + rba::PB - 1) / rba::PB;
+          int nbb = (S.nf[s] - S.npiv[s] + rba::PB - 1) / rba::PB;
+          if (b < npb + nbb) ftb.push_back({s, b});
+        }
+      c->fwdb_lv[L] = {bo, (int)(ftb.size() - bo)};
+    }
     off = bt.size();
     int pmax = 0;
     for (int q = q0; q < q1; ++q) pmax = std::max(pmax, (S.npiv[S.level_fronts[q]] + rba::PB - 1) / rba::PB);
@@ -365,9 +389,23 @@ int build_plans(rba_ctx* c) {
         if (key < npb) bt.push_back({s, npb - 1 - key});
       }
     c->bwd_lv[L] = {off, (int)(bt.size() - off)};
+    {
+      int64_t bo = btb.size();
+      for (int key = 0; key < pmax; ++key)
+        for (int q = q0; q < q1; ++q) {
+          int s = S.level_fronts[q];
+          if (S.npiv[s] <= rba::PB) continue;
+          int npb = (S.npiv[s] + rba::PB - 1) / rba::PB;
+          if (key < npb) btb.push_back({s, npb - 1 - key});
+        }
+      c->bwdb_lv[L] = {bo, (int)(btb.size() - bo)};
+    }
   }
   if ((rc = upload(c, c->allocs, &c->fwd_tasks, ft.data(), ft.size()))) return rc;
   if ((rc = upload(c, c->allocs, &c->bwd_tasks, bt.data(), bt.size()))) return rc;
+  if ((rc = upload(c, c->allocs, &c->fwdb_tasks, ftb.data(), ftb.size()))) return rc;
+  if ((rc = upload(c, c->allocs, &c->bwdb_tasks, btb.data(), btb.size()))) return rc;
+  if ((rc = upload(c, c->allocs, &c->small_fronts, smallf.data(), smallf.size()))) return rc;
   {
     // fused backward: levels top-down in one task list
     std::vector<rba::SolveTask> ba;
@@ -558,19 +596,35 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR) {
     CKL();
   } else {
     for (int L = 0; L < S.nlevels; ++L) {
-      Timed tm(c, KC_FWD);
-      rba::launch_solve_level(c->st, true, NR, c->fwd_tasks + c->fwd_lv[L].first,
-                              c->fwd_lv[L].second, ns, c->F, b, c->tickets + L, c->epoch,
-                              c->parent_d, c->need_u_d, false);
-      CKL();
+      if (c->small_lv[L].second > 0) {
+        Timed tm(c, KC_FWD);
+        rba::launch_solve_small(c->st, true, NR, c->small_fronts + c->small_lv[L].first,
+                                c->small_lv[L].second, ns, c->F, b);
+        CKL();
+      }
+      if (c->fwdb_lv[L].second > 0) {
+        Timed tm(c, KC_FWD);
+        rba::launch_solve_level(c->st, true, NR, c->fwdb_tasks + c->fwdb_lv[L].first,
+                                c->fwdb_lv[L].second, ns, c->F, b, c->tickets + L, c->epoch,
+                                c->parent_d, c->need_u_d, false);
+        CKL();
+      }
     }
     if (c->timing) cudaEventRecord(c->ev[1], c->st);
     for (int L = S.nlevels - 1; L >= 0; --L) {
-      Timed tm(c, KC_BWD);
-      rba::launch_solve_level(c->st, false, NR, c->bwd_tasks + c->bwd_lv[L].first,
-                              c->bwd_lv[L].second, ns, c->F, b, c->tickets + S.nlevels + L,
-                              c->epoch, c->parent_d, c->need_u_d, false);
-      CKL();
+      if (c->bwdb_lv[L].second > 0) {
+        Timed tm(c, KC_BWD);
+        rba::launch_solve_level(c->st, false, NR, c->bwdb_tasks + c->bwdb_lv[L].first,
+                                c->bwdb_lv[L].second, ns, c->F, b, c->tickets + S.nlevels + L,
+                                c->epoch, c->parent_d, c->need_u_d, false);
+        CKL();
+      }
+      if (c->small_lv[L].second > 0) {
+        Timed tm(c, KC_BWD);
+        rba::launch_solve_small(c->st, false, NR, c->small_fronts + c->small_lv[L].first,
+                                c->small_lv[L].second, ns, c->F, b);
+        CKL();
+      }
     }
   }
   if (c->timing) {

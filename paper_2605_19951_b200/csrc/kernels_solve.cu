@@ -359,6 +359,213 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   }
 }
 
+// ---------------------------------------------------------------------------
+// Small fronts (one pivot block, npiv <= 64): one WARP per (front, pole) does
+// the whole front -- no tickets, flags or block barriers.  The bottom levels
+// of the tree (C4: levels 0-4, ~20k fronts per pole) are all of this kind.
+// ---------------------------------------------------------------------------
+template <int NR>
+__global__ void __launch_bounds__(256) k_fwd_small(const int32_t* __restrict__ fronts, int nfr,
+                                                   int nslots, FrontsDev F, SolveBatchDev sb) {
+  extern __shared__ cplx dsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int item = blockIdx.x * 8 + warp;
+  if (item >= nfr * nslots) return;
+  const int slot = item % nslots;
+  const int s = fronts[item / nslots];
+  cplx(*vy)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + warp * PB * NR);   // [PB][NR]
+  const int p = F.npiv[s], nf = F.nf[s], first = F.first[s];
+  const cplx* panel = sb.factor[slot] + F.panel_off[s];
+  cplx* x = sb.x[slot];
+  const cplx* uvec = sb.uvec[slot];
+  const int64_t ro = F.rows_off[s];
+  // pivot rows: v = b + child contributions
+  for (int c = lane; c < p; c += 32) {
+    cplx val[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) val[r] = x[(int64_t)(first + c) * NR + r];
+    for (int64_t q = F.ucon_ptr[ro + c]; q < F.ucon_ptr[ro + c + 1]; ++q) {
+      const int64_t u = F.ucon_idx[q];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) val[r] = cadd(val[r], uvec[u * NR + r]);
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) vy[c][r] = val[r];
+  }
+  __syncwarp();
+  // y = X v  (X = L_bb^{-1}; X[c][t] sits at (row t, col c))
+  cplx yv[2][NR];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+#pragma unroll
+    for (int r = 0; r < NR; ++r) yv[h][r] = cmk(0.0, 0.0);
+    if (c < p) {
+      const cplx* xc = panel + (int64_t)c * nf;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) yv[h][r] = vy[c][r];
+      for (int t = 0; t < c; ++t) {
+        const cplx w = __ldg(xc + t);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) yv[h][r] = cfma(w, vy[t][r], yv[h][r]);
+      }
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+    if (c < p) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        vy[c][r] = yv[h][r];
+        x[(int64_t)(first + c) * NR + r] = yv[h][r];
+      }
+    }
+  }
+  __syncwarp();
+  // border rows: u = contributions - L21 y
+  cplx* uout = sb.uvec[slot] + F.uvec_off[s] * NR;
+  for (int rho = p + lane; rho < nf; rho += 32) {
+    cplx acc[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[r] = cmk(0.0, 0.0);
+    for (int64_t q = F.ucon_ptr[ro + rho]; q < F.ucon_ptr[ro + rho + 1]; ++q) {
+      const int64_t u = F.ucon_idx[q];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) acc[r] = cadd(acc[r], uvec[u * NR + r]);
+    }
+    const cplx* lrow = panel + rho;
+#pragma unroll 4
+    for (int c = 0; c < p; ++c) {
+      const cplx l = __ldg(lrow + (int64_t)c * nf);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) acc[r] = cfms(l, vy[c][r], acc[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) uout[(int64_t)(rho - p) * NR + r] = acc[r];
+  }
+}
+
+template <int NR>
+__global__ void __launch_bounds__(256) k_bwd_small(const int32_t* __restrict__ fronts, int nfr,
+                                                   int nslots, FrontsDev F, SolveBatchDev sb) {
+  extern __shared__ cplx dsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int item = blockIdx.x * 8 + warp;
+  if (item >= nfr * nslots) return;
+  const int slot = item % nslots;
+  const int s = fronts[item / nslots];
+  cplx(*xs)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + warp * 2 * 32 * NR);   // [32][NR] chunk
+  cplx(*ts)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + warp * 2 * 32 * NR + 32 * NR);
+  const int p = F.npiv[s], nf = F.nf[s], first = F.first[s];
+  const cplx* panel = sb.factor[slot] + F.panel_off[s];
+  cplx* x = sb.x[slot];
+  const int* rows = F.rows + F.rows_off[s];
+  cplx acc[2][NR];
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[h][r] = cmk(0.0, 0.0);
+  // border rows in chunks of 32: gather x (ancestors, final) then stream L columns
+  for (int q0 = p; q0 < nf; q0 += 32) {
+    const int n = min(32, nf - q0);
+    if (lane < n) {
+      const int g = __ldg(rows + q0 + lane);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) xs[lane][r] = __ldg(x + (int64_t)g * NR + r);
+    }
+    __syncwarp();
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (c < p) {
+        const cplx* lc = panel + (int64_t)c * nf + q0;
+        for (int i = 0; i < n; ++i) {
+          const cplx l = __ldg(lc + i);
+#pragma unroll
+          for (int r = 0; r < NR; ++r) acc[h][r] = cfma(l, xs[i][r], acc[h][r]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+  // t = y / d - acc, then x = X^T t  (X[i][c] at (row c, col i), i > c)
+  cplx(*tv)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + 16 * 32 * NR + warp * PB * NR);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+    if (c < p) {
+      const cplx d = panel[(int64_t)c * nf + c];
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        tv[c][r] = csub(cdiv(x[(int64_t)(first + c) * NR + r], d), acc[h][r]);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+    if (c < p) {
+      cplx xv[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) xv[r] = tv[c][r];
+      for (int i = c + 1; i < p; ++i) {
+        const cplx w = __ldg(panel + (int64_t)i * nf + c);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) xv[r] = cfma(w, tv[i][r], xv[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < NR; ++r) x[(int64_t)(first + c) * NR + r] = xv[r];
+    }
+  }
+  (void)ts;
+}
+
+template <int NR>
+static void small_nr(cudaStream_t st, bool forward, const int32_t* fronts, int nfr, int nslots,
+                     const FrontsDev& F, const SolveBatchDev& sb) {
+  const int items = nfr * nslots;
+  const int grid = (items + 7) / 8;
+  if (forward) {
+    const size_t smem = 8 * PB * NR * sizeof(cplx);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_fwd_small<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k_fwd_small<NR><<<grid, 256, smem, st>>>(fronts, nfr, nslots, F, sb);
+  } else {
+    const size_t smem = (16 * 32 * NR + 8 * PB * NR) * sizeof(cplx);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_bwd_small<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k_bwd_small<NR><<<grid, 256, smem, st>>>(fronts, nfr, nslots, F, sb);
+  }
+}
+
+void launch_solve_small(cudaStream_t st, bool forward, int nr, const int32_t* fronts, int nfr,
+                        int nslots, const FrontsDev& F, const SolveBatch& b) {
+  if (nfr <= 0) return;
+  SolveBatchDev sb;
+  for (int i = 0; i < nslots; ++i) {
+    sb.factor[i] = b.factor[i];
+    sb.x[i] = b.x[i];
+    sb.uvec[i] = b.uvec[i];
+    sb.flags[i] = nullptr;
+    sb.done[i] = nullptr;
+    sb.epoch[i] = 0;
+  }
+  switch (nr) {
+    case 1: small_nr<1>(st, forward, fronts, nfr, nslots, F, sb); break;
+    case 2: small_nr<2>(st, forward, fronts, nfr, nslots, F, sb); break;
+    case 4: small_nr<4>(st, forward, fronts, nfr, nslots, F, sb); break;
+    default: small_nr<8>(st, forward, fronts, nfr, nslots, F, sb); break;
+  }
+}
+
 template <int NR>
 static void fwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
                    const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch,
