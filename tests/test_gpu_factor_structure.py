@@ -69,8 +69,9 @@ def test_dmma_gemm_matches_dfma_reference(gpu, monkeypatch):
 
 
 def test_fused_sweep_equals_level_sweeps(gpu, monkeypatch):
-    """The single-launch solve sweeps (cross-front counters) give bitwise the
-    same solutions as one launch per level (same arithmetic order)."""
+    """The single-launch solve sweeps (cross-front counters, block tasks for
+    every front) agree with the per-level path (warp-per-front kernels for
+    single-block fronts) to rounding; each path is bitwise repeatable."""
     prob, _ = rb.build_config("C3", n=8)
     approx = rb.config_approximant("C3")
     model = prob.true_model()
@@ -89,7 +90,7 @@ def test_fused_sweep_equals_level_sweeps(gpu, monkeypatch):
         outs.append((d, opr.jvp(v), opr.vjp(w)))
         cache.engine.close()
     for a, b in zip(*outs):
-        np.testing.assert_array_equal(a, b)
+        assert rel(a, b) <= 1e-10
 
 
 def test_blocked_diag_matches_unblocked(gpu, monkeypatch):
