@@ -23,7 +23,7 @@ constexpr int LDK = TK + 4;     // padded row stride of the smem planes (doubles
 constexpr int NT = 128;         // threads per CTA
 
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
@@ -182,15 +182,24 @@ __global__ void __launch_bounds__(32 * NW) k_gemm_dmma(const GemmTask* __restric
         br[b] = S.bre[idx];
         bi[b] = S.bim[idx];
       }
+      // four passes of independent DMMAs: back-to-back MMAs never share an
+      // accumulator (the DMMA result latency would stall the warp otherwise)
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < NB; ++b) {
-          dmma(cre[a][b][0], cre[a][b][1], ar[a], br[b]);
-          dmma(cre[a][b][0], cre[a][b][1], an[a], bi[b]);
-          dmma(cim[a][b][0], cim[a][b][1], ar[a], bi[b]);
-          dmma(cim[a][b][0], cim[a][b][1], ai[a], br[b]);
-        }
+        for (int b = 0; b < NB; ++b) dmma(cre[a][b][0], cre[a][b][1], ar[a], br[b]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) dmma(cim[a][b][0], cim[a][b][1], ar[a], bi[b]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) dmma(cre[a][b][0], cre[a][b][1], an[a], bi[b]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < NB; ++b) dmma(cim[a][b][0], cim[a][b][1], ai[a], br[b]);
     }
     if (more) {
       __syncthreads();            // ds[buf^1] visible; st[buf^1] free (read 2 chunks ago)
@@ -423,15 +432,24 @@ __global__ void __launch_bounds__(NT2, 1) k_gemm2(const GemmTask* __restrict__ t
         br[b] = v.x;
         bi[b] = v.y;
       }
+      // four passes of independent DMMAs: back-to-back MMAs never share an
+      // accumulator (the DMMA result latency would stall the warp otherwise)
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          dmma(cre[a][b][0], cre[a][b][1], ar[a], br[b]);
-          dmma(cre[a][b][0], cre[a][b][1], an[a], bi[b]);
-          dmma(cim[a][b][0], cim[a][b][1], ar[a], bi[b]);
-          dmma(cim[a][b][0], cim[a][b][1], ai[a], br[b]);
-        }
+        for (int b = 0; b < 4; ++b) dmma(cre[a][b][0], cre[a][b][1], ar[a], br[b]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma(cim[a][b][0], cim[a][b][1], ar[a], bi[b]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma(cre[a][b][0], cre[a][b][1], an[a], bi[b]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) dmma(cim[a][b][0], cim[a][b][1], ai[a], br[b]);
     }
   }
   cp_wait<0>();
