@@ -472,6 +472,8 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
           rba::launch_trsm(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
         else if (c->gemm_v == 1)
           rba::launch_trsm_dmma(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
+        else if (c->gemm_v == 3)
+          rba::launch_trsm3(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
         else
           rba::launch_trsm2(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
         break;
@@ -482,6 +484,8 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
           rba::launch_gemm_update(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
         else if (c->gemm_v == 1)
           rba::launch_gemm_dmma(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
+        else if (c->gemm_v == 3)
+          rba::launch_gemm3(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
         else
           rba::launch_gemm2(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
         break;
@@ -750,6 +754,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     c->gemm_dfma = std::string(e) == "dfma";
     if (std::string(e) == "v1" || c->gemm_dfma) c->gemm_v = 1;
     if (std::string(e) == "v2") c->gemm_v = 2;
+    if (std::string(e) == "v3") c->gemm_v = 3;
   }
   if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) == "fused";
   if (const char* e = getenv("RBA_DIAG")) c->diag_v1 = std::string(e) == "v1";

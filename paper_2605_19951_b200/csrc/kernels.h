@@ -49,6 +49,10 @@ void launch_gemm2(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
                   const FrontsDev& F, const PoleBatch& pb);
 void launch_trsm2(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
                   const PoleBatch& pb);
+void launch_gemm3(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
+                  const FrontsDev& F, const PoleBatch& pb);
+void launch_trsm3(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
+                  const PoleBatch& pb);
 
 // solves
 void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* tasks,

@@ -502,5 +502,225 @@ void launch_trsm2(cudaStream_t st, const PanelTask* tasks, int ntasks, const Fro
   dim3 grid(ntasks, pb.count);
   k_gemm2<1><<<grid, NT2, smem, st>>>(nullptr, 0, tasks, F, pb);
 }
+// ---------------------------------------------------------------------------
+// v3: 64x64 CTA tile, 8 warps of 32x16 (<=128 registers: 2 CTAs = 16 warps/SM), interleaved complex [row][k]
+// shared-memory tiles filled by cp.async (16 B, zero-fill out of range) in a
+// 3-stage pipeline with one barrier per stage; one LDS.128 yields both the re
+// and im DMMA fragments.  The d_t scaling (MODE 0) and the unit-triangular
+// mask of X (MODE 1) are applied to the B fragments in registers.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int T3K = 8;             // k per stage (complex)
+constexpr int L3K = T3K + 4;       // padded row stride (complex): 12 x 16 B -> conflict-free
+constexpr int NS3 = 3;             // pipeline stages
+constexpr int BM3 = 64, BN3 = 64;
+constexpr int NT3 = 256;
+
+__device__ __forceinline__ void cp_async16_3(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit3() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait3() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+struct Stage3 {
+  cplx a[BM3 * L3K];
+  cplx b[BN3 * L3K];
+  cplx d[T3K];
+};
+}  // namespace
+
+template <int MODE>
+__global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ tasks, int ntasks,
+                                                  const PanelTask* __restrict__ ptasks,
+                                                  FrontsDev F, PoleBatch pb) {
+  extern __shared__ __align__(16) unsigned char smraw3[];
+  Stage3* st = reinterpret_cast<Stage3*>(smraw3);
+  __shared__ cplx dinv[BN3];
+  const int slot = blockIdx.y;
+  int s, t0, t1, r0, cc0, cmax, kbase = 0;
+  if (MODE == 0) {
+    const int ti = find_task(tasks, ntasks, blockIdx.x);
+    const GemmTask tk = tasks[ti];
+    int local = blockIdx.x - tk.tile_start;
+    int j = 0;
+    while (local >= tk.ntr - j) { local -= tk.ntr - j; ++j; }
+    const int i = j + local;
+    s = tk.s; t0 = tk.t0; t1 = tk.t1;
+    r0 = tk.c_lo + i * GT;
+    cc0 = tk.c_lo + j * GT;
+    cmax = min(cc0 + GT, tk.c_hi);
+  } else {
+    const PanelTask pt = ptasks[blockIdx.x];
+    s = pt.s;
+    t0 = 0;
+    t1 = min(GT, F.npiv[s] - pt.k0);
+    kbase = pt.k0;
+    r0 = pt.r0;
+    cc0 = 0;
+    cmax = t1;
+  }
+  const int nf = F.nf[s], p = F.npiv[s];
+  const cplx* __restrict__ panel = pb.factor[slot] + F.panel_off[s];
+  cplx* pw = pb.factor[slot] + F.panel_off[s];
+  cplx* upd = pb.upd[slot] + (F.upd_off[s] >= 0 ? F.upd_off[s] : 0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  const int g = lane >> 2, t4 = lane & 3;
+
+  double cre[4][2][2], cim[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      cre[a][b][0] = cre[a][b][1] = 0.0;
+      cim[a][b][0] = cim[a][b][1] = 0.0;
+    }
+  if (MODE == 1 && tid < BN3)
+    dinv[tid] = tid < cmax ? cinv(__ldg(panel + (int64_t)(kbase + tid) * nf + kbase + tid))
+                           : cmk(0.0, 0.0);
+
+  const int nchunks = (t1 - t0 + T3K - 1) / T3K;
+  auto issue = [&](int ch) {
+    if (ch < nchunks) {
+      Stage3& S = st[ch % NS3];
+      const int kt = t0 + ch * T3K;
+#pragma unroll
+      for (int q = 0; q < (BM3 * T3K) / NT3; ++q) {
+        const int e = tid + q * NT3;
+        const int rr = e % BM3, kk = e / BM3;
+        const int t = kt + kk;
+        const int row = r0 + rr;
+        const bool ok = t < t1 && row < nf;
+        const int64_t col = MODE == 0 ? (int64_t)t : (int64_t)(kbase + t);
+        cp_async16_3(&S.a[rr * L3K + kk], panel + (ok ? col * nf + row : 0), ok);
+      }
+#pragma unroll
+      for (int q = 0; q < (BN3 * T3K) / NT3; ++q) {
+        const int e = tid + q * NT3;
+        const int rr = e % BN3, kk = e / BN3;
+        const int t = kt + kk;
+        bool ok;
+        const cplx* src;
+        if (MODE == 0) {
+          ok = t < t1 && cc0 + rr < cmax;
+          src = panel + (ok ? (int64_t)t * nf + cc0 + rr : 0);
+        } else {
+          // X[c][t] at (row kbase+t, col kbase+c); masked to t < c in registers
+          ok = t < t1 && rr < cmax;
+          src = panel + (ok ? (int64_t)(kbase + rr) * nf + kbase + t : 0);
+        }
+        cp_async16_3(&S.b[rr * L3K + kk], src, ok);
+      }
+      if (MODE == 0 && tid < T3K) {
+        const int t = kt + tid;
+        S.d[tid] = t < t1 ? __ldg(panel + (int64_t)t * nf + t) : cmk(0.0, 0.0);
+      }
+    }
+    cp_commit3();
+  };
+  for (int c = 0; c < NS3 - 1; ++c) issue(c);
+  for (int ch = 0; ch < nchunks; ++ch) {
+    cp_wait3<NS3 - 2>();
+    __syncthreads();
+    issue(ch + NS3 - 1);
+    const Stage3& S = st[ch % NS3];
+    const int kt = t0 + ch * T3K;
+#pragma unroll
+    for (int k4 = 0; k4 < T3K; k4 += 4) {
+      double ar[4], ai[4], an[4], br[2], bi[2];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const cplx v = S.a[(wm + a * 8 + g) * L3K + k4 + t4];
+        ar[a] = v.x;
+        ai[a] = v.y;
+        an[a] = -v.y;
+      }
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        cplx v = S.b[(wn + b * 8 + g) * L3K + k4 + t4];
+        if (MODE == 0) {
+          v = cmul(v, S.d[k4 + t4]);
+        } else {
+          const int c = wn + b * 8 + g, t = kt + k4 + t4;
+          v = t < c ? v : (t == c ? cmk(1.0, 0.0) : cmk(0.0, 0.0));
+        }
+        br[b] = v.x;
+        bi[b] = v.y;
+      }
+      // four passes of independent DMMAs: back-to-back MMAs never share an
+      // accumulator (the DMMA result latency would stall the warp otherwise)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma(cre[a][b][0], cre[a][b][1], ar[a], br[b]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma(cim[a][b][0], cim[a][b][1], ar[a], bi[b]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma(cre[a][b][0], cre[a][b][1], an[a], bi[b]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma(cim[a][b][0], cim[a][b][1], ai[a], br[b]);
+    }
+  }
+  cp_wait3<0>();
+  __syncthreads();
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = r0 + wm + a * 8 + g;
+        const int c = cc0 + wn + b * 8 + t4 * 2 + h;
+        if (MODE == 0) {
+          if (r < nf && c < cmax && r >= c) {
+            cplx* dst = faddr(pw, upd, p, nf, r, c);
+            cplx v = *dst;
+            v.x -= cre[a][b][h];
+            v.y -= cim[a][b][h];
+            *dst = v;
+          }
+        } else {
+          if (r < nf && c < cmax)
+            pw[(int64_t)(kbase + c) * nf + r] = cmul(cmk(cre[a][b][h], cim[a][b][h]), dinv[c]);
+        }
+      }
+}
+
+void launch_gemm3(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
+                  const FrontsDev& F, const PoleBatch& pb) {
+  if (ntasks <= 0 || nctas <= 0) return;
+  const size_t smem = NS3 * sizeof(Stage3);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm3<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid(nctas, pb.count);
+  k_gemm3<0><<<grid, NT3, smem, st>>>(tasks, ntasks, nullptr, F, pb);
+}
+
+void launch_trsm3(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
+                  const PoleBatch& pb) {
+  if (ntasks <= 0) return;
+  const size_t smem = NS3 * sizeof(Stage3);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid(ntasks, pb.count);
+  k_gemm3<1><<<grid, NT3, smem, st>>>(nullptr, 0, tasks, F, pb);
+}
+
 
 }  // namespace rba

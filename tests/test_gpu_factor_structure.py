@@ -51,7 +51,7 @@ def test_dmma_gemm_matches_dfma_reference(gpu, monkeypatch):
     approx = rb.config_approximant("C1")
     model = prob.true_model()
     out = []
-    for mode in ("dfma", "v1", "v2"):
+    for mode in ("dfma", "v1", "v2", "v3"):
         monkeypatch.setenv("RBA_GEMM", mode)
         cache = rb.ShiftedFactorCache()
         rb.factorize_all_poles(prob, model, approx, cache)
@@ -66,6 +66,7 @@ def test_dmma_gemm_matches_dfma_reference(gpu, monkeypatch):
     # uses the inverted diagonal block: rounding-level differences only
     assert rel(out[1], out[0]) <= 1e-10
     assert rel(out[2], out[0]) <= 1e-10
+    assert rel(out[3], out[0]) <= 1e-10
 
 
 def test_fused_sweep_equals_level_sweeps(gpu, monkeypatch):
