@@ -137,7 +137,7 @@ struct rba_ctx {
   // by rba_set_timing) and the launch count of this context's kernels
   double cls_ms[16] = {0};
   bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernels
-  int gemm_v = 1;             // RBA_GEMM=v2 selects the cp.async 128x64 kernel
+  int gemm_v = 3;             // RBA_GEMM=v1|v2 select the earlier DMMA kernels
   int64_t launches = 0;
   std::vector<cudaEvent_t> evpool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -539,8 +539,12 @@ int ensure_slots(rba_ctx* c) {
   {
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
+    // more poles per factor launch fill the GPU at the top of the tree;
+    // each needs its own update arena
     const size_t need = (size_t)S.upd_total * sizeof(cplx);
-    c->fbatch = (nl >= 2 && fr > 2 * need + ((size_t)4 << 30)) ? 2 : 1;
+    c->fbatch = 1;
+    for (int k = 2; k <= 3 && k <= nl; ++k)
+      if (fr > k * need + ((size_t)8 << 30)) c->fbatch = k;
   }
   if (const char* e = getenv("RBA_FACTOR_BATCH")) c->fbatch = std::max(1, std::min(atoi(e), nl));
   c->upd.assign(c->fbatch, nullptr);
