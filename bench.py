@@ -172,6 +172,7 @@ def run_ours(args, world, rank):
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     cls = eng.timings()
+    lev = eng.timings_detail()
     eng.set_timing(0)
     n_fact = cache.counters.factorizations - fac0
     n_solve = cache.counters.solves - sol0
@@ -256,6 +257,7 @@ def run_ours(args, world, rank):
         "gpu_launches": int(cls["launches"]),
         "components": comp,
         "kernel_ms": {k: round(v, 3) for k, v in cls.items() if k != "launches"},
+        "solve_ms_by_level": {k: [x for x in v if x > 0] for k, v in lev.items()},
         "counts": {"factorizations": n_fact, "solves": n_solve},
         "roofline": roof,
         "clocks": clk,
@@ -377,14 +379,28 @@ def cpu_baseline_sample(name):
                        f"on {min(cores, m)} cores; the config itself exceeds host RAM")}
 
 
+def workload_desc(name, n_override, lsqr_override):
+    """The `config` object shared by both arms (host-only)."""
+    import paper_2605_19951_b200 as rb
+    prob, meta, approx, lsqr_iters = build_workload(name, n_override, lsqr_override)
+    return {"workload": f"{name}: {meta['n']}^3-hex Kuhn-tet Nedelec box, "
+                        f"N={prob.dof_count} edge dofs, P={prob.grid.cell_count} cells, "
+                        f"{approx.pole_count} poles, {prob.source_count} sources x "
+                        f"{prob.receiver_count} receivers x {approx.channels.count} times, "
+                        f"{lsqr_iters} LSQR its, lambda={meta.get('lam', 1e-2)}",
+            "global_batch": approx.pole_count}
+
+
 def run_reference(args):
     """--impl reference: the reference's CPU path (oracle port) on the host."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return None
     t0 = time.perf_counter()
+    cfg = workload_desc(args.config, args.n, args.lsqr)
+    cfg["parallelism"] = "host cores (pole-parallel SuperLU, extrapolated; see cpu_baseline)"
     for _ in range(args.warmup):
-        pass
+        cpu_baseline_sample(args.config)
     vals = []
     for _ in range(max(1, args.steps)):
         cb = cpu_baseline_sample(args.config)
@@ -393,11 +409,106 @@ def run_reference(args):
     return {"impl": "reference", "metric": METRIC, "value": cb["value"],
             "unit": "s/GN-iteration", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
-            "dtype": "c128/f64", "data": "synthetic", "config": {"workload": args.config},
+            "dtype": "c128/f64", "data": "synthetic", "config": cfg,
             "cpu_baseline": cb,
             "e2e": {"value": cb["value"], "unit": "s/GN-iteration", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "wall_s": time.perf_counter() - t0}
+
+
+def run_c2(args, world, rank):
+    """BASELINE config 2: shifted-solve microbenchmark.  32^3-hex box, sigma
+    log-uniform in [1e-3, 1] (seed 1), 16 poles; per pole factorise once, then
+    solve 4 random complex RHS (unit-normal re/im).  Reports factor TFLOP/s and
+    solve GB/s (algorithmic bytes 2 nnz(L) 16 + 16 N + 4 N nrhs 16)."""
+    import torch
+    import paper_2605_19951_b200 as rb
+    from paper_2605_19951_b200.engine import Engine
+    prob, meta, approx, _ = build_workload("C2", args.n, None)
+    rng = np.random.default_rng(1)
+    F = rng.standard_normal((4, prob.dof_count)) + 1j * rng.standard_normal((4, prob.dof_count))
+    eng = Engine(prob, None)
+    eng.set_sources(F)
+    eng.set_poles(approx)
+    eng.set_model(prob.m_true)
+    flops, nnzL = symbolic_stats(eng)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(args.warmup):
+        eng.factor()
+        eng.forward()
+    tf, ts = [], []
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        e0.record(stream)
+        eng.factor()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        tf.append(e0.elapsed_time(e1))
+        e0.record(stream)
+        eng.forward()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    nl = len(eng.local)
+    bytes_one = 2 * nnzL * 16 + eng.N * 16 + 4 * eng.N * 4 * 16
+    fac_tf = flops * nl / (np.mean(tf) * 1e-3) / 1e12
+    sol_gbs = bytes_one * nl / (np.mean(ts) * 1e-3) / 1e9
+    peaks = measured_peaks()
+    return {"metric": METRIC, "value": fac_tf, "unit": "factor FP64 TFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128/f64",
+            "data": "synthetic (seed 1)",
+            "config": {"workload": f"C2: {meta['n']}^3 hexes, N={eng.N}, {eng.m} poles, "
+                                   f"4 random complex RHS"},
+            "solve_gbs": sol_gbs, "factor_ms_per_pole": float(np.mean(tf)) / nl,
+            "solve_ms_per_pole": float(np.mean(ts)) / nl,
+            "roofline": {"factor": {"achieved": fac_tf, "peak": peaks["fp64_tflops"],
+                                    "unit": "TFLOP/s", "frac": fac_tf / peaks["fp64_tflops"]},
+                         "solve": {"achieved": sol_gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                                   "frac": sol_gbs / peaks["hbm_gbs"]}},
+            "flops_per_pole": flops, "nnzL_per_pole": nnzL}
+
+
+def run_c3(args, world, rank):
+    """BASELINE config 3: Jacobian operator benchmark on the 32^3 box (two 6^3
+    blocks, 4 loop sources, 10x10 receivers, 31 times, 16 poles): 50 J v and
+    50 J^T w with the adjointness check <Jv, w> = <v, J^T w>."""
+    import torch
+    import paper_2605_19951_b200 as rb
+    prob, meta, approx, _ = build_workload("C3", args.n, None)
+    model = prob.true_model()
+    cache = rb.ShiftedFactorCache()
+    opr = rb.JacobianOperator(prob, model, approx, cache)
+    eng = opr.engine
+    rng = np.random.default_rng(3)
+    trials = 50 if args.steps >= 2 else 5
+    V = torch.as_tensor(rng.standard_normal((trials, opr.shape[1])), device="cuda")
+    Wt = torch.as_tensor(rng.standard_normal((trials, opr.shape[0])), device="cuda")
+    for _ in range(args.warmup):
+        opr.jvp_d(V[0])
+        opr.vjp_d(Wt[0])
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    jv = [opr.jvp_d(V[k]) for k in range(trials)]
+    jt = [opr.vjp_d(Wt[k]) for k in range(trials)]
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    worst = 0.0
+    for k in range(trials):
+        lhs = float(torch.dot(jv[k], Wt[k]))
+        rhs = float(torch.dot(V[k], jt[k]))
+        worst = max(worst, abs(lhs - rhs) / max(abs(lhs), abs(rhs)))
+    return {"metric": METRIC, "value": 2 * trials / (ms * 1e-3), "unit": "J·v or Jᵀ·w per s",
+            "n_gpus": world, "steps": trials, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128/f64",
+            "data": "synthetic (seed 3)",
+            "config": {"workload": f"C3: {meta['n']}^3 hexes, N={eng.N}, P={eng.P}, {eng.m} "
+                                   f"poles, {eng.S} sources x {eng.Mr} receivers x {eng.Kt} times"},
+            "adjoint_max_mismatch": worst, "ms_per_action": ms / (2 * trials)}
 
 
 def main():
@@ -408,6 +519,11 @@ def main():
             print(json.dumps(line))
         return
     world, rank = dist_setup(args)
+    if args.config.upper() in ("C2", "C3"):
+        line = (run_c2 if args.config.upper() == "C2" else run_c3)(args, world, rank)
+        if rank == 0:
+            print(json.dumps(line))
+        return
     line = run_ours(args, world, rank)
     if rank == 0 and world == 1 and not args.no_cpu:
         try:

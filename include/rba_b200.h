@@ -84,6 +84,8 @@ int rba_set_mesh(rba_ctx* ctx, int64_t N, int64_t P, int32_t k, const int32_t* c
 int rba_set_observation(rba_ctx* ctx, int64_t Mr, const int64_t* Q_indptr_h,
                         const int32_t* Q_indices_h, const double* Q_data_h);
 int rba_set_sources(rba_ctx* ctx, int32_t S, const double* F_h);
+/* Complex right-hand sides (S x N complex) -- e.g. the C2 random-RHS solves. */
+int rba_set_sources_complex(rba_ctx* ctx, int32_t S, const double* F_h);
 /* Poles xi_i (m complex) and residues alpha (m x K_t complex, row-major);
  * local_poles: the global pole indices this context factorises (sharding
  * i mod G, shifted.py:147-149). */
@@ -159,6 +161,9 @@ int rba_sync(rba_ctx* ctx);
  * rba_set_timing: 1 on, 0 off, 2 reset the accumulators. */
 int rba_timings(rba_ctx* ctx, double* out_h);
 int rba_set_timing(rba_ctx* ctx, int32_t enabled);
+/* out[128]: out[0..15] as rba_timings; out[16+L] forward-sweep ms of level L,
+ * out[48+L] backward-sweep ms of level L (L < 32). */
+int rba_timings_detail(rba_ctx* ctx, double* out_h);
 
 #ifdef __cplusplus
 }

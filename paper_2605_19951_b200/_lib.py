@@ -43,6 +43,7 @@ _SIGS = {
     "rba_set_mesh": (C.c_int, [vp, i64, i64, i32, vp, vp, vp, vp, vp, vp, i32]),
     "rba_set_observation": (C.c_int, [vp, i64, vp, vp, vp]),
     "rba_set_sources": (C.c_int, [vp, i32, vp]),
+    "rba_set_sources_complex": (C.c_int, [vp, i32, vp]),
     "rba_set_poles": (C.c_int, [vp, i32, vp, i32, vp, i32, vp]),
     "rba_set_model": (C.c_int, [vp, vp]),
     "rba_set_model_d": (C.c_int, [vp, vp]),
@@ -69,6 +70,7 @@ _SIGS = {
     "rba_sync": (C.c_int, [vp]),
     "rba_timings": (C.c_int, [vp, vp]),
     "rba_set_timing": (C.c_int, [vp, i32]),
+    "rba_timings_detail": (C.c_int, [vp, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

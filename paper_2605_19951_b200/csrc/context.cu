@@ -135,7 +135,7 @@ struct rba_ctx {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // per-kernel-class device time (CUDA events around every launch, enabled
   // by rba_set_timing) and the launch count of this context's kernels
-  double cls_ms[16] = {0};
+  double cls_ms[128] = {0};   // 0-15 kernel classes; 16+L fwd, 48+L bwd, 80+L gemm per level
   bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernels
   int gemm_v = 3;             // RBA_GEMM=v1|v2 select the earlier DMMA kernels
   int64_t launches = 0;
@@ -259,6 +259,10 @@ int build_plans(rba_ctx* c) {
       int s = S.level_fronts[q];
       bool kids = S.child_ptr[s + 1] > S.child_ptr[s];
       if (!kids && S.nf[s] == S.npiv[s]) continue;
+      if (S.nf[s] <= 384) {
+        ea.push_back(make_int2(s, -1));      // small front: one CTA does it all
+        continue;
+      }
       int c0 = kids ? 0 : S.npiv[s] / 32;
       for (int ct = c0; ct * 32 < S.nf[s]; ++ct) ea.push_back(make_int2(s, ct));
     }
@@ -604,6 +608,7 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR) {
     CKL();
   } else {
     for (int L = 0; L < S.nlevels; ++L) {
+      Timed tl(c, 16 + std::min(L, 31), 0);
       if (c->small_lv[L].second > 0) {
         Timed tm(c, KC_FWD);
         rba::launch_solve_small(c->st, true, NR, c->small_fronts + c->small_lv[L].first,
@@ -620,6 +625,7 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR) {
     }
     if (c->timing) cudaEventRecord(c->ev[1], c->st);
     for (int L = S.nlevels - 1; L >= 0; --L) {
+      Timed tl(c, 48 + std::min(L, 31), 0);
       if (c->bwdb_lv[L].second > 0) {
         Timed tm(c, KC_BWD);
         rba::launch_solve_level(c->st, false, NR, c->bwdb_tasks + c->bwdb_lv[L].first,
@@ -904,6 +910,23 @@ int rba_set_sources(rba_ctx* c, int32_t S_, const double* F) {
   for (int64_t kk = 0; kk < c->N; ++kk) {
     int32_t o = c->sym.perm[kk];
     for (int s = 0; s < S_; ++s) h[kk * c->NRs + s] = rba::cmk(F[(int64_t)s * c->N + o], 0.0);
+  }
+  return upload(c, c->obs_allocs, &c->Fsrc, h.data(), h.size());
+}
+
+int rba_set_sources_complex(rba_ctx* c, int32_t S_, const double* F) {
+  if (!c || !c->have_mesh) return fail(RBA_ERR_STATE, "set_mesh first");
+  if (S_ < 1 || S_ > 8 || !F) return fail(RBA_ERR_INVALID, "1 <= S <= 8 sources required");
+  if (!c->q_ptr) return fail(RBA_ERR_STATE, "set_observation first");
+  CK(cudaSetDevice(c->device));
+  free_slots(c);
+  c->S = S_;
+  c->NRs = nr_pad(S_);
+  const cplx* Fc = (const cplx*)F;
+  std::vector<cplx> h((size_t)c->N * c->NRs, rba::cmk(0.0, 0.0));
+  for (int64_t kk = 0; kk < c->N; ++kk) {
+    int32_t o = c->sym.perm[kk];
+    for (int s = 0; s < S_; ++s) h[kk * c->NRs + s] = Fc[(int64_t)s * c->N + o];
   }
   return upload(c, c->obs_allocs, &c->Fsrc, h.data(), h.size());
 }
@@ -1295,6 +1318,12 @@ int rba_timings(rba_ctx* c, double* out) {
   flush_timing(c);
   for (int i = 0; i < 16; ++i) out[i] = c->cls_ms[i];
   out[15] = (double)c->launches;
+  return RBA_OK;
+}
+
+int rba_timings_detail(rba_ctx* c, double* out) {
+  flush_timing(c);
+  for (int i = 0; i < 128; ++i) out[i] = c->cls_ms[i];
   return RBA_OK;
 }
 

@@ -84,9 +84,33 @@ __global__ void __launch_bounds__(256) k_extend_add(const int2* __restrict__ tas
   const int2 tk = tasks[blockIdx.x];
   const int s = tk.x;
   const int nf = F.nf[s], p = F.npiv[s];
-  const int c0 = tk.y * 32, c1 = min(c0 + 32, nf);
   cplx* panel = pb.factor[slot] + F.panel_off[s];
   cplx* upd = pb.upd[slot] + (F.upd_off[s] >= 0 ? F.upd_off[s] : 0);
+  if (tk.y < 0) {
+    // whole (small) front in one CTA: flattened loops over each block
+    const int r = nf - p;
+    for (int q = threadIdx.x; q < r * r; q += blockDim.x) {
+      const int c = q / r, i = q - c * r;
+      if (i >= c) upd[q] = cmk(0.0, 0.0);
+    }
+    __syncthreads();
+    for (int ci = F.child_ptr[s]; ci < F.child_ptr[s + 1]; ++ci) {
+      const int ch = F.child_list[ci];
+      const int rc = F.nf[ch] - F.npiv[ch];
+      const int32_t* rm = F.relmap + F.rel_off[ch];
+      const cplx* U = pb.upd[slot] + F.upd_off[ch];
+      for (int q = threadIdx.x; q < rc * rc; q += blockDim.x) {
+        const int j = q / rc, i = q - j * rc;
+        if (i >= j) {
+          cplx* dst = faddr(panel, upd, p, nf, rm[i], rm[j]);
+          *dst = cadd(*dst, U[q]);
+        }
+      }
+      __syncthreads();
+    }
+    return;
+  }
+  const int c0 = tk.y * 32, c1 = min(c0 + 32, nf);
   // zero update-block columns (rows >= column)
   for (int c = max(c0, p); c < c1; ++c)
     for (int r = c + threadIdx.x; r < nf; r += blockDim.x)

@@ -93,11 +93,16 @@ class Engine:
 
     # ------------------------------------------------------------------ setup
     def set_sources(self, F):
-        F = np.ascontiguousarray(np.atleast_2d(F), dtype=np.float64)
+        F = np.atleast_2d(F)
         if F.shape[1] != self.N:
             raise ValueError("source vectors must have length N")
         self.S = F.shape[0]
-        check(self.lib.rba_set_sources(self.ctx, self.S, ptr(F)))
+        if np.iscomplexobj(F):
+            Fc = np.ascontiguousarray(F, dtype=np.complex128)
+            check(self.lib.rba_set_sources_complex(self.ctx, self.S, ptr(Fc.view(np.float64))))
+        else:
+            Fr = np.ascontiguousarray(F, dtype=np.float64)
+            check(self.lib.rba_set_sources(self.ctx, self.S, ptr(Fr)))
         self.factored = False
 
     def set_poles(self, approx):
@@ -289,6 +294,12 @@ class Engine:
         d = {k: float(out[i]) for i, k in enumerate(self.KCLASSES)}
         d["launches"] = int(out[15])
         return d
+
+    def timings_detail(self) -> dict:
+        out = np.zeros(128)
+        check(self.lib.rba_timings_detail(self.ctx, ptr(out)))
+        return {"solve_fwd_by_level": out[16:48].round(3).tolist(),
+                "solve_bwd_by_level": out[48:80].round(3).tolist()}
 
     def sync(self):
         check(self.lib.rba_sync(self.ctx))
