@@ -22,5 +22,6 @@ from .inversion import (InversionConfig, InversionState, IterationRecord, LineSe
                         LsqrConfig, chi_squared, default_lambda0, gn_step, line_search,
                         run_inversion)
 from .synthetic import DataSet, NoiseSpec, load_dataset, make_dataset, save_dataset
+from .reporting import TimingModel, fit_timing_model, pole_solution_checksum, scaling_benchmark
 
 __version__ = "0.1.0"

@@ -547,7 +547,7 @@ int ensure_slots(rba_ctx* c) {
     // each needs its own update arena
     const size_t need = (size_t)S.upd_total * sizeof(cplx);
     c->fbatch = 1;
-    for (int k = 2; k <= 3 && k <= nl; ++k)
+    for (int k = 2; k <= 8 && k <= nl; ++k)
       if (fr > k * need + ((size_t)8 << 30)) c->fbatch = k;
   }
   if (const char* e = getenv("RBA_FACTOR_BATCH")) c->fbatch = std::max(1, std::min(atoi(e), nl));

@@ -34,10 +34,14 @@ struct PoleBatch {
 constexpr int PB = 64;   // pivot block (factorisation) and solve row block
 constexpr int GT = 64;   // GEMM tile (complex)
 
-// element address in front s: columns < p live in the factor panel (ld = nf),
-// columns >= p in the update block (ld = nf - p, row offset p).
+// Packed lower-triangular update block of order n: column j holds rows j..n-1.
+__host__ __device__ __forceinline__ int64_t ucol(int64_t j, int64_t n) {
+  return j * n - j * (j - 1) / 2;
+}
+// element address in front s (r >= c): columns < p live in the factor panel
+// (ld = nf), columns >= p in the packed lower-triangular update block.
 __device__ __forceinline__ cplx* faddr(cplx* panel, cplx* upd, int p, int nf, int r, int c) {
-  return c < p ? panel + (int64_t)c * nf + r : upd + (int64_t)(c - p) * (nf - p) + (r - p);
+  return c < p ? panel + (int64_t)c * nf + r : upd + ucol(c - p, nf - p) + (r - c);
 }
 
 struct PanelTask { int32_t s, k0, r0, pad; };

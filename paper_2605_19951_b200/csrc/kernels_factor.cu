@@ -87,23 +87,23 @@ __global__ void __launch_bounds__(256) k_extend_add(const int2* __restrict__ tas
   cplx* panel = pb.factor[slot] + F.panel_off[s];
   cplx* upd = pb.upd[slot] + (F.upd_off[s] >= 0 ? F.upd_off[s] : 0);
   if (tk.y < 0) {
-    // whole (small) front in one CTA: flattened loops over each block
+    // whole (small) front in one CTA: zero the packed update block, then
+    // add each child's packed block column by column
     const int r = nf - p;
-    for (int q = threadIdx.x; q < r * r; q += blockDim.x) {
-      const int c = q / r, i = q - c * r;
-      if (i >= c) upd[q] = cmk(0.0, 0.0);
-    }
+    for (int64_t q = threadIdx.x; q < (int64_t)r * (r + 1) / 2; q += blockDim.x)
+      upd[q] = cmk(0.0, 0.0);
     __syncthreads();
     for (int ci = F.child_ptr[s]; ci < F.child_ptr[s + 1]; ++ci) {
       const int ch = F.child_list[ci];
       const int rc = F.nf[ch] - F.npiv[ch];
       const int32_t* rm = F.relmap + F.rel_off[ch];
       const cplx* U = pb.upd[slot] + F.upd_off[ch];
-      for (int q = threadIdx.x; q < rc * rc; q += blockDim.x) {
-        const int j = q / rc, i = q - j * rc;
-        if (i >= j) {
-          cplx* dst = faddr(panel, upd, p, nf, rm[i], rm[j]);
-          *dst = cadd(*dst, U[q]);
+      for (int j = 0; j < rc; ++j) {
+        const cplx* Uc = U + ucol(j, rc);
+        const int tc = rm[j];
+        for (int i = j + threadIdx.x; i < rc; i += blockDim.x) {
+          cplx* dst = faddr(panel, upd, p, nf, rm[i], tc);
+          *dst = cadd(*dst, Uc[i - j]);
         }
       }
       __syncthreads();
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) k_extend_add(const int2* __restrict__ tas
   // zero update-block columns (rows >= column)
   for (int c = max(c0, p); c < c1; ++c)
     for (int r = c + threadIdx.x; r < nf; r += blockDim.x)
-      upd[(int64_t)(c - p) * (nf - p) + (r - p)] = cmk(0.0, 0.0);
+      upd[ucol(c - p, nf - p) + (r - c)] = cmk(0.0, 0.0);
   __syncthreads();
   for (int ci = F.child_ptr[s]; ci < F.child_ptr[s + 1]; ++ci) {
     const int ch = F.child_list[ci];
@@ -124,10 +124,10 @@ __global__ void __launch_bounds__(256) k_extend_add(const int2* __restrict__ tas
     const cplx* U = pb.upd[slot] + F.upd_off[ch];
     for (int j = j0; j < j1; ++j) {
       const int tc = rm[j];
-      const cplx* Uc = U + (int64_t)j * rc;
+      const cplx* Uc = U + ucol(j, rc);
       for (int i = j + threadIdx.x; i < rc; i += blockDim.x) {
         cplx* dst = faddr(panel, upd, p, nf, rm[i], tc);
-        *dst = cadd(*dst, Uc[i]);
+        *dst = cadd(*dst, Uc[i - j]);
       }
     }
     __syncthreads();

@@ -358,14 +358,14 @@ std::string analyze(int64_t n, const int64_t* indptr, const int32_t* indices,
       int32_t s = S.level_fronts[q];
       if (S.parent[s] < 0) continue;
       int64_t r = S.nf[s] - S.npiv[s];
-      S.upd_off[s] = fls.alloc(align16(std::max<int64_t>(r * r, 1)));
+      S.upd_off[s] = fls.alloc(align16(std::max<int64_t>(r * (r + 1) / 2, 1)));
     }
     for (int32_t q = S.level_ptr[l]; q < S.level_ptr[l + 1]; ++q) {
       int32_t s = S.level_fronts[q];
       for (int32_t ci = S.child_ptr[s]; ci < S.child_ptr[s + 1]; ++ci) {
         int32_t c = S.child_list[ci];
         int64_t r = S.nf[c] - S.npiv[c];
-        fls.release(S.upd_off[c], align16(std::max<int64_t>(r * r, 1)));
+        fls.release(S.upd_off[c], align16(std::max<int64_t>(r * (r + 1) / 2, 1)));
       }
     }
   }

@@ -29,7 +29,8 @@ struct Symbolic {
   std::vector<int64_t> rel_off;    // nfront + 1 ; (nf - npiv) entries per front
   std::vector<int32_t> relmap;     // local row in parent of rows[npiv + k]
   std::vector<int64_t> panel_off;  // nfront + 1 ; nf*npiv complex entries per front
-  std::vector<int64_t> upd_off;    // per front offset into the update arena (-1: root)
+  std::vector<int64_t> upd_off;    // per front offset into the update arena (-1: root);
+                                   // packed lower-triangular blocks of order nf - npiv
   int64_t upd_total = 0;           // complex entries
   std::vector<int64_t> uvec_off;   // nfront + 1 ; (nf - npiv) per front (solve arena)
   int32_t nlevels = 0;

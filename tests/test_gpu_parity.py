@@ -187,3 +187,14 @@ def test_singular_shift_raises(gpu):
     cache.activate("t")
     with pytest.raises(rb.SolveError):
         cache.factorize(0, sp.csr_matrix(np.array([[0.0 + 0.0j]])))
+
+
+def test_scaling_benchmark_checksums_bitwise(gpu):
+    """reporting.scaling_benchmark (the C2 harness template, reporting.py:87-122):
+    pole-solution checksums identical across repetitions / worker counts."""
+    prob, _ = rb.build_config("C1", n=6)
+    approx = rb.config_approximant("C1")
+    rows = rb.scaling_benchmark(prob, prob.true_model(), approx, worker_counts=(1, 2),
+                                solve_repeats=2)
+    assert rows[0]["checksum"] == rows[1]["checksum"]
+    assert rows[0]["factorize_ms"] > 0 and rows[0]["solve_ms"] > 0
