@@ -71,6 +71,16 @@ __global__ void __launch_bounds__(256, 2) k_fwd(const SolveTask* __restrict__ ta
   const int r0 = pivot ? blk * PB : p + (blk - npb) * PB;
   const int nr = pivot ? min(PB, p - r0) : min(PB, nf - r0);
   const int jmax = pivot ? blk : npb;
+  cplx* Xs = dsm + 9 * PB * NR;      // [PB][PB+1]: column r0+i of the diagonal block in row i
+  if (pivot) {
+    for (int e = tid; e < nr * nr; e += blockDim.x) {
+      const int i = e / nr, c = e - i * nr;
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(Xs + i * (PB + 1) + c);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                   "l"(panel + (int64_t)(r0 + i) * nf + r0 + c) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
   if (dep.fused) {
     // every child's border (u-vector) tasks must have completed
     const int need = dep.need_u[s];
@@ -109,12 +119,21 @@ __global__ void __launch_bounds__(256, 2) k_fwd(const SolveTask* __restrict__ ta
   }
   constexpr int YPL = (8 * NR + 31) / 32;   // y values per lane per block
   for (int j = 0; j < jmax; ++j) {
+    const int c0 = j * PB, ncol = min(PB, p - c0);
+    // L does not depend on y: issue its loads before waiting for block j
+    cplx l0[8], l1[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int c = warp + 8 * q;
+      const cplx* colp = rowp + (int64_t)(c0 + c) * nf;
+      l0[q] = (c < ncol && ok0) ? __ldg(colp) : cmk(0.0, 0.0);
+      l1[q] = (c < ncol && ok1) ? __ldg(colp + 32) : cmk(0.0, 0.0);
+    }
     if (pivot) {
       if (lane == 0)
         spin_wait_geq(flags + j, epoch);
       __syncwarp();
     }
-    const int c0 = j * PB, ncol = min(PB, p - c0);
     // y of this warp's 8 columns (c0 + warp + 8q), NR each
     cplx yv[YPL];
 #pragma unroll
@@ -124,14 +143,6 @@ __global__ void __launch_bounds__(256, 2) k_fwd(const SolveTask* __restrict__ ta
       const int c = warp + 8 * q;
       yv[h] = (e < 8 * NR && c < ncol) ? ldcg_c(x + (int64_t)(first + c0 + c) * NR + r)
                                        : cmk(0.0, 0.0);
-    }
-    cplx l0[8], l1[8];
-#pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const int c = warp + 8 * q;
-      const cplx* colp = rowp + (int64_t)(c0 + c) * nf;
-      l0[q] = (c < ncol && ok0) ? __ldg(colp) : cmk(0.0, 0.0);
-      l1[q] = (c < ncol && ok1) ? __ldg(colp + 32) : cmk(0.0, 0.0);
     }
 #pragma unroll
     for (int q = 0; q < 8; ++q)
@@ -161,17 +172,20 @@ __global__ void __launch_bounds__(256, 2) k_fwd(const SolveTask* __restrict__ ta
   }
   __syncthreads();
   if (pivot) {
-    // y_i = t_i + sum_{c<i} X[i][c] t_c ; X[i][c] sits at (row r0+c, col r0+i).
+    // y_i = t_i + sum_{c<i} X[i][c] t_c ; X[i][c] sits at (row r0+c, col r0+i),
+    // staged in shared memory at the start of the task.
     // 4 threads per output row (c = k mod 4), shuffle-reduced.
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
     const int i = tid >> 2, k = tid & 3;
     cplx yv[NR];
 #pragma unroll
     for (int r = 0; r < NR; ++r) yv[r] = cmk(0.0, 0.0);
     if (i < nr) {
-      const cplx* xcol = panel + (int64_t)(r0 + i) * nf + r0;
+      const cplx* xcol = Xs + i * (PB + 1);
 #pragma unroll 8
       for (int c = k; c < i; c += 4) {
-        const cplx xv = __ldg(xcol + c);
+        const cplx xv = xcol[c];
 #pragma unroll
         for (int r = 0; r < NR; ++r) yv[r] = cfma(xv, v[c][r], yv[r]);
       }
@@ -234,6 +248,15 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   int* flags = sb.flags[slot] + F.blk_off[s];
   const int c0 = cb * PB, ncol = min(PB, p - c0);
   const int* rows = F.rows + F.rows_off[s];
+  // stage the diagonal block (X^T in its upper triangle) for the final GEMV
+  cplx* Xs = dsm + 2 * PB * NR;       // [PB][PB+1]: Xs[i][c] = panel(row c0+c, col c0+i)
+  for (int e = tid; e < ncol * ncol; e += blockDim.x) {
+    const int i = e / ncol, c = e - i * ncol;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(Xs + i * (PB + 1) + c);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                 "l"(panel + (int64_t)(c0 + i) * nf + c0 + c) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
   cplx acc[4][NR];
 #pragma unroll
   for (int k = 0; k < 4; ++k)
@@ -272,21 +295,29 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   // later pivot blocks of this front (produced by earlier tickets in this
   // launch): per-warp wait, L2 reads
   for (int rb = npb - 1; rb > cb; --rb) {
+    const int q0 = rb * PB, q1 = min(q0 + PB, p);
+    // the block's 64 rows = 2 per lane: load L before waiting for x
+    cplx lv[2][4];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int rho = q0 + lane + 32 * h;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        lv[h][k] = (k < nk && rho < q1) ? __ldg(colp + (int64_t)k * nf + rho) : cmk(0.0, 0.0);
+    }
     if (lane == 0)
       spin_wait_geq(flags + rb, epoch);
     __syncwarp();
-    const int q0 = rb * PB, q1 = min(q0 + PB, p);
-#pragma unroll 2
-    for (int rho = q0 + lane; rho < q1; rho += 32) {
-      cplx lv[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
-        lv[k] = k < nk ? __ldg(colp + (int64_t)k * nf + rho) : cmk(0.0, 0.0);
+    for (int h = 0; h < 2; ++h) {
+      const int rho = q0 + lane + 32 * h;
+      if (rho < q1) {
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        const cplx xv = ldcg_c(x + (int64_t)(first + rho) * NR + r);
+        for (int r = 0; r < NR; ++r) {
+          const cplx xv = ldcg_c(x + (int64_t)(first + rho) * NR + r);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) acc[k][r] = cfma(lv[k], xv, acc[k][r]);
+          for (int k = 0; k < 4; ++k) acc[k][r] = cfma(lv[h][k], xv, acc[k][r]);
+        }
       }
     }
   }
@@ -310,8 +341,10 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
         for (int r = 0; r < NR; ++r) red[cw + k][r] = acc[k][r];
   }
   __syncthreads();
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
   if (tid < ncol) {
-    const cplx d = panel[(int64_t)(c0 + tid) * nf + c0 + tid];
+    const cplx d = Xs[tid * (PB + 1) + tid];
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       const cplx y = x[(int64_t)(first + c0 + tid) * NR + r];
@@ -327,10 +360,9 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
 #pragma unroll
     for (int r = 0; r < NR; ++r) xv[r] = cmk(0.0, 0.0);
     if (c < ncol) {
-      const cplx* xrow = panel + c0 + c;
 #pragma unroll 4
       for (int i = c + 1 + k; i < ncol; i += 8) {
-        const cplx w = __ldg(xrow + (int64_t)(c0 + i) * nf);
+        const cplx w = Xs[i * (PB + 1) + c];
 #pragma unroll
         for (int r = 0; r < NR; ++r) xv[r] = cfma(w, tv[i][r], xv[r]);
       }
@@ -570,7 +602,7 @@ template <int NR>
 static void fwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
                    const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch,
                    const SweepDeps& dep) {
-  const size_t smem = (9 * PB * NR) * sizeof(cplx);
+  const size_t smem = (9 * PB * NR + PB * (PB + 1)) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_fwd<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -582,7 +614,7 @@ template <int NR>
 static void bwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
                    const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch,
                    const SweepDeps& dep) {
-  const size_t smem = (2 * PB * NR) * sizeof(cplx);
+  const size_t smem = (2 * PB * NR + PB * (PB + 1)) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_bwd<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
