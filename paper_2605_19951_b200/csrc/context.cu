@@ -617,9 +617,10 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR) {
       }
       if (c->fwdb_lv[L].second > 0) {
         Timed tm(c, KC_FWD);
+        const int nfr_lv = S.level_ptr[L + 1] - S.level_ptr[L];
         rba::launch_solve_level(c->st, true, NR, c->fwdb_tasks + c->fwdb_lv[L].first,
                                 c->fwdb_lv[L].second, ns, c->F, b, c->tickets + L, c->epoch,
-                                c->parent_d, c->need_u_d, false);
+                                c->parent_d, c->need_u_d, false, nfr_lv <= 2);
         CKL();
       }
     }

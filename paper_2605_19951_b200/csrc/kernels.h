@@ -58,7 +58,7 @@ void launch_trsm3(cudaStream_t st, const PanelTask* tasks, int ntasks, const Fro
 void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* tasks,
                         int ntasks, int nslots, const FrontsDev& F, const SolveBatch& b,
                         int* ticket, int epoch, const int32_t* parent, const int32_t* need_u,
-                        bool fused);
+                        bool fused, bool stagex = false);
 void launch_solve_small(cudaStream_t st, bool forward, int nr, const int32_t* fronts, int nfr,
                         int nslots, const FrontsDev& F, const SolveBatch& b);
 void launch_perm_in(cudaStream_t st, int64_t n, int nrhs, int NR, const int32_t* perm,

@@ -45,7 +45,7 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 // segment; each warp fetches the y values of its 8 columns of a block with one
 // L2 load per lane (they were produced by other CTAs) and broadcasts them with
 // shuffles.  16 L loads per lane are in flight per block.
-template <int NR>
+template <int NR, bool STAGEX>
 __global__ void __launch_bounds__(256, 2) k_fwd(const SolveTask* __restrict__ tasks, int nslots,
                                              FrontsDev F, SolveBatchDev sb, int* ticket,
                                              int /*unused*/, SweepDeps dep) {
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(256, 2) k_fwd(const SolveTask* __restrict__ ta
   const int nr = pivot ? min(PB, p - r0) : min(PB, nf - r0);
   const int jmax = pivot ? blk : npb;
   cplx* Xs = dsm + 9 * PB * NR;      // [PB][PB+1]: column r0+i of the diagonal block in row i
-  if (pivot) {
+  if (STAGEX && pivot) {
     for (int e = tid; e < nr * nr; e += blockDim.x) {
       const int i = e / nr, c = e - i * nr;
       const unsigned sa = (unsigned)__cvta_generic_to_shared(Xs + i * (PB + 1) + c);
@@ -175,14 +175,16 @@ __global__ void __launch_bounds__(256, 2) k_fwd(const SolveTask* __restrict__ ta
     // y_i = t_i + sum_{c<i} X[i][c] t_c ; X[i][c] sits at (row r0+c, col r0+i),
     // staged in shared memory at the start of the task.
     // 4 threads per output row (c = k mod 4), shuffle-reduced.
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    __syncthreads();
+    if (STAGEX) {
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
+      __syncthreads();
+    }
     const int i = tid >> 2, k = tid & 3;
     cplx yv[NR];
 #pragma unroll
     for (int r = 0; r < NR; ++r) yv[r] = cmk(0.0, 0.0);
     if (i < nr) {
-      const cplx* xcol = Xs + i * (PB + 1);
+      const cplx* xcol = STAGEX ? Xs + i * (PB + 1) : panel + (int64_t)(r0 + i) * nf + r0;
 #pragma unroll 8
       for (int c = k; c < i; c += 4) {
         const cplx xv = xcol[c];
@@ -601,20 +603,26 @@ void launch_solve_small(cudaStream_t st, bool forward, int nr, const int32_t* fr
 template <int NR>
 static void fwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
                    const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch,
-                   const SweepDeps& dep) {
-  const size_t smem = (9 * PB * NR + PB * (PB + 1)) * sizeof(cplx);
+                   const SweepDeps& dep, bool stagex) {
+  const size_t smem0 = (9 * PB * NR) * sizeof(cplx);
+  const size_t smem1 = smem0 + PB * (PB + 1) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_fwd<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_fwd<NR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem0);
+    cudaFuncSetAttribute(k_fwd<NR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
     attr = true;
   }
-  k_fwd<NR><<<ntasks * nslots, 256, smem, st>>>(tasks, nslots, F, sb, ticket, epoch, dep);
+  // staging the diagonal block only pays where the pivot chain dominates
+  if (stagex)
+    k_fwd<NR, true><<<ntasks * nslots, 256, smem1, st>>>(tasks, nslots, F, sb, ticket, epoch, dep);
+  else
+    k_fwd<NR, false><<<ntasks * nslots, 256, smem0, st>>>(tasks, nslots, F, sb, ticket, epoch, dep);
 }
 template <int NR>
 static void bwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
                    const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch,
                    const SweepDeps& dep) {
-  const size_t smem = (2 * PB * NR + PB * (PB + 1)) * sizeof(cplx);
+  const size_t smem = (2 * PB * NR + PB * (PB + 1)) * sizeof(cplx);  // + staged X
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_bwd<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -626,7 +634,7 @@ static void bwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslo
 void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* tasks,
                         int ntasks, int nslots, const FrontsDev& F, const SolveBatch& b,
                         int* ticket, int epoch, const int32_t* parent, const int32_t* need_u,
-                        bool fused) {
+                        bool fused, bool stagex) {
   if (ntasks <= 0) return;
   SolveBatchDev sb;
   for (int i = 0; i < nslots; ++i) {
@@ -639,13 +647,13 @@ void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* 
   }
   SweepDeps dep{parent, need_u, fused ? 1 : 0};
   switch (nr) {
-    case 1: forward ? fwd_nr<1>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep)
+    case 1: forward ? fwd_nr<1>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep, stagex)
                     : bwd_nr<1>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep); break;
-    case 2: forward ? fwd_nr<2>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep)
+    case 2: forward ? fwd_nr<2>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep, stagex)
                     : bwd_nr<2>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep); break;
-    case 4: forward ? fwd_nr<4>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep)
+    case 4: forward ? fwd_nr<4>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep, stagex)
                     : bwd_nr<4>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep); break;
-    default: forward ? fwd_nr<8>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep)
+    default: forward ? fwd_nr<8>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep, stagex)
                      : bwd_nr<8>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep); break;
   }
 }
