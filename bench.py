@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--n", type=int, default=None, help="override the mesh size (debug)")
     ap.add_argument("--lsqr", type=int, default=None)
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--shard", type=int, default=0,
+                    help="run only rank 0's pole shard of a G-GPU job on this GPU")
     ap.add_argument("--profile-once", action="store_true",
                     help="one factorisation + one forward only (for ncu captures)")
     return ap.parse_args()
@@ -511,6 +513,66 @@ def run_c3(args, world, rank):
             "adjoint_max_mismatch": worst, "ms_per_action": ms / (2 * trials)}
 
 
+def run_shard(args, world, rank):
+    """Per-rank workload of a G-GPU run on ONE GPU: the poles rank 0 owns
+    (i mod G == 0), factorised and solved (forward, J v and J^T w partials,
+    without the cross-rank exchange).  Used for C5 (20 poles, 8 sources,
+    n = 64: 33 GB of factor per pole), which only fits when sharded."""
+    import torch
+    import paper_2605_19951_b200 as rb
+    from paper_2605_19951_b200.engine import Engine
+    from paper_2605_19951_b200.parallel import PoleComm
+    from paper_2605_19951_b200 import _lib
+    from paper_2605_19951_b200._lib import ptr
+    G = args.shard
+    prob, meta, approx, lsqr_iters = build_workload(args.config, args.n, args.lsqr)
+    eng = Engine(prob, approx, comm=PoleComm(G, 0))
+    eng.set_model(prob.m_true)
+    flops, nnzL = symbolic_stats(eng)
+    stream = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(8)]
+    v = torch.randn(eng.P, dtype=torch.float64, device="cuda")
+    w = torch.randn(eng.S * eng.Kt * eng.Mr, dtype=torch.float64, device="cuda")
+    for _ in range(max(1, args.warmup)):
+        eng.factor()
+        _lib.check(eng.lib.rba_forward_partial(eng.ctx, ptr(eng.qpart)))
+    torch.cuda.synchronize()
+    ev[0].record(stream)
+    eng.factor()
+    ev[1].record(stream)
+    _lib.check(eng.lib.rba_forward_partial(eng.ctx, ptr(eng.qpart)))
+    ev[2].record(stream)
+    _lib.check(eng.lib.rba_jvp_partial(eng.ctx, ptr(v), ptr(eng.qpart)))
+    ev[3].record(stream)
+    _lib.check(eng.lib.rba_vjp_partial(eng.ctx, ptr(w), ptr(eng.tpart)))
+    ev[4].record(stream)
+    torch.cuda.synchronize()
+    tf, tfw, tj, tv = (ev[i].elapsed_time(ev[i + 1]) for i in range(4))
+    nl = len(eng.local)
+    nr = {1: 1, 2: 2, 3: 4, 4: 4}.get(eng.S, 8)
+    bytes_one = 2 * nnzL * 16 + eng.N * 16 + 4 * eng.N * nr * 16
+    phi = 2
+    proj = phi * (tf + tfw) + (2 * lsqr_iters + 2) * 0.5 * (tj + tv)
+    peaks = measured_peaks()
+    fac_tf = flops * nl / (tf * 1e-3) / 1e12
+    return {"metric": METRIC, "value": proj / 1e3,
+            "unit": "s/GN-iteration (projected per-rank, no exchange)", "n_gpus": 1,
+            "shard_of": G, "steps": 1, "warmup": args.warmup, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "c128/f64", "data": "synthetic",
+            "config": {"workload": f"{args.config} rank-0 shard of {G}: {meta['n']}^3 hexes, "
+                                   f"N={eng.N}, poles {eng.local} of {eng.m}, {eng.S} sources x "
+                                   f"{eng.Mr} receivers x {eng.Kt} times"},
+            "factor_ms": tf, "forward_ms": tfw, "jvp_ms": tj, "vjp_ms": tv,
+            "factor_tflops": fac_tf, "solve_gbs": bytes_one * nl / (tfw * 1e-3) / 1e9,
+            "roofline": {"bound": "tensor", "achieved": fac_tf, "peak": peaks["fp64_tflops"],
+                         "unit": "TFLOP/s", "frac": fac_tf / peaks["fp64_tflops"]},
+            "flops_per_pole": flops, "nnzL_per_pole": nnzL,
+            "memory_gb": {k: v / 1e9 for k, v in eng.info().items() if k.startswith("mem")},
+            "note": "projection = 2 line-search evals x (factor + forward) + (2*itn+2) x "
+                    "mean(J v, J^T w) partial times; the all-gather (<0.1 ms over NVLink for "
+                    "these sizes) is not included"}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -519,6 +581,10 @@ def main():
             print(json.dumps(line))
         return
     world, rank = dist_setup(args)
+    if args.shard > 1:
+        line = run_shard(args, world, rank)
+        print(json.dumps(line))
+        return
     if args.config.upper() in ("C2", "C3"):
         line = (run_c2 if args.config.upper() == "C2" else run_c3)(args, world, rank)
         if rank == 0:

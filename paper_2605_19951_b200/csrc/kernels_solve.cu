@@ -259,14 +259,10 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
                  "l"(panel + (int64_t)(c0 + i) * nf + c0 + c) : "memory");
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
-  cplx acc[4][NR];
-#pragma unroll
-  for (int k = 0; k < 4; ++k)
-#pragma unroll
-    for (int r = 0; r < NR; ++r) acc[k][r] = cmk(0.0, 0.0);
-  const int cw = 4 * warp;
-  const int nk = max(0, min(4, ncol - cw));
-  const cplx* colp = panel + (int64_t)(c0 + cw) * nf;
+  // columns per warp per pass: 4 (NR <= 4) or 2 in two passes (NR = 8), so
+  // the accumulators stay in registers
+  constexpr int CPW = NR <= 4 ? 4 : 2;
+  constexpr int NPASS = 4 / CPW;
   if (dep.fused && nf > p) {
     // border rows are final once the parent front is complete (its own tasks
     // waited for every owner of its border)
@@ -277,21 +273,30 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
     __syncthreads();
   }
 
+  for (int pass = 0; pass < NPASS; ++pass) {
+  cplx acc[CPW][NR];
+#pragma unroll
+  for (int k = 0; k < CPW; ++k)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[k][r] = cmk(0.0, 0.0);
+  const int cw = (pass * 16 + warp) * CPW;
+  const int nk = max(0, min(CPW, ncol - cw));
+  const cplx* colp = panel + (int64_t)(c0 + cw) * nf;
   // border rows: pivots of ancestors, final before this launch (L1 is
   // invalidated at launch, so the read-only path is safe); the 16 warps of
   // the CTA read the same x rows, which therefore hit in L1.
 #pragma unroll 2
   for (int rho = p + lane; rho < nf; rho += 32) {
     const int g = __ldg(rows + rho);
-    cplx lv[4];
+    cplx lv[CPW];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < CPW; ++k)
       lv[k] = k < nk ? __ldg(colp + (int64_t)k * nf + rho) : cmk(0.0, 0.0);
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       const cplx xv = __ldg(x + (int64_t)g * NR + r);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) acc[k][r] = cfma(lv[k], xv, acc[k][r]);
+      for (int k = 0; k < CPW; ++k) acc[k][r] = cfma(lv[k], xv, acc[k][r]);
     }
   }
   // later pivot blocks of this front (produced by earlier tickets in this
@@ -299,12 +304,12 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   for (int rb = npb - 1; rb > cb; --rb) {
     const int q0 = rb * PB, q1 = min(q0 + PB, p);
     // the block's 64 rows = 2 per lane: load L before waiting for x
-    cplx lv[2][4];
+    cplx lv[2][CPW];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int rho = q0 + lane + 32 * h;
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < CPW; ++k)
         lv[h][k] = (k < nk && rho < q1) ? __ldg(colp + (int64_t)k * nf + rho) : cmk(0.0, 0.0);
     }
     if (lane == 0)
@@ -318,13 +323,13 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
         for (int r = 0; r < NR; ++r) {
           const cplx xv = ldcg_c(x + (int64_t)(first + rho) * NR + r);
 #pragma unroll
-          for (int k = 0; k < 4; ++k) acc[k][r] = cfma(lv[h][k], xv, acc[k][r]);
+          for (int k = 0; k < CPW; ++k) acc[k][r] = cfma(lv[h][k], xv, acc[k][r]);
         }
       }
     }
   }
 #pragma unroll
-  for (int k = 0; k < 4; ++k)
+  for (int k = 0; k < CPW; ++k)
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       double a = acc[k][r].x, b = acc[k][r].y;
@@ -337,12 +342,13 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
     }
   if (lane == 0) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < CPW; ++k)
       if (k < nk)
 #pragma unroll
         for (int r = 0; r < NR; ++r) red[cw + k][r] = acc[k][r];
   }
   __syncthreads();
+  }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   if (tid < ncol) {
