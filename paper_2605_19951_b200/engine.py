@@ -210,8 +210,10 @@ class Engine:
         """Predicted data d (S*K_t*M_r,) on the device; stores g_i."""
         check(self.lib.rba_forward_partial(self.ctx, ptr(self.qpart)))
         self.g_valid = True
-        qall = self._gather(self.qpart)
         d = torch.empty(self.S * self.Kt * self.Mr, dtype=torch.float64, device=self.device)
+        if self.Mr == 0:
+            return d
+        qall = self._gather(self.qpart)
         check(self.lib.rba_combine_data(self.ctx, ptr(qall), ptr(self.slot_of_pole), 0, ptr(d)))
         return d
 
