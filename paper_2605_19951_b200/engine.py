@@ -52,8 +52,13 @@ class Engine:
                                    else device)
         self.stream = torch.cuda.current_stream(self.device)
         h = _lib.vp()
-        check(self.lib.rba_ctx_create(self.device.index, _lib.vp(self.stream.cuda_stream),
-                                      _lib.C.byref(h)))
+        # run on torch's current stream so torch ops (H2D copies, allocations,
+        # collectives) and the library's kernels are ordered.  torch's default
+        # stream is the legacy NULL stream, which must be passed as
+        # cudaStreamLegacy (0x1): a NULL handle would make the library create
+        # its own non-blocking stream.
+        handle = self.stream.cuda_stream or 0x1
+        check(self.lib.rba_ctx_create(self.device.index, _lib.vp(handle), _lib.C.byref(h)))
         self.ctx = h
         self.problem = problem
         self.N = int(problem.K.shape[0])
