@@ -626,6 +626,17 @@ __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ t
   for (int ch = 0; ch < nchunks; ++ch) {
     cp_wait3<NS3 - 2>();
     __syncthreads();
+    if (MODE == 0) {
+      // scale this stage's B tile by d_t once (instead of per fragment per warp)
+      Stage3& Sw = st[ch % NS3];
+#pragma unroll
+      for (int q = 0; q < (BN3 * T3K) / NT3; ++q) {
+        const int e = tid + q * NT3;
+        const int rr = e % BN3, kk = e / BN3;
+        Sw.b[rr * L3K + kk] = cmul(Sw.b[rr * L3K + kk], Sw.d[kk]);
+      }
+      __syncthreads();
+    }
     issue(ch + NS3 - 1);
     const Stage3& S = st[ch % NS3];
     const int kt = t0 + ch * T3K;
@@ -642,9 +653,7 @@ __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ t
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
         cplx v = S.b[(wn + b * 8 + g) * L3K + k4 + t4];
-        if (MODE == 0) {
-          v = cmul(v, S.d[k4 + t4]);
-        } else {
+        if (MODE == 1) {
           const int c = wn + b * 8 + g, t = kt + k4 + t4;
           v = t < c ? v : (t == c ? cmk(1.0, 0.0) : cmk(0.0, 0.0));
         }
@@ -673,27 +682,45 @@ __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ t
   }
   cp_wait3<0>();
   __syncthreads();
+  if (MODE == 0) {
+    // batched read-modify-write: all C loads of two m-tiles in flight at once
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+    for (int a0 = 0; a0 < 4; a0 += 2) {
+      cplx* dst[2][2][2];
+      cplx cv[2][2][2];
 #pragma unroll
-    for (int b = 0; b < 2; ++b)
+      for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = r0 + wm + a * 8 + g;
-        const int c = cc0 + wn + b * 8 + t4 * 2 + h;
-        if (MODE == 0) {
-          if (r < nf && c < cmax && r >= c) {
-            cplx* dst = faddr(pw, upd, p, nf, r, c);
-            cplx v = *dst;
-            v.x -= cre[a][b][h];
-            v.y -= cim[a][b][h];
-            *dst = v;
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = r0 + wm + (a0 + a) * 8 + g;
+            const int c = cc0 + wn + b * 8 + t4 * 2 + h;
+            dst[a][b][h] = (r < nf && c < cmax && r >= c) ? faddr(pw, upd, p, nf, r, c) : nullptr;
+            cv[a][b][h] = dst[a][b][h] ? __ldcg(dst[a][b][h]) : cmk(0.0, 0.0);
           }
-        } else {
+#pragma unroll
+      for (int a = 0; a < 2; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (dst[a][b][h])
+              *dst[a][b][h] = cmk(cv[a][b][h].x - cre[a0 + a][b][h], cv[a][b][h].y - cim[a0 + a][b][h]);
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + wm + a * 8 + g;
+          const int c = cc0 + wn + b * 8 + t4 * 2 + h;
           if (r < nf && c < cmax)
             pw[(int64_t)(kbase + c) * nf + r] = cmul(cmk(cre[a][b][h], cim[a][b][h]), dinv[c]);
         }
-      }
+  }
 }
 
 void launch_gemm3(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
