@@ -626,17 +626,6 @@ __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ t
   for (int ch = 0; ch < nchunks; ++ch) {
     cp_wait3<NS3 - 2>();
     __syncthreads();
-    if (MODE == 0) {
-      // scale this stage's B tile by d_t once (instead of per fragment per warp)
-      Stage3& Sw = st[ch % NS3];
-#pragma unroll
-      for (int q = 0; q < (BN3 * T3K) / NT3; ++q) {
-        const int e = tid + q * NT3;
-        const int rr = e % BN3, kk = e / BN3;
-        Sw.b[rr * L3K + kk] = cmul(Sw.b[rr * L3K + kk], Sw.d[kk]);
-      }
-      __syncthreads();
-    }
     issue(ch + NS3 - 1);
     const Stage3& S = st[ch % NS3];
     const int kt = t0 + ch * T3K;
@@ -653,7 +642,9 @@ __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ t
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
         cplx v = S.b[(wn + b * 8 + g) * L3K + k4 + t4];
-        if (MODE == 1) {
+        if (MODE == 0) {
+          v = cmul(v, S.d[k4 + t4]);
+        } else {
           const int c = wn + b * 8 + g, t = kt + k4 + t4;
           v = t < c ? v : (t == c ? cmk(1.0, 0.0) : cmk(0.0, 0.0));
         }
