@@ -198,3 +198,53 @@ def test_scaling_benchmark_checksums_bitwise(gpu):
                                 solve_repeats=2)
     assert rows[0]["checksum"] == rows[1]["checksum"]
     assert rows[0]["factorize_ms"] > 0 and rows[0]["solve_ms"] > 0
+
+
+def test_taylor_slopes_device(gpu):
+    """sensitivity.py:135-172 / test_sensitivity.py:166-174 on the device path."""
+    prob, _ = rb.build_config("C1", n=6)
+    approx = rb.config_approximant("C1")
+    m = np.where(prob.m_true < np.log(1e-6), np.log(0.01), prob.m_true)
+    model = rb.Model(m, m)
+    rng = np.random.default_rng(1)
+    direction = rng.standard_normal(prob.grid.cell_count)
+    direction /= np.max(np.abs(direction))
+    rep = rb.taylor_test(prob, model, approx, direction, [1e-1, 1e-2, 1e-3, 1e-4])
+    assert 0.9 <= rep.slope0 <= 1.1
+    assert 1.8 <= rep.slope1 <= 2.2
+
+
+def test_run_inversion_matches_oracle_first_iteration(gpu):
+    """One full GN iteration of run_inversion (gradient, 5 LSQR its, Armijo
+    line search with refactorisations) against the oracle's restatement on the
+    same inputs: same accepted step and objective to tolerance."""
+    z = golden("ref3d_n6.npz")
+    prob, _ = rb.build_config("C1", n=6)
+    approx = rb.config_approximant("C1")
+    data = _data(z)
+    reg = rb.build_reg(prob.grid, root="chol")
+    cfg = rb.InversionConfig(lambda0=float(z["lam"]), max_gn=1, chi2_target=0.0,
+                             lsqr=rb.LsqrConfig(tol=0.0, max_iters=5), m0=z["m"])
+    prob.sigma_background = float(np.exp(z["m"][0]))
+    st = rb.run_inversion(prob, data, approx, cfg, reg=reg)
+    rec = st.history[0]
+    # oracle: same iteration by hand
+    fac = orc.PoleFactors()
+    m0 = z["m"]
+    W = 1.0 / z["sigma_d"]
+    d0, g = orc.forward_response(prob, m0, approx.poles, approx.residues, fac)
+    J = orc.Jacobian(prob, m0, approx.poles, approx.residues, fac, g=g)
+    dm, _, _ = orc.augmented_lsqr(J, reg.R_factor, W, z["d_obs"], d0, m0, m0,
+                                  float(z["lam"]), 0.0, 5)
+    def phi(mm):
+        d, _ = orc.forward_response(prob, mm, approx.poles, approx.residues, orc.PoleFactors())
+        r = mm - m0
+        return 0.5 * float(np.sum((W * (d - z["d_obs"])) ** 2)) + float(z["lam"]) * 0.5 * float(r @ (reg.L @ r))
+    phi0 = phi(m0)
+    grad = J.vjp(W * W * (d0 - z["d_obs"]))
+    slope = float(grad @ dm)
+    eta, ok, phi_acc, n = orc.line_search(phi0, slope, lambda e: phi(m0 + e * dm))
+    assert rec.accepted == ok and rec.phi_evals == n
+    assert abs(rec.eta - eta) <= 1e-6 * max(1.0, abs(eta))
+    assert abs(rec.phi - phi_acc) <= 1e-6 * abs(phi_acc)
+    assert abs(rec.directional_slope - slope) <= 1e-6 * abs(slope)
