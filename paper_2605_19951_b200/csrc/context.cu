@@ -138,6 +138,8 @@ struct rba_ctx {
   double cls_ms[128] = {0};   // 0-15 kernel classes; 16+L fwd, 48+L bwd, 80+L gemm per level
   bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernels
   int gemm_v = 3;             // RBA_GEMM=v1|v2 select the earlier DMMA kernels
+  int gemm_var = 1;           // v3 stage shape: 1 (default, RBA_GEMM=v4) = 16 k x 2 stages,
+                              // 0 (RBA_GEMM=v3) = 8 k x 3 stages
   int64_t launches = 0;
   std::vector<cudaEvent_t> evpool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -477,7 +479,7 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
         else if (c->gemm_v == 1)
           rba::launch_trsm_dmma(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
         else if (c->gemm_v == 3)
-          rba::launch_trsm3(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
+          rba::launch_trsm3(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->gemm_var);
         else
           rba::launch_trsm2(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
         break;
@@ -489,7 +491,7 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
         else if (c->gemm_v == 1)
           rba::launch_gemm_dmma(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
         else if (c->gemm_v == 3)
-          rba::launch_gemm3(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
+          rba::launch_gemm3(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->gemm_var);
         else
           rba::launch_gemm2(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
         break;
@@ -765,7 +767,8 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     c->gemm_dfma = std::string(e) == "dfma";
     if (std::string(e) == "v1" || c->gemm_dfma) c->gemm_v = 1;
     if (std::string(e) == "v2") c->gemm_v = 2;
-    if (std::string(e) == "v3") c->gemm_v = 3;
+    if (std::string(e) == "v3") { c->gemm_v = 3; c->gemm_var = 0; }
+    if (std::string(e) == "v4") { c->gemm_v = 3; c->gemm_var = 1; }
   }
   if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) == "fused";
   if (const char* e = getenv("RBA_DIAG")) c->diag_v1 = std::string(e) == "v1";

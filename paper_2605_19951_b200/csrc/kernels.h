@@ -50,9 +50,9 @@ void launch_gemm2(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
 void launch_trsm2(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
                   const PoleBatch& pb);
 void launch_gemm3(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
-                  const FrontsDev& F, const PoleBatch& pb);
+                  const FrontsDev& F, const PoleBatch& pb, int variant);
 void launch_trsm3(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
-                  const PoleBatch& pb);
+                  const PoleBatch& pb, int variant);
 
 // solves
 void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* tasks,

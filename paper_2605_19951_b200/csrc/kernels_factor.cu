@@ -211,11 +211,13 @@ constexpr int SB = 16;
 
 __global__ void __launch_bounds__(256) k_diag2(const PanelTask* __restrict__ tasks, FrontsDev F,
                                                PoleBatch pb, int* err) {
+  // Dg holds L (lower) and, transposed in the free upper triangle, X = L^{-1}
+  // (X[i][j], i > j, at Dg[j][i]) -- exactly the panel layout written back.
+  // Ts is one 16-row block row of T; 85 KB in all -> 2 CTAs per SM.
   extern __shared__ cplx sm[];
   cplx* Dg = sm;                   // [PB][LDS]
-  cplx* Xs = sm + PB * LDS;        // [PB][LDS]
-  cplx* Ts = sm + 2 * PB * LDS;    // [PB][LDS]
-  cplx* dv = sm + 3 * PB * LDS;    // [PB]
+  cplx* Ts = sm + PB * LDS;        // [SB][LDS]
+  cplx* dv = Ts + SB * LDS;        // [PB]
   cplx* di = dv + PB;              // [PB]
   const int slot = blockIdx.y;
   const PanelTask tk = tasks[blockIdx.x];
@@ -290,39 +292,41 @@ __global__ void __launch_bounds__(256) k_diag2(const PanelTask* __restrict__ tas
     if (j < b1) {
       for (int i = j + 1; i < b1; ++i) {
         cplx acc = Dg[i * LDS + j];
-        for (int t = j + 1; t < i; ++t) acc = cfma(Dg[i * LDS + t], Xs[t * LDS + j], acc);
-        Xs[i * LDS + j] = cmk(-acc.x, -acc.y);
+        for (int t = j + 1; t < i; ++t) acc = cfma(Dg[i * LDS + t], Dg[j * LDS + t], acc);
+        Dg[j * LDS + i] = cmk(-acc.x, -acc.y);
       }
     }
   }
   __syncthreads();
   for (int bi = 1; bi < nsub; ++bi) {
     const int i0 = bi * SB, i1 = min(i0 + SB, kb), ni = i1 - i0;
+    // T = L[bi, :i0] X[:i0, :i0]  (X[t][j] at Dg[j][t])
     for (int q = tid; q < ni * i0; q += blockDim.x) {
       const int i = i0 + q % ni, j = q / ni;
       cplx acc = Dg[i * LDS + j];
-      for (int t = j + 1; t < i0; ++t) acc = cfma(Dg[i * LDS + t], Xs[t * LDS + j], acc);
-      Ts[i * LDS + j] = acc;
+      for (int t = j + 1; t < i0; ++t) acc = cfma(Dg[i * LDS + t], Dg[j * LDS + t], acc);
+      Ts[(i - i0) * LDS + j] = acc;
     }
     __syncthreads();
+    // X[bi, :i0] = -X[bi, bi] T   (X[i][t] at Dg[t][i])
     for (int q = tid; q < ni * i0; q += blockDim.x) {
       const int i = i0 + q % ni, j = q / ni;
-      cplx acc = Ts[i * LDS + j];
-      for (int t = i0; t < i; ++t) acc = cfma(Xs[i * LDS + t], Ts[t * LDS + j], acc);
-      Xs[i * LDS + j] = cmk(-acc.x, -acc.y);
+      cplx acc = Ts[(i - i0) * LDS + j];
+      for (int t = i0; t < i; ++t) acc = cfma(Dg[t * LDS + i], Ts[(t - i0) * LDS + j], acc);
+      Dg[j * LDS + i] = cmk(-acc.x, -acc.y);
     }
     __syncthreads();
   }
   for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
     int i = idx % kb, j = idx / kb;
-    panel[(int64_t)(k0 + j) * nf + k0 + i] = i >= j ? Dg[i * LDS + j] : Xs[j * LDS + i];
+    panel[(int64_t)(k0 + j) * nf + k0 + i] = Dg[i * LDS + j];
   }
 }
 
 void launch_diag2(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
                   const PoleBatch& pb, int* err) {
   if (ntasks <= 0) return;
-  size_t smem = (3 * PB * LDS + 2 * PB) * sizeof(cplx);
+  size_t smem = ((PB + SB) * LDS + 2 * PB) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_diag2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -510,9 +510,6 @@ void launch_trsm2(cudaStream_t st, const PanelTask* tasks, int ntasks, const Fro
 // mask of X (MODE 1) are applied to the B fragments in registers.
 // ---------------------------------------------------------------------------
 namespace {
-constexpr int T3K = 8;             // k per stage (complex)
-constexpr int L3K = T3K + 4;       // padded row stride (complex): 12 x 16 B -> conflict-free
-constexpr int NS3 = 3;             // pipeline stages
 constexpr int BM3 = 64, BN3 = 64;
 constexpr int NT3 = 256;
 
@@ -526,19 +523,25 @@ __device__ __forceinline__ void cp_commit3() { asm volatile("cp.async.commit_gro
 template <int N>
 __device__ __forceinline__ void cp_wait3() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
+// T3K: k per stage (complex); row stride T3K + 4 (x 16 B) keeps the LDS.128
+// fragment loads conflict-free
+template <int T3K>
 struct Stage3 {
+  static constexpr int L3K = T3K + 4;
   cplx a[BM3 * L3K];
   cplx b[BN3 * L3K];
   cplx d[T3K];
 };
 }  // namespace
 
-template <int MODE>
+template <int MODE, int T3K, int NS3>
 __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ tasks, int ntasks,
                                                   const PanelTask* __restrict__ ptasks,
                                                   FrontsDev F, PoleBatch pb) {
   extern __shared__ __align__(16) unsigned char smraw3[];
-  Stage3* st = reinterpret_cast<Stage3*>(smraw3);
+  using St = Stage3<T3K>;
+  constexpr int L3K = St::L3K;
+  St* st = reinterpret_cast<St*>(smraw3);
   __shared__ cplx dinv[BN3];
   const int slot = blockIdx.y;
   int s, t0, t1, r0, cc0, cmax, kbase = 0;
@@ -586,7 +589,7 @@ __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ t
   const int nchunks = (t1 - t0 + T3K - 1) / T3K;
   auto issue = [&](int ch) {
     if (ch < nchunks) {
-      Stage3& S = st[ch % NS3];
+      St& S = st[ch % NS3];
       const int kt = t0 + ch * T3K;
 #pragma unroll
       for (int q = 0; q < (BM3 * T3K) / NT3; ++q) {
@@ -627,7 +630,7 @@ __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ t
     cp_wait3<NS3 - 2>();
     __syncthreads();
     issue(ch + NS3 - 1);
-    const Stage3& S = st[ch % NS3];
+    const St& S = st[ch % NS3];
     const int kt = t0 + ch * T3K;
 #pragma unroll
     for (int k4 = 0; k4 < T3K; k4 += 4) {
@@ -714,30 +717,34 @@ __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ t
   }
 }
 
-void launch_gemm3(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
-                  const FrontsDev& F, const PoleBatch& pb) {
-  if (ntasks <= 0 || nctas <= 0) return;
-  const size_t smem = NS3 * sizeof(Stage3);
+template <int MODE, int T3K, int NS3>
+static void launch_g3(cudaStream_t st, dim3 grid, const GemmTask* tasks, int ntasks,
+                      const PanelTask* ptasks, const FrontsDev& F, const PoleBatch& pb) {
+  const size_t smem = NS3 * sizeof(Stage3<T3K>);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm3<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_gemm3<MODE, T3K, NS3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
     attr = true;
   }
+  k_gemm3<MODE, T3K, NS3><<<grid, NT3, smem, st>>>(tasks, ntasks, ptasks, F, pb);
+}
+
+// variant 0: 8 k per stage, 3 stages; variant 1: 16 k per stage, 2 stages
+void launch_gemm3(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
+                  const FrontsDev& F, const PoleBatch& pb, int variant) {
+  if (ntasks <= 0 || nctas <= 0) return;
   dim3 grid(nctas, pb.count);
-  k_gemm3<0><<<grid, NT3, smem, st>>>(tasks, ntasks, nullptr, F, pb);
+  if (variant == 1) launch_g3<0, 16, 2>(st, grid, tasks, ntasks, nullptr, F, pb);
+  else launch_g3<0, 8, 3>(st, grid, tasks, ntasks, nullptr, F, pb);
 }
 
 void launch_trsm3(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
-                  const PoleBatch& pb) {
+                  const PoleBatch& pb, int variant) {
   if (ntasks <= 0) return;
-  const size_t smem = NS3 * sizeof(Stage3);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gemm3<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
   dim3 grid(ntasks, pb.count);
-  k_gemm3<1><<<grid, NT3, smem, st>>>(nullptr, 0, tasks, F, pb);
+  if (variant == 1) launch_g3<1, 16, 2>(st, grid, nullptr, 0, tasks, F, pb);
+  else launch_g3<1, 8, 3>(st, grid, nullptr, 0, tasks, F, pb);
 }
 
 
