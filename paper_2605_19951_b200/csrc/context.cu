@@ -80,6 +80,7 @@ struct rba_ctx {
   rba::PanelTask* pt_tasks = nullptr;
   rba::GemmTask* gm_tasks = nullptr;
   std::vector<std::pair<int64_t, int>> fwd_lv, bwd_lv, fwdb_lv, bwdb_lv, small_lv;
+  std::vector<int> small_mb;   // per level: pivot blocks of the largest warp-per-front front
   rba::SolveTask *fwdb_tasks = nullptr, *bwdb_tasks = nullptr;
   int32_t* small_fronts = nullptr;
   rba::SolveTask *fwd_tasks = nullptr, *bwd_tasks = nullptr, *bwd_all = nullptr;
@@ -138,6 +139,7 @@ struct rba_ctx {
   double cls_ms[128] = {0};   // 0-15 kernel classes; 16+L fwd, 48+L bwd, 80+L gemm per level
   bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernels
   int gemm_v = 3;             // RBA_GEMM=v1|v2 select the earlier DMMA kernels
+  int small_p = 2 * rba::PB;  // warp-per-front solves up to this npiv (RBA_SMALLP=64|128)
   int gemm_var = 1;           // v3 stage shape: 1 (default, RBA_GEMM=v4) = 16 k x 2 stages,
                               // 0 (RBA_GEMM=v3) = 8 k x 3 stages
   int64_t launches = 0;
@@ -346,6 +348,7 @@ int build_plans(rba_ctx* c) {
   c->fwdb_lv.assign(S.nlevels, {0, 0});
   c->bwdb_lv.assign(S.nlevels, {0, 0});
   c->small_lv.assign(S.nlevels, {0, 0});
+  c->small_mb.assign(S.nlevels, 1);
   std::vector<int64_t> blk_off(S.nfront + 1, 0);
   for (int s = 0; s < S.nfront; ++s) blk_off[s + 1] = blk_off[s] + (S.npiv[s] + rba::PB - 1) / rba::PB;
   c->nblocks = blk_off[S.nfront];
@@ -367,18 +370,21 @@ int build_plans(rba_ctx* c) {
         if (b < npb + nbb) ft.push_back({s, b});
       }
     c->fwd_lv[L] = {off, (int)(ft.size() - off)};
-    // split for the per-level path: single-pivot-block fronts go to the
-    // warp-per-front kernels, the rest keep the block-task kernels
+    // split for the per-level path: fronts with at most two pivot blocks go
+    // to the warp-per-front kernels, the rest keep the block-task kernels
     {
       int64_t so = smallf.size();
       for (int q = q0; q < q1; ++q)
-        if (S.npiv[S.level_fronts[q]] <= rba::PB) smallf.push_back(S.level_fronts[q]);
+        if (S.npiv[S.level_fronts[q]] <= c->small_p) {
+          smallf.push_back(S.level_fronts[q]);
+          if (S.npiv[S.level_fronts[q]] > rba::PB) c->small_mb[L] = 2;
+        }
       c->small_lv[L] = {so, (int)(smallf.size() - so)};
       int64_t bo = ftb.size();
       for (int b = 0; b < bmax; ++b)
         for (int q = q0; q < q1; ++q) {
           int s = S.level_fronts[q];
-          if (S.npiv[s] <= rba::PB) continue;
+          if (S.npiv[s] <= c->small_p) continue;
           int npb = (S.npiv[s] + rba::PB - 1) / rba::PB;
           int nbb = (S.nf[s] - S.npiv[s] + rba::PB - 1) / rba::PB;
           if (b < npb + nbb) ftb.push_back({s, b});
@@ -400,7 +406,7 @@ int build_plans(rba_ctx* c) {
       for (int key = 0; key < pmax; ++key)
         for (int q = q0; q < q1; ++q) {
           int s = S.level_fronts[q];
-          if (S.npiv[s] <= rba::PB) continue;
+          if (S.npiv[s] <= c->small_p) continue;
           int npb = (S.npiv[s] + rba::PB - 1) / rba::PB;
           if (key < npb) btb.push_back({s, npb - 1 - key});
         }
@@ -614,7 +620,7 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR) {
       if (c->small_lv[L].second > 0) {
         Timed tm(c, KC_FWD);
         rba::launch_solve_small(c->st, true, NR, c->small_fronts + c->small_lv[L].first,
-                                c->small_lv[L].second, ns, c->F, b);
+                                c->small_lv[L].second, ns, c->F, b, c->small_mb[L]);
         CKL();
       }
       if (c->fwdb_lv[L].second > 0) {
@@ -639,7 +645,7 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR) {
       if (c->small_lv[L].second > 0) {
         Timed tm(c, KC_BWD);
         rba::launch_solve_small(c->st, false, NR, c->small_fronts + c->small_lv[L].first,
-                                c->small_lv[L].second, ns, c->F, b);
+                                c->small_lv[L].second, ns, c->F, b, c->small_mb[L]);
         CKL();
       }
     }
@@ -771,6 +777,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     if (std::string(e) == "v4") { c->gemm_v = 3; c->gemm_var = 1; }
   }
   if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) == "fused";
+  if (const char* e = getenv("RBA_SMALLP")) c->small_p = std::string(e) == "64" ? rba::PB : 2 * rba::PB;
   if (const char* e = getenv("RBA_DIAG")) c->diag_v1 = std::string(e) == "v1";
   int rc;
   if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||

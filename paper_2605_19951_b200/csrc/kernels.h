@@ -60,7 +60,7 @@ void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* 
                         int* ticket, int epoch, const int32_t* parent, const int32_t* need_u,
                         bool fused, bool stagex = false);
 void launch_solve_small(cudaStream_t st, bool forward, int nr, const int32_t* fronts, int nfr,
-                        int nslots, const FrontsDev& F, const SolveBatch& b);
+                        int nslots, const FrontsDev& F, const SolveBatch& b, int mb);
 void launch_perm_in(cudaStream_t st, int64_t n, int nrhs, int NR, const int32_t* perm,
                     const cplx* b, int64_t ldb, cplx* x);
 void launch_perm_out(cudaStream_t st, int64_t n, int nrhs, int NR, const int32_t* perm,

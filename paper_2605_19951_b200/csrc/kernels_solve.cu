@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
 // the whole front -- no tickets, flags or block barriers.  The bottom levels
 // of the tree (C4: levels 0-4, ~20k fronts per pole) are all of this kind.
 // ---------------------------------------------------------------------------
-template <int NR>
+template <int NR, int MB>
 __global__ void __launch_bounds__(256) k_fwd_small(const int32_t* __restrict__ fronts, int nfr,
                                                    int nslots, FrontsDev F, SolveBatchDev sb) {
   extern __shared__ cplx dsm[];
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(256) k_fwd_small(const int32_t* __restrict__ f
   if (item >= nfr * nslots) return;
   const int slot = item % nslots;
   const int s = fronts[item / nslots];
-  cplx(*vy)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + warp * PB * NR);   // [PB][NR]
+  cplx(*vy)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + warp * MB * PB * NR);   // [MB*PB][NR]
   const int p = F.npiv[s], nf = F.nf[s], first = F.first[s];
   const cplx* panel = sb.factor[slot] + F.panel_off[s];
   cplx* x = sb.x[slot];
@@ -433,37 +433,58 @@ __global__ void __launch_bounds__(256) k_fwd_small(const int32_t* __restrict__ f
     for (int r = 0; r < NR; ++r) vy[c][r] = val[r];
   }
   __syncwarp();
-  // y = X v  (X = L_bb^{-1}; X[c][t] sits at (row t, col c))
-  cplx yv[2][NR];
+  for (int c0 = 0; c0 < p; c0 += PB) {
+    const int pb = min(PB, p - c0);
+    // y = X v on this pivot block (X = L_bb^{-1}; X[c][t] sits at (row t, col c))
+    cplx yv[2][NR];
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int c = lane + 32 * h;
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
 #pragma unroll
-    for (int r = 0; r < NR; ++r) yv[h][r] = cmk(0.0, 0.0);
-    if (c < p) {
-      const cplx* xc = panel + (int64_t)c * nf;
+      for (int r = 0; r < NR; ++r) yv[h][r] = cmk(0.0, 0.0);
+      if (c < pb) {
+        const cplx* xc = panel + (int64_t)(c0 + c) * nf + c0;
 #pragma unroll
-      for (int r = 0; r < NR; ++r) yv[h][r] = vy[c][r];
-      for (int t = 0; t < c; ++t) {
-        const cplx w = __ldg(xc + t);
+        for (int r = 0; r < NR; ++r) yv[h][r] = vy[c0 + c][r];
+        for (int t = 0; t < c; ++t) {
+          const cplx w = __ldg(xc + t);
 #pragma unroll
-        for (int r = 0; r < NR; ++r) yv[h][r] = cfma(w, vy[t][r], yv[h][r]);
+          for (int r = 0; r < NR; ++r) yv[h][r] = cfma(w, vy[c0 + t][r], yv[h][r]);
+        }
       }
     }
-  }
-  __syncwarp();
+    __syncwarp();
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int c = lane + 32 * h;
-    if (c < p) {
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (c < pb) {
 #pragma unroll
-      for (int r = 0; r < NR; ++r) {
-        vy[c][r] = yv[h][r];
-        x[(int64_t)(first + c) * NR + r] = yv[h][r];
+        for (int r = 0; r < NR; ++r) {
+          vy[c0 + c][r] = yv[h][r];
+          x[(int64_t)(first + c0 + c) * NR + r] = yv[h][r];
+        }
       }
     }
+    __syncwarp();
+    if (MB > 1) {
+      // later pivot rows: v -= L[rows, block] y_block
+      for (int rho = c0 + PB + lane; rho < p; rho += 32) {
+        cplx acc[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) acc[r] = vy[rho][r];
+        const cplx* lrow = panel + (int64_t)c0 * nf + rho;
+#pragma unroll 4
+        for (int c = 0; c < pb; ++c) {
+          const cplx l = __ldg(lrow + (int64_t)c * nf);
+#pragma unroll
+          for (int r = 0; r < NR; ++r) acc[r] = cfms(l, vy[c0 + c][r], acc[r]);
+        }
+#pragma unroll
+        for (int r = 0; r < NR; ++r) vy[rho][r] = acc[r];
+      }
+      __syncwarp();
+    }
   }
-  __syncwarp();
   // border rows: u = contributions - L21 y
   cplx* uout = sb.uvec[slot] + F.uvec_off[s] * NR;
   for (int rho = p + lane; rho < nf; rho += 32) {
@@ -497,84 +518,99 @@ __global__ void __launch_bounds__(256) k_bwd_small(const int32_t* __restrict__ f
   const int slot = item % nslots;
   const int s = fronts[item / nslots];
   cplx(*xs)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + warp * 2 * 32 * NR);   // [32][NR] chunk
-  cplx(*ts)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + warp * 2 * 32 * NR + 32 * NR);
+  cplx(*tv)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + 16 * 32 * NR + warp * PB * NR);
   const int p = F.npiv[s], nf = F.nf[s], first = F.first[s];
   const cplx* panel = sb.factor[slot] + F.panel_off[s];
   cplx* x = sb.x[slot];
   const int* rows = F.rows + F.rows_off[s];
-  cplx acc[2][NR];
+  // pivot blocks from the last one down; rows beyond the block are final
+  // (ancestors: before this launch; later blocks: written by this warp, so
+  // read with coherent loads)
+  for (int c0 = ((p - 1) / PB) * PB; c0 >= 0; c0 -= PB) {
+    const int pb = min(PB, p - c0);
+    cplx acc[2][NR];
 #pragma unroll
-  for (int h = 0; h < 2; ++h)
+    for (int h = 0; h < 2; ++h)
 #pragma unroll
-    for (int r = 0; r < NR; ++r) acc[h][r] = cmk(0.0, 0.0);
-  // border rows in chunks of 32: gather x (ancestors, final) then stream L columns
-  for (int q0 = p; q0 < nf; q0 += 32) {
-    const int n = min(32, nf - q0);
-    if (lane < n) {
-      const int g = __ldg(rows + q0 + lane);
+      for (int r = 0; r < NR; ++r) acc[h][r] = cmk(0.0, 0.0);
+    // rows beyond the block in chunks of 32: gather x then stream L columns
+    for (int q0 = c0 + pb; q0 < nf; q0 += 32) {
+      const int n = min(32, nf - q0);
+      if (lane < n) {
+        const int g = __ldg(rows + q0 + lane);
 #pragma unroll
-      for (int r = 0; r < NR; ++r) xs[lane][r] = __ldg(x + (int64_t)g * NR + r);
+        for (int r = 0; r < NR; ++r) xs[lane][r] = x[(int64_t)g * NR + r];
+      }
+      __syncwarp();
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = lane + 32 * h;
+        if (c < pb) {
+          const cplx* lc = panel + (int64_t)(c0 + c) * nf + q0;
+          for (int i = 0; i < n; ++i) {
+            const cplx l = __ldg(lc + i);
+#pragma unroll
+            for (int r = 0; r < NR; ++r) acc[h][r] = cfma(l, xs[i][r], acc[h][r]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+    // t = y / d - acc, then x = X^T t  (X[i][c] at (row c, col i), i > c)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int c = lane + 32 * h;
+      if (c < pb) {
+        const cplx d = panel[(int64_t)(c0 + c) * nf + c0 + c];
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+          tv[c][r] = csub(cdiv(x[(int64_t)(first + c0 + c) * NR + r], d), acc[h][r]);
+      }
     }
     __syncwarp();
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int c = lane + 32 * h;
-      if (c < p) {
-        const cplx* lc = panel + (int64_t)c * nf + q0;
-        for (int i = 0; i < n; ++i) {
-          const cplx l = __ldg(lc + i);
+      if (c < pb) {
+        cplx xv[NR];
 #pragma unroll
-          for (int r = 0; r < NR; ++r) acc[h][r] = cfma(l, xs[i][r], acc[h][r]);
+        for (int r = 0; r < NR; ++r) xv[r] = tv[c][r];
+        for (int i = c + 1; i < pb; ++i) {
+          const cplx w = __ldg(panel + (int64_t)(c0 + i) * nf + c0 + c);
+#pragma unroll
+          for (int r = 0; r < NR; ++r) xv[r] = cfma(w, tv[i][r], xv[r]);
         }
+#pragma unroll
+        for (int r = 0; r < NR; ++r) x[(int64_t)(first + c0 + c) * NR + r] = xv[r];
       }
     }
     __syncwarp();
   }
-  // t = y / d - acc, then x = X^T t  (X[i][c] at (row c, col i), i > c)
-  cplx(*tv)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + 16 * 32 * NR + warp * PB * NR);
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int c = lane + 32 * h;
-    if (c < p) {
-      const cplx d = panel[(int64_t)c * nf + c];
-#pragma unroll
-      for (int r = 0; r < NR; ++r)
-        tv[c][r] = csub(cdiv(x[(int64_t)(first + c) * NR + r], d), acc[h][r]);
-    }
-  }
-  __syncwarp();
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int c = lane + 32 * h;
-    if (c < p) {
-      cplx xv[NR];
-#pragma unroll
-      for (int r = 0; r < NR; ++r) xv[r] = tv[c][r];
-      for (int i = c + 1; i < p; ++i) {
-        const cplx w = __ldg(panel + (int64_t)i * nf + c);
-#pragma unroll
-        for (int r = 0; r < NR; ++r) xv[r] = cfma(w, tv[i][r], xv[r]);
-      }
-#pragma unroll
-      for (int r = 0; r < NR; ++r) x[(int64_t)(first + c) * NR + r] = xv[r];
-    }
-  }
-  (void)ts;
 }
 
 template <int NR>
 static void small_nr(cudaStream_t st, bool forward, const int32_t* fronts, int nfr, int nslots,
-                     const FrontsDev& F, const SolveBatchDev& sb) {
+                     const FrontsDev& F, const SolveBatchDev& sb, int mb) {
   const int items = nfr * nslots;
   const int grid = (items + 7) / 8;
   if (forward) {
-    const size_t smem = 8 * PB * NR * sizeof(cplx);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_fwd_small<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
+    if (mb <= 1) {
+      const size_t smem = 8 * PB * NR * sizeof(cplx);
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_fwd_small<NR, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+      }
+      k_fwd_small<NR, 1><<<grid, 256, smem, st>>>(fronts, nfr, nslots, F, sb);
+    } else {
+      const size_t smem = 8 * 2 * PB * NR * sizeof(cplx);
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_fwd_small<NR, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+      }
+      k_fwd_small<NR, 2><<<grid, 256, smem, st>>>(fronts, nfr, nslots, F, sb);
     }
-    k_fwd_small<NR><<<grid, 256, smem, st>>>(fronts, nfr, nslots, F, sb);
   } else {
     const size_t smem = (16 * 32 * NR + 8 * PB * NR) * sizeof(cplx);
     static bool attr = false;
@@ -587,7 +623,7 @@ static void small_nr(cudaStream_t st, bool forward, const int32_t* fronts, int n
 }
 
 void launch_solve_small(cudaStream_t st, bool forward, int nr, const int32_t* fronts, int nfr,
-                        int nslots, const FrontsDev& F, const SolveBatch& b) {
+                        int nslots, const FrontsDev& F, const SolveBatch& b, int mb) {
   if (nfr <= 0) return;
   SolveBatchDev sb;
   for (int i = 0; i < nslots; ++i) {
@@ -599,10 +635,10 @@ void launch_solve_small(cudaStream_t st, bool forward, int nr, const int32_t* fr
     sb.epoch[i] = 0;
   }
   switch (nr) {
-    case 1: small_nr<1>(st, forward, fronts, nfr, nslots, F, sb); break;
-    case 2: small_nr<2>(st, forward, fronts, nfr, nslots, F, sb); break;
-    case 4: small_nr<4>(st, forward, fronts, nfr, nslots, F, sb); break;
-    default: small_nr<8>(st, forward, fronts, nfr, nslots, F, sb); break;
+    case 1: small_nr<1>(st, forward, fronts, nfr, nslots, F, sb, mb); break;
+    case 2: small_nr<2>(st, forward, fronts, nfr, nslots, F, sb, mb); break;
+    case 4: small_nr<4>(st, forward, fronts, nfr, nslots, F, sb, mb); break;
+    default: small_nr<8>(st, forward, fronts, nfr, nslots, F, sb, mb); break;
   }
 }
 
