@@ -127,6 +127,7 @@ struct rba_ctx {
   // misc
   double* red_part = nullptr;
   double* red_res = nullptr;
+  cplx* zeros = nullptr;      // 1 KB of zeros: source of out-of-range bulk-copy columns
   int* err_d = nullptr;
   int64_t n_fact = 0, n_solve = 0;
   int epoch = 0;
@@ -138,7 +139,7 @@ struct rba_ctx {
   // by rba_set_timing) and the launch count of this context's kernels
   double cls_ms[128] = {0};   // 0-15 kernel classes; 16+L fwd, 48+L bwd, 80+L gemm per level
   bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernels
-  int gemm_v = 3;             // RBA_GEMM=v1|v2 select the earlier DMMA kernels
+  int gemm_v = 5;             // RBA_GEMM=v1|v2|v3|v4 select the earlier DMMA kernels
   int small_p = 2 * rba::PB;  // warp-per-front solves up to this npiv (RBA_SMALLP=64|128)
   int gemm_var = 1;           // v3 stage shape: 1 (default, RBA_GEMM=v4) = 16 k x 2 stages,
                               // 0 (RBA_GEMM=v3) = 8 k x 3 stages
@@ -484,7 +485,7 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
           rba::launch_trsm(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
         else if (c->gemm_v == 1)
           rba::launch_trsm_dmma(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
-        else if (c->gemm_v == 3)
+        else if (c->gemm_v == 3 || c->gemm_v == 5)
           rba::launch_trsm3(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->gemm_var);
         else
           rba::launch_trsm2(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
@@ -498,6 +499,8 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
           rba::launch_gemm_dmma(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
         else if (c->gemm_v == 3)
           rba::launch_gemm3(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->gemm_var);
+        else if (c->gemm_v == 5)
+          rba::launch_gemm5(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros);
         else
           rba::launch_gemm2(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
         break;
@@ -775,6 +778,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     if (std::string(e) == "v2") c->gemm_v = 2;
     if (std::string(e) == "v3") { c->gemm_v = 3; c->gemm_var = 0; }
     if (std::string(e) == "v4") { c->gemm_v = 3; c->gemm_var = 1; }
+    if (std::string(e) == "v5") { c->gemm_v = 5; c->gemm_var = 1; }
   }
   if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) == "fused";
   if (const char* e = getenv("RBA_SMALLP")) c->small_p = std::string(e) == "64" ? rba::PB : 2 * rba::PB;
@@ -782,11 +786,13 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   int rc;
   if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||
       (rc = dalloc(c, c->allocs, &c->red_part, 1024, &c->mem_other)) ||
-      (rc = dalloc(c, c->allocs, &c->red_res, 8, &c->mem_other))) {
+      (rc = dalloc(c, c->allocs, &c->red_res, 8, &c->mem_other)) ||
+      (rc = dalloc(c, c->allocs, &c->zeros, 64, &c->mem_other))) {
     rba_ctx_destroy(c);
     return rc;
   }
   cudaMemsetAsync(c->err_d, 0, sizeof(int), c->st);
+  cudaMemsetAsync(c->zeros, 0, 64 * sizeof(cplx), c->st);
   *out = c;
   return RBA_OK;
 }

@@ -51,6 +51,8 @@ void launch_trsm2(cudaStream_t st, const PanelTask* tasks, int ntasks, const Fro
                   const PoleBatch& pb);
 void launch_gemm3(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
                   const FrontsDev& F, const PoleBatch& pb, int variant);
+void launch_gemm5(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
+                  const FrontsDev& F, const PoleBatch& pb, const cplx* zeros);
 void launch_trsm3(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
                   const PoleBatch& pb, int variant);
 

@@ -748,4 +748,221 @@ void launch_trsm3(cudaStream_t st, const PanelTask* tasks, int ntasks, const Fro
 }
 
 
+// ---------------------------------------------------------------------------
+// v5 (trailing/Schur update only): the same 64x64 tile and 8 warps of 32x16 as
+// v3, but the operands move by bulk async copies (cp.async.bulk, one 1 KB
+// copy per k column of A and of B -- the panel is column-major, so a
+// column's 64 rows are contiguous) completing on a per-stage "full" mbarrier.
+// There is no CTA-wide barrier in the main loop: each warp waits only for
+// its stage's bytes, and the last warp to finish a stage (shared-memory
+// counter) refills it.  Smem layout [k][row] with a 66-complex column stride
+// keeps the LDS.128 fragment loads conflict-free.  Out-of-range k columns
+// are copied from a zero buffer (so they contribute exactly 0); rows and
+// columns past the tile edge only feed discarded outputs.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int G5K = 16;     // k per stage (complex)
+constexpr int G5LD = 66;    // column stride (complex)
+constexpr int G5W = 8;      // warps
+struct Stage5 {
+  cplx a[G5K * G5LD];
+  cplx b[G5K * G5LD];
+  cplx d[G5K];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  unsigned done = 0;
+  unsigned tries = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (++tries > (1u << 28)) __trap();   // a lost copy must not hang the device
+  } while (!done);
+}
+}  // namespace
+
+template <int NS>
+__global__ void __launch_bounds__(32 * G5W, 2) k_gemm5(const GemmTask* __restrict__ tasks, int ntasks,
+                                                     FrontsDev F, PoleBatch pb,
+                                                     const cplx* __restrict__ zeros) {
+  extern __shared__ __align__(128) unsigned char smraw5[];
+  Stage5* st = reinterpret_cast<Stage5*>(smraw5);
+  __shared__ __align__(8) unsigned long long full[NS];
+  __shared__ int cnt[NS];
+  const int slot = blockIdx.y;
+  const int ti = find_task(tasks, ntasks, blockIdx.x);
+  const GemmTask tk = tasks[ti];
+  int local = blockIdx.x - tk.tile_start;
+  int j = 0;
+  while (local >= tk.ntr - j) { local -= tk.ntr - j; ++j; }
+  const int i = j + local;
+  const int s = tk.s, t0 = tk.t0, t1 = tk.t1;
+  const int r0 = tk.c_lo + i * GT;
+  const int cc0 = tk.c_lo + j * GT;
+  const int cmax = min(cc0 + GT, tk.c_hi);
+  const int nf = F.nf[s], p = F.npiv[s];
+  const cplx* __restrict__ panel = pb.factor[slot] + F.panel_off[s];
+  cplx* pw = pb.factor[slot] + F.panel_off[s];
+  cplx* upd = pb.upd[slot] + (F.upd_off[s] >= 0 ? F.upd_off[s] : 0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nchunks = (t1 - t0 + G5K - 1) / G5K;
+  const unsigned na = (unsigned)min(GT, nf - r0) * 16u;     // valid A rows (bytes)
+  const unsigned nb = (unsigned)min(GT, nf - cc0) * 16u;    // valid B rows (bytes)
+
+  // one thread: arm stage ch % NS and copy chunk ch into it
+  auto issue = [&](int ch) {
+    Stage5& S = st[ch % NS];
+    const unsigned bar = smem_u32(&full[ch % NS]);
+    const int kt = t0 + ch * G5K;
+    unsigned bytes = 0;
+#pragma unroll 1
+    for (int kk = 0; kk < G5K; ++kk) bytes += (kt + kk < t1) ? na + nb + 16u : 2048u + 16u;
+    mbar_expect_tx(bar, bytes);
+#pragma unroll 1
+    for (int kk = 0; kk < G5K; ++kk) {
+      const int t = kt + kk;
+      if (t < t1) {
+        const cplx* col = panel + (int64_t)t * nf;
+        bulk_g2s(smem_u32(&S.a[kk * G5LD]), col + r0, na, bar);
+        bulk_g2s(smem_u32(&S.b[kk * G5LD]), col + cc0, nb, bar);
+        bulk_g2s(smem_u32(&S.d[kk]), col + t, 16u, bar);
+      } else {
+        bulk_g2s(smem_u32(&S.a[kk * G5LD]), zeros, 1024u, bar);
+        bulk_g2s(smem_u32(&S.b[kk * G5LD]), zeros, 1024u, bar);
+        bulk_g2s(smem_u32(&S.d[kk]), zeros, 16u, bar);
+      }
+    }
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      mbar_init(smem_u32(&full[q]), 1);
+      cnt[q] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int ch = 0; ch < min(NS, nchunks); ++ch) issue(ch);
+
+  double cre[4][2][2], cim[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      cre[a][b][0] = cre[a][b][1] = 0.0;
+      cim[a][b][0] = cim[a][b][1] = 0.0;
+    }
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int sidx = ch % NS;
+    mbar_wait(smem_u32(&full[sidx]), (unsigned)((ch / NS) & 1));
+    const Stage5& S = st[sidx];
+#pragma unroll
+    for (int k4 = 0; k4 < G5K; k4 += 4) {
+      double ar[4], ai[4], br[2], bi[2];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const cplx v = S.a[(k4 + t4) * G5LD + wm + a * 8 + g];
+        ar[a] = v.x;
+        ai[a] = v.y;
+      }
+      const cplx dk = S.d[k4 + t4];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const cplx v = cmul(S.b[(k4 + t4) * G5LD + wn + b * 8 + g], dk);
+        br[b] = v.x;
+        bi[b] = v.y;
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma(cre[a][b][0], cre[a][b][1], ar[a], br[b]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma(cim[a][b][0], cim[a][b][1], ar[a], bi[b]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma(cre[a][b][0], cre[a][b][1], -ai[a], bi[b]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) dmma(cim[a][b][0], cim[a][b][1], ai[a], br[b]);
+    }
+    // stage consumed by this warp; the last warp refills it
+    __syncwarp();
+    if (lane == 0 && ch + NS < nchunks) {
+      __threadfence_block();
+      const int old = atomicAdd(&cnt[sidx], 1);
+      if (old == G5W - 1) {
+        __threadfence_block();
+        cnt[sidx] = 0;
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(ch + NS);
+      }
+    }
+  }
+  // batched read-modify-write epilogue (as v3)
+#pragma unroll
+  for (int a0 = 0; a0 < 4; a0 += 2) {
+    cplx* dst[2][2][2];
+    cplx cv[2][2][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + wm + (a0 + a) * 8 + g;
+          const int c = cc0 + wn + b * 8 + t4 * 2 + h;
+          dst[a][b][h] = (r < nf && c < cmax && r >= c) ? faddr(pw, upd, p, nf, r, c) : nullptr;
+          cv[a][b][h] = dst[a][b][h] ? __ldcg(dst[a][b][h]) : cmk(0.0, 0.0);
+        }
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (dst[a][b][h])
+            *dst[a][b][h] = cmk(cv[a][b][h].x - cre[a0 + a][b][h], cv[a][b][h].y - cim[a0 + a][b][h]);
+  }
+}
+
+void launch_gemm5(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
+                  const FrontsDev& F, const PoleBatch& pb, const cplx* zeros) {
+  if (ntasks <= 0 || nctas <= 0) return;
+  constexpr int NS = 3;
+  const size_t smem = NS * sizeof(Stage5);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm5<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  dim3 grid(nctas, pb.count);
+  k_gemm5<NS><<<grid, 32 * G5W, smem, st>>>(tasks, ntasks, F, pb, zeros);
+}
+
 }  // namespace rba
