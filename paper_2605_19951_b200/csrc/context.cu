@@ -114,6 +114,7 @@ struct rba_ctx {
   std::vector<char> valid;
   int NRw = 1;
   std::vector<cplx*> upd;
+  std::vector<cplx*> dvec;
   int fbatch = 1;
   cplx* wa = nullptr;
   cplx* stage = nullptr;
@@ -141,6 +142,7 @@ struct rba_ctx {
   bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernels
   int gemm_v = 5;             // RBA_GEMM=v1|v2|v3|v4 select the earlier DMMA kernels
   int small_p = 2 * rba::PB;  // warp-per-front solves up to this npiv (RBA_SMALLP=64|128)
+  int gemm5_var = 0;          // v5 ring: 0 = 16 k x 3 stages, 1 (RBA_GEMM=v5b) = 8 k x 6
   int gemm_var = 1;           // v3 stage shape: 1 (default, RBA_GEMM=v4) = 16 k x 2 stages,
                               // 0 (RBA_GEMM=v3) = 8 k x 3 stages
   int64_t launches = 0;
@@ -500,7 +502,8 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
         else if (c->gemm_v == 3)
           rba::launch_gemm3(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->gemm_var);
         else if (c->gemm_v == 5)
-          rba::launch_gemm5(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros);
+          rba::launch_gemm5(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros,
+                            c->gemm5_var);
         else
           rba::launch_gemm2(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
         break;
@@ -563,8 +566,11 @@ int ensure_slots(rba_ctx* c) {
   }
   if (const char* e = getenv("RBA_FACTOR_BATCH")) c->fbatch = std::max(1, std::min(atoi(e), nl));
   c->upd.assign(c->fbatch, nullptr);
-  for (int b = 0; b < c->fbatch; ++b)
+  c->dvec.assign(c->fbatch, nullptr);
+  for (int b = 0; b < c->fbatch; ++b) {
     if ((rc = dalloc(c, c->pole_allocs, &c->upd[b], (size_t)S.upd_total, &c->mem_work))) return rc;
+    if ((rc = dalloc(c, c->pole_allocs, &c->dvec[b], (size_t)S.n, &c->mem_work))) return rc;
+  }
   if ((rc = dalloc(c, c->pole_allocs, &c->wa, (size_t)nl * std::max(c->S, 1) * std::max<int64_t>(c->Mr, 1), &c->mem_work))) return rc;
   std::vector<int32_t> pos(c->local.begin(), c->local.end());
   if ((rc = dalloc(c, c->pole_allocs, &c->pole_of_slot, nl, &c->mem_other))) return rc;
@@ -779,6 +785,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     if (std::string(e) == "v3") { c->gemm_v = 3; c->gemm_var = 0; }
     if (std::string(e) == "v4") { c->gemm_v = 3; c->gemm_var = 1; }
     if (std::string(e) == "v5") { c->gemm_v = 5; c->gemm_var = 1; }
+    if (std::string(e) == "v5b") { c->gemm_v = 5; c->gemm_var = 1; c->gemm5_var = 1; }
   }
   if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) == "fused";
   if (const char* e = getenv("RBA_SMALLP")) c->small_p = std::string(e) == "64" ? rba::PB : 2 * rba::PB;
@@ -1012,6 +1019,7 @@ int rba_factor(rba_ctx* c) {
       c->valid[l] = 0;
       pb.factor[i] = c->factor[l];
       pb.upd[i] = c->upd[i];
+      pb.dvec[i] = c->dvec[i];
       pb.xi[i] = c->poles_h[c->local[l]];
       CK(cudaMemsetAsync(c->factor[l], 0, S.panel_off[S.nfront] * sizeof(cplx), c->st));
     }
@@ -1051,6 +1059,7 @@ int rba_factor_values(rba_ctx* c, int32_t slot, const double* vals) {
   pb.count = 1;
   pb.factor[0] = c->factor[slot];
   pb.upd[0] = c->upd[0];
+  pb.dvec[0] = c->dvec[0];
   pb.xi[0] = rba::cmk(0.0, 0.0);
   c->valid[slot] = 0;
   if ((rc = run_plan(c, pb))) return rc;

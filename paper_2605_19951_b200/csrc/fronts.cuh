@@ -27,6 +27,7 @@ struct FrontsDev {
 struct PoleBatch {
   cplx* factor[32];     // per slot: factor storage base
   cplx* upd[32];        // per slot: update arena base
+  cplx* dvec[32];       // per slot: pivots d in global pivot order (contiguous copy of the diagonal)
   cplx xi[32];          // per slot: pole value
   int32_t count;
 };

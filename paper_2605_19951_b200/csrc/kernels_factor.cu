@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(256) k_diag(const PanelTask* __restrict__ task
     int i = idx % kb, j = idx / kb;
     panel[(int64_t)(k0 + j) * nf + k0 + i] = i >= j ? Dg[i * LDS + j] : Xs[j * LDS + i];
   }
+  if (tid < kb) pb.dvec[slot][F.first[s] + k0 + tid] = Dg[tid * LDS + tid];
 }
 
 // K4a (v2): the same diagonal-block LDL^T + inverse, blocked by 16 so that
@@ -321,6 +322,7 @@ __global__ void __launch_bounds__(256) k_diag2(const PanelTask* __restrict__ tas
     int i = idx % kb, j = idx / kb;
     panel[(int64_t)(k0 + j) * nf + k0 + i] = Dg[i * LDS + j];
   }
+  if (tid < kb) pb.dvec[slot][F.first[s] + k0 + tid] = Dg[tid * LDS + tid];
 }
 
 void launch_diag2(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,

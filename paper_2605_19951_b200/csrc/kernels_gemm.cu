@@ -761,9 +761,9 @@ void launch_trsm3(cudaStream_t st, const PanelTask* tasks, int ntasks, const Fro
 // columns past the tile edge only feed discarded outputs.
 // ---------------------------------------------------------------------------
 namespace {
-constexpr int G5K = 16;     // k per stage (complex)
 constexpr int G5LD = 66;    // column stride (complex)
 constexpr int G5W = 8;      // warps
+template <int G5K>          // k per stage (complex)
 struct Stage5 {
   cplx a[G5K * G5LD];
   cplx b[G5K * G5LD];
@@ -800,12 +800,13 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
 }
 }  // namespace
 
-template <int NS>
+template <int G5K, int NS>
 __global__ void __launch_bounds__(32 * G5W, 2) k_gemm5(const GemmTask* __restrict__ tasks, int ntasks,
                                                      FrontsDev F, PoleBatch pb,
                                                      const cplx* __restrict__ zeros) {
   extern __shared__ __align__(128) unsigned char smraw5[];
-  Stage5* st = reinterpret_cast<Stage5*>(smraw5);
+  using St = Stage5<G5K>;
+  St* st = reinterpret_cast<St*>(smraw5);
   __shared__ __align__(8) unsigned long long full[NS];
   __shared__ int cnt[NS];
   const int slot = blockIdx.y;
@@ -829,16 +830,18 @@ __global__ void __launch_bounds__(32 * G5W, 2) k_gemm5(const GemmTask* __restric
   const int nchunks = (t1 - t0 + G5K - 1) / G5K;
   const unsigned na = (unsigned)min(GT, nf - r0) * 16u;     // valid A rows (bytes)
   const unsigned nb = (unsigned)min(GT, nf - cc0) * 16u;    // valid B rows (bytes)
+  const cplx* __restrict__ dvec = pb.dvec[slot] + F.first[s];   // d of this front's pivots
 
   // one thread: arm stage ch % NS and copy chunk ch into it
   auto issue = [&](int ch) {
-    Stage5& S = st[ch % NS];
+    St& S = st[ch % NS];
     const unsigned bar = smem_u32(&full[ch % NS]);
     const int kt = t0 + ch * G5K;
-    unsigned bytes = 0;
-#pragma unroll 1
-    for (int kk = 0; kk < G5K; ++kk) bytes += (kt + kk < t1) ? na + nb + 16u : 2048u + 16u;
-    mbar_expect_tx(bar, bytes);
+    const int nval = max(0, min(G5K, t1 - kt));
+    mbar_expect_tx(bar, (unsigned)nval * (na + nb) + (unsigned)(G5K - nval) * 2048u +
+                            (unsigned)G5K * 16u);
+    if (nval > 0) bulk_g2s(smem_u32(&S.d[0]), dvec + kt, (unsigned)nval * 16u, bar);
+    if (nval < G5K) bulk_g2s(smem_u32(&S.d[nval]), zeros, (unsigned)(G5K - nval) * 16u, bar);
 #pragma unroll 1
     for (int kk = 0; kk < G5K; ++kk) {
       const int t = kt + kk;
@@ -846,11 +849,9 @@ __global__ void __launch_bounds__(32 * G5W, 2) k_gemm5(const GemmTask* __restric
         const cplx* col = panel + (int64_t)t * nf;
         bulk_g2s(smem_u32(&S.a[kk * G5LD]), col + r0, na, bar);
         bulk_g2s(smem_u32(&S.b[kk * G5LD]), col + cc0, nb, bar);
-        bulk_g2s(smem_u32(&S.d[kk]), col + t, 16u, bar);
       } else {
         bulk_g2s(smem_u32(&S.a[kk * G5LD]), zeros, 1024u, bar);
         bulk_g2s(smem_u32(&S.b[kk * G5LD]), zeros, 1024u, bar);
-        bulk_g2s(smem_u32(&S.d[kk]), zeros, 16u, bar);
       }
     }
   };
@@ -877,7 +878,7 @@ __global__ void __launch_bounds__(32 * G5W, 2) k_gemm5(const GemmTask* __restric
   for (int ch = 0; ch < nchunks; ++ch) {
     const int sidx = ch % NS;
     mbar_wait(smem_u32(&full[sidx]), (unsigned)((ch / NS) & 1));
-    const Stage5& S = st[sidx];
+    const St& S = st[sidx];
 #pragma unroll
     for (int k4 = 0; k4 < G5K; k4 += 4) {
       double ar[4], ai[4], br[2], bi[2];
@@ -951,18 +952,25 @@ __global__ void __launch_bounds__(32 * G5W, 2) k_gemm5(const GemmTask* __restric
   }
 }
 
-void launch_gemm5(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
-                  const FrontsDev& F, const PoleBatch& pb, const cplx* zeros) {
-  if (ntasks <= 0 || nctas <= 0) return;
-  constexpr int NS = 3;
-  const size_t smem = NS * sizeof(Stage5);
+template <int G5K, int NS>
+static void launch_g5(cudaStream_t st, dim3 grid, const GemmTask* tasks, int ntasks,
+                      const FrontsDev& F, const PoleBatch& pb, const cplx* zeros) {
+  const size_t smem = NS * sizeof(Stage5<G5K>);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm5<NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_gemm5<G5K, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
+  k_gemm5<G5K, NS><<<grid, 32 * G5W, smem, st>>>(tasks, ntasks, F, pb, zeros);
+}
+
+// variant 0: 16 k x 3 stages; 1: 8 k x 6 stages
+void launch_gemm5(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
+                  const FrontsDev& F, const PoleBatch& pb, const cplx* zeros, int variant) {
+  if (ntasks <= 0 || nctas <= 0) return;
   dim3 grid(nctas, pb.count);
-  k_gemm5<NS><<<grid, 32 * G5W, smem, st>>>(tasks, ntasks, F, pb, zeros);
+  if (variant == 1) launch_g5<8, 6>(st, grid, tasks, ntasks, F, pb, zeros);
+  else launch_g5<16, 3>(st, grid, tasks, ntasks, F, pb, zeros);
 }
 
 }  // namespace rba

@@ -51,7 +51,7 @@ def test_dmma_gemm_matches_dfma_reference(gpu, monkeypatch):
     approx = rb.config_approximant("C1")
     model = prob.true_model()
     out = []
-    for mode in ("dfma", "v1", "v2", "v3", "v4", "v5"):
+    for mode in ("dfma", "v1", "v2", "v3", "v4", "v5", "v5b"):
         monkeypatch.setenv("RBA_GEMM", mode)
         cache = rb.ShiftedFactorCache()
         rb.factorize_all_poles(prob, model, approx, cache)
