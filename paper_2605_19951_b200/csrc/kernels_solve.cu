@@ -10,6 +10,7 @@
 // tasks with smaller tickets, which are already resident, so no deadlock.
 // Child contributions enter through a deterministic gather (ucon lists), so
 // results are bitwise reproducible.
+#include <cstdlib>
 #include "fronts.cuh"
 #include "kernels.h"
 
@@ -225,10 +226,10 @@ __global__ void __launch_bounds__(256, 2) k_fwd(const SolveTask* __restrict__ ta
 
 // Backward task (front s, pivot column block cb), blocks processed from the
 // last one down:  x_cb = X^T (y_cb / d_cb - sum_{rho beyond block} L[rho, cb]^T x_rho).
-// 16 warps x 4 columns, lanes stride the rows; no block barrier in the main
+// NW warps x 64/NW columns, lanes stride the rows; no block barrier in the main
 // loop (the pivot-block waits are per warp).
-template <int NR>
-__global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks, int nslots,
+template <int NR, int NW>
+__global__ void __launch_bounds__(32 * NW) k_bwd(const SolveTask* __restrict__ tasks, int nslots,
                                              FrontsDev F, SolveBatchDev sb, int* ticket,
                                              int /*unused*/, SweepDeps dep) {
   __shared__ int s_t;
@@ -259,10 +260,11 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
                  "l"(panel + (int64_t)(c0 + i) * nf + c0 + c) : "memory");
   }
   asm volatile("cp.async.commit_group;\n" ::: "memory");
-  // columns per warp per pass: 4 (NR <= 4) or 2 in two passes (NR = 8), so
-  // the accumulators stay in registers
-  constexpr int CPW = NR <= 4 ? 4 : 2;
-  constexpr int NPASS = 4 / CPW;
+  // columns per warp per pass: 64 / NW, halved (in two passes) when the
+  // NR accumulators would not fit in registers
+  constexpr int CW = PB / NW;
+  constexpr int CPW = (NR * CW > 16) ? CW / 2 : CW;
+  constexpr int NPASS = CW / CPW;
   if (dep.fused && nf > p) {
     // border rows are final once the parent front is complete (its own tasks
     // waited for every owner of its border)
@@ -279,7 +281,7 @@ __global__ void __launch_bounds__(512) k_bwd(const SolveTask* __restrict__ tasks
   for (int k = 0; k < CPW; ++k)
 #pragma unroll
     for (int r = 0; r < NR; ++r) acc[k][r] = cmk(0.0, 0.0);
-  const int cw = (pass * 16 + warp) * CPW;
+  const int cw = (pass * NW + warp) * CPW;
   const int nk = max(0, min(CPW, ncol - cw));
   const cplx* colp = panel + (int64_t)(c0 + cw) * nf;
   // border rows: pivots of ancestors, final before this launch (L1 is
@@ -660,17 +662,29 @@ static void fwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslo
   else
     k_fwd<NR, false><<<ntasks * nslots, 256, smem0, st>>>(tasks, nslots, F, sb, ticket, epoch, dep);
 }
-template <int NR>
-static void bwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
+template <int NR, int NW>
+static void bwd_nw(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
                    const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch,
                    const SweepDeps& dep) {
   const size_t smem = (2 * PB * NR + PB * (PB + 1)) * sizeof(cplx);  // + staged X
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_bwd<NR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_bwd<NR, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_bwd<NR><<<ntasks * nslots, 512, smem, st>>>(tasks, nslots, F, sb, ticket, epoch, dep);
+  k_bwd<NR, NW><<<ntasks * nslots, 32 * NW, smem, st>>>(tasks, nslots, F, sb, ticket, epoch, dep);
+}
+static int g_bwd_nw = -1;
+template <int NR>
+static void bwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
+                   const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch,
+                   const SweepDeps& dep) {
+  if (g_bwd_nw < 0) {
+    const char* e = getenv("RBA_BWD_NW");
+    g_bwd_nw = (e && atoi(e) == 32) ? 32 : 16;
+  }
+  if (g_bwd_nw == 16) bwd_nw<NR, 16>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep);
+  else bwd_nw<NR, 32>(st, tasks, ntasks, nslots, F, sb, ticket, epoch, dep);
 }
 
 void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* tasks,
