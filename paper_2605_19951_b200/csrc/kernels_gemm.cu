@@ -770,34 +770,6 @@ struct Stage5 {
   cplx d[G5K];
 };
 
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bar), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(dst),
-      "l"(src), "r"(bytes), "r"(bar)
-      : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
-  unsigned done = 0;
-  unsigned tries = 0;
-  do {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    if (++tries > (1u << 28)) __trap();   // a lost copy must not hang the device
-  } while (!done);
-}
 }  // namespace
 
 template <int G5K, int NS>
@@ -832,27 +804,26 @@ __global__ void __launch_bounds__(32 * G5W, 2) k_gemm5(const GemmTask* __restric
   const unsigned nb = (unsigned)min(GT, nf - cc0) * 16u;    // valid B rows (bytes)
   const cplx* __restrict__ dvec = pb.dvec[slot] + F.first[s];   // d of this front's pivots
 
-  // one thread: arm stage ch % NS and copy chunk ch into it
+  // one warp: lane 0 arms stage ch % NS, the lanes split the copies of chunk ch
   auto issue = [&](int ch) {
     St& S = st[ch % NS];
     const unsigned bar = smem_u32(&full[ch % NS]);
     const int kt = t0 + ch * G5K;
     const int nval = max(0, min(G5K, t1 - kt));
-    mbar_expect_tx(bar, (unsigned)nval * (na + nb) + (unsigned)(G5K - nval) * 2048u +
-                            (unsigned)G5K * 16u);
-    if (nval > 0) bulk_g2s(smem_u32(&S.d[0]), dvec + kt, (unsigned)nval * 16u, bar);
-    if (nval < G5K) bulk_g2s(smem_u32(&S.d[nval]), zeros, (unsigned)(G5K - nval) * 16u, bar);
-#pragma unroll 1
-    for (int kk = 0; kk < G5K; ++kk) {
+    if (lane == 0) {
+      mbar_expect_tx(bar, (unsigned)nval * (na + nb) + (unsigned)(G5K - nval) * 2048u +
+                              (unsigned)G5K * 16u);
+      if (nval > 0) bulk_g2s(smem_u32(&S.d[0]), dvec + kt, (unsigned)nval * 16u, bar);
+      if (nval < G5K) bulk_g2s(smem_u32(&S.d[nval]), zeros, (unsigned)(G5K - nval) * 16u, bar);
+    }
+    for (int q = lane; q < 2 * G5K; q += 32) {
+      const int kk = q >> 1;
       const int t = kt + kk;
-      if (t < t1) {
-        const cplx* col = panel + (int64_t)t * nf;
-        bulk_g2s(smem_u32(&S.a[kk * G5LD]), col + r0, na, bar);
-        bulk_g2s(smem_u32(&S.b[kk * G5LD]), col + cc0, nb, bar);
-      } else {
-        bulk_g2s(smem_u32(&S.a[kk * G5LD]), zeros, 1024u, bar);
-        bulk_g2s(smem_u32(&S.b[kk * G5LD]), zeros, 1024u, bar);
-      }
+      cplx* dst = (q & 1) ? &S.b[kk * G5LD] : &S.a[kk * G5LD];
+      if (t < t1)
+        bulk_g2s(smem_u32(dst), panel + (int64_t)t * nf + ((q & 1) ? cc0 : r0), (q & 1) ? nb : na, bar);
+      else
+        bulk_g2s(smem_u32(dst), zeros, 1024u, bar);
     }
   };
   if (tid == 0) {
@@ -864,7 +835,7 @@ __global__ void __launch_bounds__(32 * G5W, 2) k_gemm5(const GemmTask* __restric
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (tid == 0)
+  if (warp == 0)
     for (int ch = 0; ch < min(NS, nchunks); ++ch) issue(ch);
 
   double cre[4][2][2], cim[4][2][2];
@@ -914,12 +885,17 @@ __global__ void __launch_bounds__(32 * G5W, 2) k_gemm5(const GemmTask* __restric
     }
     // stage consumed by this warp; the last warp refills it
     __syncwarp();
-    if (lane == 0 && ch + NS < nchunks) {
-      __threadfence_block();
-      const int old = atomicAdd(&cnt[sidx], 1);
-      if (old == G5W - 1) {
+    if (ch + NS < nchunks) {
+      int last = 0;
+      if (lane == 0) {
         __threadfence_block();
-        cnt[sidx] = 0;
+        last = atomicAdd(&cnt[sidx], 1) == G5W - 1;
+        if (last) {
+          __threadfence_block();
+          cnt[sidx] = 0;
+        }
+      }
+      if (__shfl_sync(0xffffffffu, last, 0)) {
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         issue(ch + NS);
       }
