@@ -103,6 +103,15 @@ class Clocks:
                 "samples": len(rows)}
 
 
+def measured_traffic():
+    """Per-unit DRAM traffic of the factorisation / solve kernel classes from the
+    committed ncu capture (profiles/dram_r01.json, tools/ncu_summary.py)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "dram_r01.json")))
+    except OSError:
+        return {}
+
+
 def measured_peaks():
     peaks = {}
     try:
@@ -220,6 +229,7 @@ def run_ours(args, world, rank):
 
     # ---- roofline of the dominant kernel class in the timed region ---------
     peaks = measured_peaks()
+    traffic = measured_traffic()
     fact_ms = sum(cls[k] for k in ("scatter", "extend_add", "diag", "trsm", "gemm"))
     solve_ms = cls["solve_fwd"] + cls["solve_bwd"]
     n_local_fact = n_fact if world == 1 else n_fact  # counters count local poles
@@ -234,13 +244,17 @@ def run_ours(args, world, rank):
                 "bound": "tensor", "achieved": achieved, "peak": peaks["fp64_tflops"],
                 "unit": "TFLOP/s", "frac": achieved / peaks["fp64_tflops"],
                 "peak_source": "measured FP64 DMMA microbenchmark (profiles/fp64_peak_r01.json)",
-                "traffic": None, "per_unit": "8*sum_s(p^3/6 + r p^2/2 + r^2 p/2) flops/pole",
+                "traffic": traffic.get("factor_bytes_per_pole"),
+                "traffic_unit": "DRAM bytes per pole factorisation (ncu, profiles/dram_r01.json)",
+                "per_unit": "8*sum_s(p^3/6 + r p^2/2 + r^2 p/2) flops/pole",
                 "units_per_step": n_local_fact / args.steps}
     else:
         achieved = solve_bytes_one * n_local_solve / (solve_ms * 1e-3) / 1e9
         roof = {"kernel": "multifrontal triangular solves (K6/K7)", "bound": "hbm",
                 "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "frac": achieved / peaks["hbm_gbs"],
+                "traffic": traffic.get("solve_bytes_per_pole_solve"),
+                "traffic_unit": "DRAM bytes per pole-solve (ncu, profiles/dram_r01.json)",
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                 "per_unit": "2*nnz(L)*16 + N*16 + 4*N*nrhs*16 bytes/solve",
                 "units_per_step": n_local_solve / args.steps}
