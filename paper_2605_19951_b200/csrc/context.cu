@@ -45,6 +45,7 @@ struct Step {
   int64_t off;
   int n;
   int ntiles;
+  int schur;   // ST_GEMM: 1 = Schur-complement update (K = npiv), 0 = panel update
 };
 
 int nr_pad(int s) { return s <= 1 ? 1 : s <= 2 ? 2 : s <= 4 ? 4 : 8; }
@@ -140,9 +141,13 @@ struct rba_ctx {
   // by rba_set_timing) and the launch count of this context's kernels
   double cls_ms[128] = {0};   // 0-15 kernel classes; 16+L fwd, 48+L bwd, 80+L gemm per level
   bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernels
-  int gemm_v = 5;             // RBA_GEMM=v1|v2|v3|v4 select the earlier DMMA kernels
+  int gemm_v = 6;             // default 3M DMMA kernel (k_gemm6); RBA_GEMM=v1..v5 select
+                              // the earlier kernels for A/B tests
   int small_p = 2 * rba::PB;  // warp-per-front solves up to this npiv (RBA_SMALLP=64|128)
-  int gemm5_var = 0;          // v5 ring: 0 = 16 k x 3 stages, 1 (RBA_GEMM=v5b) = 8 k x 6
+  int gemm5_var = 2;          // v5/v6 stage shape (see launch_gemm5 / launch_gemm6); default
+                              // v6c = 64x32 half tiles, 8 k x 5 stages, 3 CTAs/SM
+  int panel_v = 0;            // RBA_GEMM_PANEL: kernel for the panel updates (0 = as RBA_GEMM)
+  int panel_var = 0;
   int gemm_var = 1;           // v3 stage shape: 1 (default, RBA_GEMM=v4) = 16 k x 2 stages,
                               // 0 (RBA_GEMM=v3) = 8 k x 3 stages
   int64_t launches = 0;
@@ -336,7 +341,7 @@ int build_plans(rba_ctx* c) {
       else
         tiles += ntr * (ntr + 1) / 2;
     }
-    if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles});
+    if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles, 1});
   }
   int rc;
   if ((rc = upload(c, c->allocs, &c->ea_tasks, ea.data(), ea.size()))) return rc;
@@ -487,7 +492,7 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
           rba::launch_trsm(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
         else if (c->gemm_v == 1)
           rba::launch_trsm_dmma(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
-        else if (c->gemm_v == 3 || c->gemm_v == 5)
+        else if (c->gemm_v == 3 || c->gemm_v >= 5)
           rba::launch_trsm3(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->gemm_var);
         else
           rba::launch_trsm2(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
@@ -495,6 +500,16 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
       }
       case ST_GEMM: {
         Timed t(c, KC_GEMM);
+        if (!s.schur && c->panel_v > 0) {
+          // panel (look-ahead / aggregated) updates: short K, own kernel choice
+          if (c->panel_v == 5)
+            rba::launch_gemm5(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros,
+                              c->panel_var);
+          else
+            rba::launch_gemm6(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros,
+                              c->panel_var);
+          break;
+        }
         if (c->gemm_dfma)
           rba::launch_gemm_update(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
         else if (c->gemm_v == 1)
@@ -503,6 +518,9 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
           rba::launch_gemm3(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->gemm_var);
         else if (c->gemm_v == 5)
           rba::launch_gemm5(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros,
+                            c->gemm5_var);
+        else if (c->gemm_v == 6)
+          rba::launch_gemm6(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros,
                             c->gemm5_var);
         else
           rba::launch_gemm2(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
@@ -784,8 +802,21 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     if (std::string(e) == "v2") c->gemm_v = 2;
     if (std::string(e) == "v3") { c->gemm_v = 3; c->gemm_var = 0; }
     if (std::string(e) == "v4") { c->gemm_v = 3; c->gemm_var = 1; }
-    if (std::string(e) == "v5") { c->gemm_v = 5; c->gemm_var = 1; }
+    if (std::string(e) == "v5") { c->gemm_v = 5; c->gemm_var = 1; c->gemm5_var = 0; }
     if (std::string(e) == "v5b") { c->gemm_v = 5; c->gemm_var = 1; c->gemm5_var = 1; }
+    if (std::string(e) == "v6") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 0; }
+    if (std::string(e) == "v6b") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 1; }
+    if (std::string(e) == "v6c") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 2; }
+    if (std::string(e) == "v6d") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 3; }
+    if (std::string(e) == "v7") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 4; }
+    if (std::string(e) == "v7b") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 5; }
+  }
+  if (const char* e = getenv("RBA_GEMM_PANEL")) {
+    const std::string v(e);
+    const char* names[] = {"v6", "v6b", "v6c", "v6d", "v7", "v7b"};
+    for (int q = 0; q < 6; ++q)
+      if (v == names[q]) { c->panel_v = 6; c->panel_var = q; }
+    if (v == "v5") { c->panel_v = 5; c->panel_var = 0; }
   }
   if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) == "fused";
   if (const char* e = getenv("RBA_SMALLP")) c->small_p = std::string(e) == "64" ? rba::PB : 2 * rba::PB;

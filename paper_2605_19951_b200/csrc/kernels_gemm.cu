@@ -949,4 +949,231 @@ void launch_gemm5(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
   else launch_g5<16, 3>(st, grid, tasks, ntasks, F, pb, zeros);
 }
 
+
+// ---------------------------------------------------------------------------
+// v6 (trailing/Schur update only): three real DMMA products per complex
+// multiply-add instead of four (Gauss / "3M"):
+//     P = sum Are Bre,  Q = sum Aim Bim,  T = sum (Are + Aim)(Bre + Bim)
+//     Cre -= P - Q,     Cim -= T - P - Q
+// 25 % fewer tensor-core instructions for the same result; the real part is
+// bit-for-bit the 4M sum, the imaginary part differs by rounding only
+// (normwise backward stable; checked against the 4M kernels and the
+// reference goldens in tests/test_gpu_factor_structure.py and
+// tests/test_gpu_parity.py).  Three accumulator sets cost 96 registers per
+// 32x16 warp tile, so the CTA is 4 warps on a 64x32 tile (two CTAs per 64x64
+// task tile, blockIdx.x = 2*tile + half) with up to 255 registers, 2 CTAs/SM.
+// Operand movement is v5's: bulk async copies (one per k column of A and of
+// B) into an mbarrier ring, last warp through a stage refills it.
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int G6LA = 66;    // A column stride (complex): 64 rows + pad
+template <int G6K, int NCOL>
+struct Stage6 {
+  cplx a[G6K * G6LA];
+  cplx b[G6K * (NCOL + 2)];  // B column stride: NCOL cols + pad
+  cplx d[G6K];
+};
+}  // namespace
+
+// NCOL = 32: 4 warps on a 64x32 half tile (2-3 CTAs/SM); NCOL = 64: 8 warps
+// on the whole 64x64 tile, up to 255 registers, one CTA/SM.
+template <int G6K, int NS, int NCOL>
+__global__ void __launch_bounds__(NCOL * 4, NCOL == 32 ? 2 : 1) k_gemm6(
+    const GemmTask* __restrict__ tasks, int ntasks, FrontsDev F, PoleBatch pb,
+    const cplx* __restrict__ zeros) {
+  constexpr int G6W = NCOL / 8;
+  constexpr int G6LB = NCOL + 2;
+  constexpr int SPLIT = NCOL == 32 ? 2 : 1;
+  extern __shared__ __align__(128) unsigned char smraw6[];
+  using St = Stage6<G6K, NCOL>;
+  St* st = reinterpret_cast<St*>(smraw6);
+  __shared__ __align__(8) unsigned long long full[NS];
+  __shared__ int cnt[NS];
+  const int slot = blockIdx.y;
+  const int tile = blockIdx.x / SPLIT, half = blockIdx.x % SPLIT;
+  const int ti = find_task(tasks, ntasks, tile);
+  const GemmTask tk = tasks[ti];
+  int local = tile - tk.tile_start;
+  int j = 0;
+  while (local >= tk.ntr - j) { local -= tk.ntr - j; ++j; }
+  const int i = j + local;
+  const int s = tk.s, t0 = tk.t0, t1 = tk.t1;
+  const int r0 = tk.c_lo + i * GT;
+  const int cc0 = tk.c_lo + j * GT + half * NCOL;
+  const int cmax = min(cc0 + NCOL, tk.c_hi);
+  if (cc0 >= cmax) return;                       // right half beyond the column range
+  const int nf = F.nf[s], p = F.npiv[s];
+  if (cc0 >= nf) return;
+  const cplx* __restrict__ panel = pb.factor[slot] + F.panel_off[s];
+  cplx* pw = pb.factor[slot] + F.panel_off[s];
+  cplx* upd = pb.upd[slot] + (F.upd_off[s] >= 0 ? F.upd_off[s] : 0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  const int g = lane >> 2, t4 = lane & 3;
+  // a warp whose 32x16 block lies strictly above the diagonal only keeps the
+  // stage protocol going
+  const bool active = r0 + wm + 31 >= cc0 + wn && r0 + wm < nf;
+  const int nchunks = (t1 - t0 + G6K - 1) / G6K;
+  const unsigned na = (unsigned)min(GT, nf - r0) * 16u;
+  const unsigned nb = (unsigned)min(NCOL, nf - cc0) * 16u;
+  const cplx* __restrict__ dvec = pb.dvec[slot] + F.first[s];
+
+  auto issue = [&](int ch) {
+    St& S = st[ch % NS];
+    const unsigned bar = smem_u32(&full[ch % NS]);
+    const int kt = t0 + ch * G6K;
+    const int nval = max(0, min(G6K, t1 - kt));
+    if (lane == 0) {
+      mbar_expect_tx(bar, (unsigned)nval * (na + nb) + (unsigned)(G6K - nval) * (1024u + NCOL * 16u) +
+                              (unsigned)G6K * 16u);
+      if (nval > 0) bulk_g2s(smem_u32(&S.d[0]), dvec + kt, (unsigned)nval * 16u, bar);
+      if (nval < G6K) bulk_g2s(smem_u32(&S.d[nval]), zeros, (unsigned)(G6K - nval) * 16u, bar);
+    }
+    for (int q = lane; q < 2 * G6K; q += 32) {
+      const int kk = q >> 1;
+      const int t = kt + kk;
+      if (q & 1) {
+        cplx* dst = &S.b[kk * G6LB];
+        if (t < t1) bulk_g2s(smem_u32(dst), panel + (int64_t)t * nf + cc0, nb, bar);
+        else bulk_g2s(smem_u32(dst), zeros, NCOL * 16u, bar);
+      } else {
+        cplx* dst = &S.a[kk * G6LA];
+        if (t < t1) bulk_g2s(smem_u32(dst), panel + (int64_t)t * nf + r0, na, bar);
+        else bulk_g2s(smem_u32(dst), zeros, 1024u, bar);
+      }
+    }
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int q = 0; q < NS; ++q) {
+      mbar_init(smem_u32(&full[q]), 1);
+      cnt[q] = 0;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0)
+    for (int ch = 0; ch < min(NS, nchunks); ++ch) issue(ch);
+
+  double cp[4][2][2], cq[4][2][2], ct[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) cp[a][b][h] = cq[a][b][h] = ct[a][b][h] = 0.0;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int sidx = ch % NS;
+    mbar_wait(smem_u32(&full[sidx]), (unsigned)((ch / NS) & 1));
+    const St& S = st[sidx];
+    if (active) {
+#pragma unroll
+      for (int k4 = 0; k4 < G6K; k4 += 4) {
+        double ar[4], ai[4], br[2], bi[2];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const cplx v = S.a[(k4 + t4) * G6LA + wm + a * 8 + g];
+          ar[a] = v.x;
+          ai[a] = v.y;
+        }
+        const cplx dk = S.d[k4 + t4];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const cplx v = cmul(S.b[(k4 + t4) * G6LB + wn + b * 8 + g], dk);
+          br[b] = v.x;
+          bi[b] = v.y;
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) dmma(cp[a][b][0], cp[a][b][1], ar[a], br[b]);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) dmma(cq[a][b][0], cq[a][b][1], ai[a], bi[b]);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) ar[a] += ai[a];
+#pragma unroll
+        for (int b = 0; b < 2; ++b) br[b] += bi[b];
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) dmma(ct[a][b][0], ct[a][b][1], ar[a], br[b]);
+      }
+    }
+    __syncwarp();
+    if (ch + NS < nchunks) {
+      int last = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        last = atomicAdd(&cnt[sidx], 1) == G6W - 1;
+        if (last) {
+          __threadfence_block();
+          cnt[sidx] = 0;
+        }
+      }
+      if (__shfl_sync(0xffffffffu, last, 0)) {
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        issue(ch + NS);
+      }
+    }
+  }
+  if (!active) return;
+#pragma unroll
+  for (int a0 = 0; a0 < 4; a0 += 2) {
+    cplx* dst[2][2][2];
+    cplx cv[2][2][2];
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = r0 + wm + (a0 + a) * 8 + g;
+          const int c = cc0 + wn + b * 8 + t4 * 2 + h;
+          dst[a][b][h] = (r < nf && c < cmax && r >= c) ? faddr(pw, upd, p, nf, r, c) : nullptr;
+          cv[a][b][h] = dst[a][b][h] ? __ldcg(dst[a][b][h]) : cmk(0.0, 0.0);
+        }
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+          if (dst[a][b][h]) {
+            const double P = cp[a0 + a][b][h], Q = cq[a0 + a][b][h], T = ct[a0 + a][b][h];
+            *dst[a][b][h] = cmk(cv[a][b][h].x - (P - Q), cv[a][b][h].y - (T - P - Q));
+          }
+  }
+}
+
+template <int G6K, int NS, int NCOL>
+static void launch_g6(cudaStream_t st, dim3 grid, const GemmTask* tasks, int ntasks,
+                      const FrontsDev& F, const PoleBatch& pb, const cplx* zeros) {
+  const size_t smem = NS * sizeof(Stage6<G6K, NCOL>);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm6<G6K, NS, NCOL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = true;
+  }
+  k_gemm6<G6K, NS, NCOL><<<grid, NCOL * 4, smem, st>>>(tasks, ntasks, F, pb, zeros);
+}
+
+// variant 0: 16 k x 4 stages (2 CTAs/SM); 1: 8 k x 8 stages (2 CTAs/SM);
+// 2: 8 k x 5 stages (65 KB, 3 CTAs/SM); 3: 12 k x 3 stages (3 CTAs/SM);
+// 4: whole 64x64 tile, 8 warps, 16 k x 6 stages (1 CTA/SM); 5: 64x64, 16 k x 4
+// (1 CTA/SM)
+void launch_gemm6(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
+                  const FrontsDev& F, const PoleBatch& pb, const cplx* zeros, int variant) {
+  if (ntasks <= 0 || nctas <= 0) return;
+  dim3 grid(2 * nctas, pb.count), grid1(nctas, pb.count);
+  if (variant == 1) launch_g6<8, 8, 32>(st, grid, tasks, ntasks, F, pb, zeros);
+  else if (variant == 2) launch_g6<8, 5, 32>(st, grid, tasks, ntasks, F, pb, zeros);
+  else if (variant == 3) launch_g6<12, 3, 32>(st, grid, tasks, ntasks, F, pb, zeros);
+  else if (variant == 4) launch_g6<16, 6, 64>(st, grid1, tasks, ntasks, F, pb, zeros);
+  else if (variant == 5) launch_g6<16, 4, 64>(st, grid1, tasks, ntasks, F, pb, zeros);
+  else launch_g6<16, 4, 32>(st, grid, tasks, ntasks, F, pb, zeros);
+}
+
 }  // namespace rba
