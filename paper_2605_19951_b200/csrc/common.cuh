@@ -82,6 +82,13 @@ __device__ __forceinline__ void bulk_g2s(unsigned dst, const void* src, unsigned
       "l"(src), "r"(bytes), "r"(bar)
       : "memory");
 }
+// 2-D tensor copy (TMA) global -> shared, completing on an mbarrier
+__device__ __forceinline__ void tma_2d(unsigned dst, const void* tmap, int x, int y, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
+      "l"(tmap), "r"(x), "r"(y), "r"(bar)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
   unsigned done = 0;
   unsigned tries = 0;

@@ -9,6 +9,9 @@
 #include <string>
 #include <vector>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "../../include/rba_b200.h"
 #include "kernels.h"
 #include "mesh_prep.h"
@@ -110,6 +113,7 @@ struct rba_ctx {
   std::vector<void*> pole_allocs;
   // per local slot
   std::vector<cplx*> factor, g, x, uvec;
+  std::vector<rba::TMap*> tmaps;  // per slot: [nfront][2] tensor maps of the factor panels
   std::vector<int*> flf, flb, dnf, dnb;
   std::vector<int> slot_epoch;    // solves issued per local slot (flags / counters)
   std::vector<char> valid;
@@ -144,8 +148,9 @@ struct rba_ctx {
   int gemm_v = 6;             // default 3M DMMA kernel (k_gemm6); RBA_GEMM=v1..v5 select
                               // the earlier kernels for A/B tests
   int small_p = 2 * rba::PB;  // warp-per-front solves up to this npiv (RBA_SMALLP=64|128)
-  int gemm5_var = 2;          // v5/v6 stage shape (see launch_gemm5 / launch_gemm6); default
-                              // v6c = 64x32 half tiles, 8 k x 5 stages, 3 CTAs/SM
+  int gemm5_var = 6;          // v5/v6 stage shape (see launch_gemm5 / launch_gemm6); default
+                              // v8 = 64x32 half tiles, 8 k x 5 stages, 3 CTAs/SM, operands
+                              // by TMA tensor copies
   int panel_v = 0;            // RBA_GEMM_PANEL: kernel for the panel updates (0 = as RBA_GEMM)
   int panel_var = 0;
   int gemm_var = 1;           // v3 stage shape: 1 (default, RBA_GEMM=v4) = 16 k x 2 stages,
@@ -545,6 +550,51 @@ int check_err(rba_ctx* c, int pole) {
   return RBA_OK;
 }
 
+// TMA tensor maps of every front panel of one factor buffer (GEMM v6 with
+// RBA_GEMM=v8 / default): the panel is a column-major nf x npiv complex
+// matrix = a 2-D FLOAT64 tensor {2*nf, npiv} with row pitch nf*16 bytes.
+// Boxes: 66 complex rows (A operand) and 34 (B operand) by G8K columns, so a
+// box lands in shared memory with the padded strides the kernel reads
+// conflict-free.  Out-of-range rows / columns are zero-filled.
+int make_tmaps(rba_ctx* c, const cplx* base, rba::TMap** out) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(RBA_ERR_CUDA, "cuTensorMapEncodeTiled not available");
+    encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const rba::Symbolic& S = c->sym;
+  std::vector<rba::TMap> h((size_t)2 * S.nfront);
+  std::memset(h.data(), 0, h.size() * sizeof(rba::TMap));
+  for (int s = 0; s < S.nfront; ++s) {
+    const int nf = S.nf[s], p = S.npiv[s];
+    if (nf <= p || p == 0) {
+      // no trailing/Schur GEMM can touch a front without a border unless it
+      // has several pivot blocks; encode those too (panel updates)
+      if (p <= rba::PB) continue;
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)2 * nf, (cuuint64_t)p};
+    const cuuint64_t strides[1] = {(cuuint64_t)nf * sizeof(cplx)};
+    const cuuint32_t estr[2] = {1, 1};
+    for (int w = 0; w < 2; ++w) {
+      const cuuint32_t box[2] = {(cuuint32_t)(w == 0 ? 132 : 68), (cuuint32_t)rba::G8K};
+      CUresult r = encode(reinterpret_cast<CUtensorMap*>(&h[2 * s + w]), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
+                          (void*)(base + S.panel_off[s]), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS)
+        return fail(RBA_ERR_CUDA, "cuTensorMapEncodeTiled failed for front " + std::to_string(s) +
+                                      " (code " + std::to_string((int)r) + ")");
+    }
+  }
+  int rc;
+  if ((rc = upload(c, c->pole_allocs, out, h.data(), h.size()))) return rc;
+  return RBA_OK;
+}
+
 int ensure_slots(rba_ctx* c) {
   if (!c->factor.empty()) return RBA_OK;
   const int nl = (int)c->local.size();
@@ -552,6 +602,7 @@ int ensure_slots(rba_ctx* c) {
   const rba::Symbolic& S = c->sym;
   int rc;
   c->factor.assign(nl, nullptr); c->g.assign(nl, nullptr); c->x.assign(nl, nullptr);
+  c->tmaps.assign(nl, nullptr);
   c->uvec.assign(nl, nullptr); c->flf.assign(nl, nullptr); c->flb.assign(nl, nullptr);
   c->dnf.assign(nl, nullptr); c->dnb.assign(nl, nullptr);
   c->slot_epoch.assign(nl, 0);
@@ -559,6 +610,8 @@ int ensure_slots(rba_ctx* c) {
   c->NRw = c->NRs;
   for (int l = 0; l < nl; ++l) {
     if ((rc = dalloc(c, c->pole_allocs, &c->factor[l], S.panel_off[S.nfront], &c->mem_factor))) return rc;
+    if (c->gemm_v == 6 && c->gemm5_var == 6 || c->panel_v == 6 && c->panel_var == 6)
+      if ((rc = make_tmaps(c, c->factor[l], &c->tmaps[l]))) return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->g[l], (size_t)c->N * c->NRw, &c->mem_work))) return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->x[l], (size_t)c->N * c->NRw, &c->mem_work))) return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->uvec[l], (size_t)std::max<int64_t>(S.uvec_off[S.nfront], 1) * c->NRw, &c->mem_work))) return rc;
@@ -810,11 +863,12 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     if (std::string(e) == "v6d") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 3; }
     if (std::string(e) == "v7") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 4; }
     if (std::string(e) == "v7b") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 5; }
+    if (std::string(e) == "v8") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 6; }
   }
   if (const char* e = getenv("RBA_GEMM_PANEL")) {
     const std::string v(e);
-    const char* names[] = {"v6", "v6b", "v6c", "v6d", "v7", "v7b"};
-    for (int q = 0; q < 6; ++q)
+    const char* names[] = {"v6", "v6b", "v6c", "v6d", "v7", "v7b", "v8"};
+    for (int q = 0; q < 7; ++q)
       if (v == names[q]) { c->panel_v = 6; c->panel_var = q; }
     if (v == "v5") { c->panel_v = 5; c->panel_var = 0; }
   }
@@ -1049,6 +1103,7 @@ int rba_factor(rba_ctx* c) {
       int l = b0 + i;
       c->valid[l] = 0;
       pb.factor[i] = c->factor[l];
+      pb.tmap[i] = c->tmaps[l];
       pb.upd[i] = c->upd[i];
       pb.dvec[i] = c->dvec[i];
       pb.xi[i] = c->poles_h[c->local[l]];
@@ -1089,6 +1144,7 @@ int rba_factor_values(rba_ctx* c, int32_t slot, const double* vals) {
   rba::PoleBatch pb;
   pb.count = 1;
   pb.factor[0] = c->factor[slot];
+  pb.tmap[0] = c->tmaps[slot];
   pb.upd[0] = c->upd[0];
   pb.dvec[0] = c->dvec[0];
   pb.xi[0] = rba::cmk(0.0, 0.0);

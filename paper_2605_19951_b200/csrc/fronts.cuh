@@ -23,8 +23,15 @@ struct FrontsDev {
   const int64_t* blk_off;    // per front: offset of its pivot-block flags
 };
 
+// TMA tensor map (CUtensorMap, 128 B) as stored in device memory.
+struct alignas(64) TMap { unsigned char b[128]; };
+// per front: [0] A operand (66-row x G8K-column box of the panel),
+//            [1] B operand (34-row x G8K-column box)
+constexpr int G8K = 8;
+
 // Batch of poles processed by one launch (gridDim.y or ticket modulo).
 struct PoleBatch {
+  const TMap* tmap[32]; // per slot: tensor maps of the slot's factor panels (or null)
   cplx* factor[32];     // per slot: factor storage base
   cplx* upd[32];        // per slot: update arena base
   cplx* dvec[32];       // per slot: pivots d in global pivot order (contiguous copy of the diagonal)

@@ -977,7 +977,7 @@ struct Stage6 {
 
 // NCOL = 32: 4 warps on a 64x32 half tile (2-3 CTAs/SM); NCOL = 64: 8 warps
 // on the whole 64x64 tile, up to 255 registers, one CTA/SM.
-template <int G6K, int NS, int NCOL>
+template <int G6K, int NS, int NCOL, bool TMAP>
 __global__ void __launch_bounds__(NCOL * 4, NCOL == 32 ? 2 : 1) k_gemm6(
     const GemmTask* __restrict__ tasks, int ntasks, FrontsDev F, PoleBatch pb,
     const cplx* __restrict__ zeros) {
@@ -1018,11 +1018,26 @@ __global__ void __launch_bounds__(NCOL * 4, NCOL == 32 ? 2 : 1) k_gemm6(
   const unsigned nb = (unsigned)min(NCOL, nf - cc0) * 16u;
   const cplx* __restrict__ dvec = pb.dvec[slot] + F.first[s];
 
+  const TMap* tm = TMAP ? pb.tmap[slot] + 2 * s : nullptr;
   auto issue = [&](int ch) {
     St& S = st[ch % NS];
     const unsigned bar = smem_u32(&full[ch % NS]);
     const int kt = t0 + ch * G6K;
     const int nval = max(0, min(G6K, t1 - kt));
+    if (TMAP) {
+      // one tensor copy per operand: boxes of 66 (A) / 34 (B) rows x G6K
+      // columns land in the padded [k][row] layout; rows past nf and columns
+      // past npiv are zero-filled by the TMA unit (chunks never straddle t1
+      // except at t1 = npiv, see build_plans)
+      if (lane == 0) {
+        mbar_expect_tx(bar, (unsigned)G6K * (G6LA + G6LB) * 16u + (unsigned)G6K * 16u);
+        if (nval > 0) bulk_g2s(smem_u32(&S.d[0]), dvec + kt, (unsigned)nval * 16u, bar);
+        if (nval < G6K) bulk_g2s(smem_u32(&S.d[nval]), zeros, (unsigned)(G6K - nval) * 16u, bar);
+        tma_2d(smem_u32(&S.a[0]), tm, 2 * r0, kt, bar);
+        tma_2d(smem_u32(&S.b[0]), tm + 1, 2 * cc0, kt, bar);
+      }
+      return;
+    }
     if (lane == 0) {
       mbar_expect_tx(bar, (unsigned)nval * (na + nb) + (unsigned)(G6K - nval) * (1024u + NCOL * 16u) +
                               (unsigned)G6K * 16u);
@@ -1147,23 +1162,24 @@ __global__ void __launch_bounds__(NCOL * 4, NCOL == 32 ? 2 : 1) k_gemm6(
   }
 }
 
-template <int G6K, int NS, int NCOL>
+template <int G6K, int NS, int NCOL, bool TMAP = false>
 static void launch_g6(cudaStream_t st, dim3 grid, const GemmTask* tasks, int ntasks,
                       const FrontsDev& F, const PoleBatch& pb, const cplx* zeros) {
   const size_t smem = NS * sizeof(Stage6<G6K, NCOL>);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm6<G6K, NS, NCOL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_gemm6<G6K, NS, NCOL, TMAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = true;
   }
-  k_gemm6<G6K, NS, NCOL><<<grid, NCOL * 4, smem, st>>>(tasks, ntasks, F, pb, zeros);
+  k_gemm6<G6K, NS, NCOL, TMAP><<<grid, NCOL * 4, smem, st>>>(tasks, ntasks, F, pb, zeros);
 }
 
 // variant 0: 16 k x 4 stages (2 CTAs/SM); 1: 8 k x 8 stages (2 CTAs/SM);
 // 2: 8 k x 5 stages (65 KB, 3 CTAs/SM); 3: 12 k x 3 stages (3 CTAs/SM);
 // 4: whole 64x64 tile, 8 warps, 16 k x 6 stages (1 CTA/SM); 5: 64x64, 16 k x 4
-// (1 CTA/SM)
+// (1 CTA/SM); 6: as 2 with the operands moved by two TMA tensor copies per
+// stage (tensor maps per front, make_tmaps) instead of one bulk copy per column
 void launch_gemm6(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
                   const FrontsDev& F, const PoleBatch& pb, const cplx* zeros, int variant) {
   if (ntasks <= 0 || nctas <= 0) return;
@@ -1173,6 +1189,7 @@ void launch_gemm6(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
   else if (variant == 3) launch_g6<12, 3, 32>(st, grid, tasks, ntasks, F, pb, zeros);
   else if (variant == 4) launch_g6<16, 6, 64>(st, grid1, tasks, ntasks, F, pb, zeros);
   else if (variant == 5) launch_g6<16, 4, 64>(st, grid1, tasks, ntasks, F, pb, zeros);
+  else if (variant == 6) launch_g6<G8K, 5, 32, true>(st, grid, tasks, ntasks, F, pb, zeros);
   else launch_g6<16, 4, 32>(st, grid, tasks, ntasks, F, pb, zeros);
 }
 

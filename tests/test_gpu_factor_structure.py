@@ -51,7 +51,7 @@ def test_dmma_gemm_matches_dfma_reference(gpu, monkeypatch):
     approx = rb.config_approximant("C1")
     model = prob.true_model()
     out = []
-    modes = ("dfma", "v1", "v2", "v3", "v4", "v5", "v5b", "v6", "v6b", "v6c", "v6d", "v7", "v7b")
+    modes = ("dfma", "v1", "v2", "v3", "v4", "v5", "v5b", "v6", "v6b", "v6c", "v6d", "v7", "v7b", "v8")
     for mode in modes:
         monkeypatch.setenv("RBA_GEMM", mode)
         cache = rb.ShiftedFactorCache()
