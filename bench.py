@@ -335,6 +335,15 @@ def component_rates(eng, cache, drv, flops, nnzL, world):
     out["solve_ms_per_pole"] = ms / nl
     v = torch.randn(eng.P, dtype=torch.float64, device="cuda")
     w = torch.randn(eng.S * eng.Kt * eng.Mr, dtype=torch.float64, device="cuda")
+    # first action after the factorisation: builds the receiver Green's
+    # functions Z_i = A_i^{-1} Q^T in receiver-Green mode
+    info = eng.info()
+    out["jvp_mode"] = "receiver-green" if info.get("green") else "sweeps"
+    e0.record(stream)
+    eng.jvp(v)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    out["first_jvp_ms"] = e0.elapsed_time(e1)
     reps = 3
     e0.record(stream)
     for _ in range(reps):

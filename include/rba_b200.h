@@ -114,7 +114,12 @@ int rba_solve_d(rba_ctx* ctx, int32_t slot, const double* rhs_d, double* out_d, 
 /* Forward pass (solve_all_poles with the sources + Q): stores g_i per local
  * pole and writes q_part_d[slot][S][M_r] (complex) = Q g_i. */
 int rba_forward_partial(rba_ctx* ctx, double* qpart_d);
-/* J v partials (sensitivity.py:65-79): q_part_d[slot][S][M_r] = Q A_i^{-1}(dM(g_i) v). */
+/* J v partials (sensitivity.py:65-79): q_part_d[slot][S][M_r] = Q A_i^{-1}(dM(g_i) v).
+ * Receiver-Green mode (env RBA_GREEN, default on when memory allows): the
+ * first J v / J^T w after a factorisation builds Z_i = A_i^{-1} Q^T with
+ * M_r / NR multi-RHS solves; then Q A_i^{-1} h = Z_i^T h and
+ * A_i^{-T} Q^T z = Z_i z (A_i complex symmetric) stream Z_i instead of the
+ * two triangular sweeps.  Same mathematics, rounding-level differences. */
 int rba_jvp_partial(rba_ctx* ctx, const double* v_d, double* qpart_d);
 /* J^T w partials (sensitivity.py:81-97): t_part_d[slot][P] = 2 Re xi_i dM_i^T A_i^{-T} Q^T(sum_j alpha_ij w_j). */
 int rba_vjp_partial(rba_ctx* ctx, const double* w_d, double* tpart_d);
@@ -149,7 +154,8 @@ int rba_vec_dot(rba_ctx* ctx, int64_t n, const double* x_d, const double* y_d, d
 int rba_vec_lsqr_xw(rba_ctx* ctx, int64_t n, double t1, double t2, const double* v_d,
                     double* w_d, double* x_d, double* wnorm2_h);
 /* counters (CacheCounters, shifted.py:64-70) and sizes:
- * out[8]: factorizations, solves, N, P, Mr, S, m, n_local */
+ * out[10]: factorizations, solves, N, P, Mr, S, m, n_local,
+ *          receiver-Green mode on (1/0), Green builds (slots) */
 int rba_info(rba_ctx* ctx, int64_t* out_h);
 /* bytes of device memory held by the context: factors, workspace, other */
 int rba_memory(rba_ctx* ctx, int64_t* out_h);

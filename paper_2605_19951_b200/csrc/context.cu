@@ -114,6 +114,15 @@ struct rba_ctx {
   // per local slot
   std::vector<cplx*> factor, g, x, uvec;
   std::vector<rba::TMap*> tmaps;  // per slot: [nfront][2] tensor maps of the factor panels
+  // receiver Green's functions Z = A^{-1} Q^T per slot (RBA_GREEN, default on
+  // when they fit): J v / J^T w stream Z instead of sweeping the factor
+  bool green_req = true;
+  bool green = false;
+  std::vector<cplx*> Z;
+  std::vector<char> green_valid;
+  cplx* green_part = nullptr;
+  int green_chunks = 64;
+  int64_t n_green = 0;            // Z builds (slots)
   std::vector<int*> flf, flb, dnf, dnb;
   std::vector<int> slot_epoch;    // solves issued per local slot (flags / counters)
   std::vector<char> valid;
@@ -163,7 +172,7 @@ struct rba_ctx {
 namespace {
 
 enum KClass { KC_SCATTER = 0, KC_EA = 1, KC_DIAG = 2, KC_TRSM = 3, KC_GEMM = 4, KC_FWD = 5,
-              KC_BWD = 6, KC_ELEM = 7, KC_VEC = 8, KC_ASSEMBLY = 9 };
+              KC_BWD = 6, KC_ELEM = 7, KC_VEC = 8, KC_ASSEMBLY = 9, KC_GREEN = 10 };
 
 struct Timed {
   rba_ctx* c;
@@ -634,13 +643,33 @@ int ensure_slots(rba_ctx* c) {
     c->fbatch = 1;
     for (int k = 2; k <= 8 && k <= nl; ++k)
       if (fr > k * need + ((size_t)8 << 30)) c->fbatch = k;
-  }
-  if (const char* e = getenv("RBA_FACTOR_BATCH")) c->fbatch = std::max(1, std::min(atoi(e), nl));
-  c->upd.assign(c->fbatch, nullptr);
-  c->dvec.assign(c->fbatch, nullptr);
-  for (int b = 0; b < c->fbatch; ++b) {
-    if ((rc = dalloc(c, c->pole_allocs, &c->upd[b], (size_t)S.upd_total, &c->mem_work))) return rc;
-    if ((rc = dalloc(c, c->pole_allocs, &c->dvec[b], (size_t)S.n, &c->mem_work))) return rc;
+    if (const char* e = getenv("RBA_FACTOR_BATCH")) c->fbatch = std::max(1, std::min(atoi(e), nl));
+    // The receiver Green's functions Z_l (needed between a factorisation and
+    // the next one: J v / J^T w) and the update arenas (needed only inside a
+    // factorisation) are never live together, so they share one allocation;
+    // any factorisation invalidates every Z_l.
+    const size_t arenas = (size_t)c->fbatch * S.upd_total;
+    const size_t zsz = (size_t)c->N * std::max<int64_t>(c->Mr, 1);
+    const size_t zall = (size_t)nl * zsz;
+    const size_t extra = zall > arenas ? (zall - arenas) * sizeof(cplx) : 0;
+    c->green = c->green_req && c->Mr > 0 && fr > (size_t)c->fbatch * need + extra + ((size_t)8 << 30);
+    cplx* pool = nullptr;
+    if ((rc = dalloc(c, c->pole_allocs, &pool, c->green ? std::max(arenas, zall) : arenas, &c->mem_work)))
+      return rc;
+    c->upd.assign(c->fbatch, nullptr);
+    c->dvec.assign(c->fbatch, nullptr);
+    for (int b = 0; b < c->fbatch; ++b) {
+      c->upd[b] = pool + (size_t)b * S.upd_total;
+      if ((rc = dalloc(c, c->pole_allocs, &c->dvec[b], (size_t)S.n, &c->mem_work))) return rc;
+    }
+    c->Z.assign(nl, nullptr);
+    c->green_valid.assign(nl, 0);
+    if (c->green) {
+      for (int l = 0; l < nl; ++l) c->Z[l] = pool + (size_t)l * zsz;
+      if ((rc = dalloc(c, c->pole_allocs, &c->green_part,
+                       (size_t)c->green_chunks * nl * std::max(c->S, 1) * c->Mr, &c->mem_work)))
+        return rc;
+    }
   }
   if ((rc = dalloc(c, c->pole_allocs, &c->wa, (size_t)nl * std::max(c->S, 1) * std::max<int64_t>(c->Mr, 1), &c->mem_work))) return rc;
   std::vector<int32_t> pos(c->local.begin(), c->local.end());
@@ -872,6 +901,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
       if (v == names[q]) { c->panel_v = 6; c->panel_var = q; }
     if (v == "v5") { c->panel_v = 5; c->panel_var = 0; }
   }
+  if (const char* e = getenv("RBA_GREEN")) c->green_req = std::string(e) != "0";
   if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) == "fused";
   if (const char* e = getenv("RBA_SMALLP")) c->small_p = std::string(e) == "64" ? rba::PB : 2 * rba::PB;
   if (const char* e = getenv("RBA_DIAG")) c->diag_v1 = std::string(e) == "v1";
@@ -1096,6 +1126,7 @@ int rba_factor(rba_ctx* c) {
   const rba::Symbolic& S = c->sym;
   const int nl = (int)c->local.size();
   if (c->timing) cudaEventRecord(c->ev[0], c->st);
+  for (auto& v : c->green_valid) v = 0;   // the update arenas overlay Z
   for (int b0 = 0; b0 < nl; b0 += c->fbatch) {
     rba::PoleBatch pb;
     pb.count = std::min(c->fbatch, nl - b0);
@@ -1149,6 +1180,7 @@ int rba_factor_values(rba_ctx* c, int32_t slot, const double* vals) {
   pb.dvec[0] = c->dvec[0];
   pb.xi[0] = rba::cmk(0.0, 0.0);
   c->valid[slot] = 0;
+  for (auto& v : c->green_valid) v = 0;   // the update arenas overlay Z
   if ((rc = run_plan(c, pb))) return rc;
   if ((rc = check_err(c, c->local[slot]))) return rc;
   c->valid[slot] = 1;
@@ -1239,16 +1271,63 @@ int rba_forward_partial(rba_ctx* c, double* qpart) {
   return RBA_OK;
 }
 
+static rba::SlotPtrs slot_sub(const std::vector<cplx*>& v, const std::vector<int>& slots) {
+  rba::SlotPtrs p;
+  for (size_t i = 0; i < slots.size() && i < 32; ++i) p.p[i] = v[slots[i]];
+  return p;
+}
+
+// Build Z = A^{-1} Q^T for every local slot whose factor changed: Mr/NRw
+// multi-RHS solves over all such slots at once, columns stored row-major.
+static int ensure_green(rba_ctx* c) {
+  std::vector<int> slots;
+  for (int l = 0; l < (int)c->local.size(); ++l)
+    if (!c->green_valid[l]) {
+      if (!c->valid[l]) return fail(RBA_ERR_CACHE_MISS, "no factorization for pole " +
+                                                           std::to_string(c->local[l]));
+      slots.push_back(l);
+    }
+  if (slots.empty()) return RBA_OK;
+  const int ns = (int)slots.size(), nb = c->NRw;
+  const rba::SlotPtrs xs = slot_sub(c->x, slots), zs = slot_sub(c->Z, slots);
+  int rc;
+  for (int64_t m0 = 0; m0 < c->Mr; m0 += nb) {
+    const int n = (int)std::min<int64_t>(nb, c->Mr - m0);
+    {
+      Timed t(c, KC_GREEN);
+      rba::launch_green_rhs(c->st, ns, c->N, m0, n, nb, c->qt_ptr, c->qt_col, c->qt_val, xs);
+    }
+    CKL();
+    if ((rc = solve_slots(c, slots, nb))) return rc;
+    {
+      Timed t(c, KC_GREEN);
+      rba::launch_green_store(c->st, ns, c->N, c->Mr, m0, n, nb, xs, zs);
+    }
+    CKL();
+  }
+  for (int l : slots) c->green_valid[l] = 1;
+  c->n_green += ns;
+  return RBA_OK;
+}
+
 int rba_jvp_partial(rba_ctx* c, const double* v_d, double* qpart) {
   if (!c || !c->model_set || !v_d || !qpart) return fail(RBA_ERR_STATE, "bad state/arguments");
   CK(cudaSetDevice(c->device));
   const int nl = (int)c->local.size();
+  int rc;
+  if (c->green && (rc = ensure_green(c))) return rc;
   {
     Timed t(c, KC_ELEM);
     rba::launch_jvp_rhs(c->st, nl, elem(c), v_d, slot_ptrs(c->g), slot_ptrs(c->x), c->NRs, c->S);
   }
   CKL();
-  int rc;
+  if (c->green) {
+    Timed t(c, KC_GREEN, 2);
+    rba::launch_green_jvp(c->st, nl, c->N, (int)c->Mr, c->S, c->NRs, c->green_chunks,
+                          slot_ptrs(c->Z), slot_ptrs(c->x), c->green_part, (cplx*)qpart);
+    CKL();
+    return RBA_OK;
+  }
   if ((rc = solve_slots(c, all_slots(c), c->NRs))) return rc;
   if (c->Mr > 0) {
     Timed t(c, KC_ELEM);
@@ -1262,14 +1341,23 @@ int rba_vjp_partial(rba_ctx* c, const double* w_d, double* tpart) {
   if (!c || !c->model_set || !w_d || !tpart) return fail(RBA_ERR_STATE, "bad state/arguments");
   CK(cudaSetDevice(c->device));
   const int nl = (int)c->local.size();
-  {
+  int rc;
+  if (c->green) {
+    if ((rc = ensure_green(c))) return rc;
+    {
+      Timed t0(c, KC_GREEN, 2);
+      rba::launch_walpha(c->st, nl, c->pole_of_slot, c->S, c->Kt, c->Mr, w_d, c->res_d, c->wa);
+      rba::launch_green_vjp(c->st, nl, c->N, (int)c->Mr, c->S, c->NRs, slot_ptrs(c->Z), c->wa,
+                            slot_ptrs(c->x));
+    }
+    CKL();
+  } else {
   Timed t0(c, KC_ELEM, 2);
   rba::launch_vjp_rhs(c->st, nl, c->pole_of_slot, c->S, c->Kt, c->Mr, c->N, w_d, c->res_d, c->qt_ptr,
                       c->qt_col, c->qt_val, c->wa, slot_ptrs(c->x), c->NRs);
   }
   CKL();
-  int rc;
-  if ((rc = solve_slots(c, all_slots(c), c->NRs))) return rc;
+  if (!c->green && (rc = solve_slots(c, all_slots(c), c->NRs))) return rc;
   Timed t1(c, KC_ELEM);
   rba::launch_vjp_cells(c->st, nl, c->pole_of_slot, c->poles_d, elem(c), slot_ptrs(c->x), slot_ptrs(c->g),
                         c->NRs, c->S, tpart);
@@ -1413,6 +1501,7 @@ int rba_info(rba_ctx* c, int64_t* out) {
   if (!c || !out) return fail(RBA_ERR_INVALID, "null argument");
   out[0] = c->n_fact; out[1] = c->n_solve; out[2] = c->N; out[3] = c->P;
   out[4] = c->Mr; out[5] = c->S; out[6] = c->m; out[7] = (int64_t)c->local.size();
+  out[8] = c->green ? 1 : 0; out[9] = c->n_green;
   return RBA_OK;
 }
 

@@ -91,6 +91,18 @@ void launch_vjp_rhs(cudaStream_t st, int nslots, const int32_t* pole_of_slot, in
                     int64_t Mr, int64_t N, const double* w, const cplx* residues,
                     const int64_t* qtptr, const int32_t* qtcol, const double* qtval,
                     cplx* wa /* [slot][S][Mr] */, const SlotPtrs& out, int NR);
+// receiver Green's functions (kernels_ops.cu)
+void launch_green_rhs(cudaStream_t st, int nslots, int64_t N, int64_t m0, int nb, int NR,
+                      const int64_t* qtptr, const int32_t* qtcol, const double* qtval,
+                      const SlotPtrs& x);
+void launch_green_store(cudaStream_t st, int nslots, int64_t N, int64_t Mr, int64_t m0, int nb,
+                        int NR, const SlotPtrs& x, const SlotPtrs& Z);
+void launch_green_jvp(cudaStream_t st, int nslots, int64_t N, int Mr, int S, int NR, int nchunk,
+                      const SlotPtrs& Z, const SlotPtrs& h, cplx* part, cplx* qpart);
+void launch_walpha(cudaStream_t st, int nslots, const int32_t* pole_of_slot, int S, int Kt,
+                   int64_t Mr, const double* w, const cplx* residues, cplx* wa);
+void launch_green_vjp(cudaStream_t st, int nslots, int64_t N, int Mr, int S, int NR,
+                      const SlotPtrs& Z, const cplx* wa, const SlotPtrs& x);
 void launch_vjp_cells(cudaStream_t st, int nslots, const int32_t* pole_of_slot,
                       const cplx* poles, const ElemDev& E, const SlotPtrs& z,
                       const SlotPtrs& g, int NR, int S, double* tpart /* [slot][P] */);

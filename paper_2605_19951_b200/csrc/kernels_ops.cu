@@ -189,6 +189,172 @@ void launch_vjp_rhs(cudaStream_t st, int nslots, const int32_t* pole_of_slot, in
   k_qt_apply<<<grid, 256, 0, st>>>(N, S, Mr, qtptr, qtcol, qtval, wa, out, NR);
 }
 
+// ---------------------------------------------------------------------------
+// Receiver Green's functions Z_i = A_i^{-1} Q^T (N x Mr per pole, permuted
+// rows, row-major [j][m]).  With A_i complex symmetric,
+//   Q A_i^{-1} h    = Z_i^T h      (J v,  sensitivity.py:73-74)
+//   A_i^{-T} Q^T z  = Z_i z        (J^T w, sensitivity.py:89-91)
+// so once Z_i is built (Mr/NR multi-RHS solves per factorisation), every
+// LSQR action streams Z_i (N*Mr*16 bytes) instead of two triangular sweeps
+// over the factor (2*nnz(L)*16 bytes each way).
+// ---------------------------------------------------------------------------
+
+// x[slot][k][r] = Q^T[k, m0 + r]  (r < nb), 0 otherwise
+__global__ void k_green_rhs(int64_t N, int64_t m0, int nb, int NR, const int64_t* __restrict__ qtptr,
+                            const int32_t* __restrict__ qtcol, const double* __restrict__ qtval,
+                            SlotPtrs x) {
+  cplx* o = x.p[blockIdx.y];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < N;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    for (int r = 0; r < NR; ++r) {
+      double a = 0.0;
+      if (r < nb)
+        for (int64_t e = qtptr[k]; e < qtptr[k + 1]; ++e)
+          if (qtcol[e] == m0 + r) a += qtval[e];
+      o[k * NR + r] = cmk(a, 0.0);
+    }
+  }
+}
+
+// Z[slot][k][m0 + r] = x[slot][k][r]
+__global__ void k_green_store(int64_t N, int64_t Mr, int64_t m0, int nb, int NR, SlotPtrs x,
+                              SlotPtrs Z) {
+  const cplx* xs = x.p[blockIdx.y];
+  cplx* z = Z.p[blockIdx.y];
+  const int64_t total = N * nb;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = t / nb;
+    const int r = (int)(t - k * nb);
+    z[k * Mr + m0 + r] = xs[k * NR + r];
+  }
+}
+
+// part[chunk][slot][s][m] = sum_{j in chunk} Z[slot][j][m] h[slot][j][s]
+template <int NR>
+__global__ void __launch_bounds__(128) k_green_jvp(int64_t N, int Mr, int S, int64_t rows_per_chunk,
+                                                   SlotPtrs Z, SlotPtrs h, cplx* __restrict__ part) {
+  const int slot = blockIdx.y, nslots = gridDim.y, chunk = blockIdx.x;
+  const cplx* z = Z.p[slot];
+  const cplx* hs = h.p[slot];
+  const int64_t j0 = chunk * rows_per_chunk, j1 = min(N, j0 + rows_per_chunk);
+  for (int m = threadIdx.x; m < Mr; m += blockDim.x) {
+    cplx acc[NR];
+#pragma unroll
+    for (int s = 0; s < NR; ++s) acc[s] = cmk(0.0, 0.0);
+#pragma unroll 4
+    for (int64_t j = j0; j < j1; ++j) {
+      const cplx zv = __ldg(z + j * Mr + m);
+#pragma unroll
+      for (int s = 0; s < NR; ++s)
+        if (s < S) acc[s] = cfma(zv, __ldg(hs + j * NR + s), acc[s]);
+    }
+    for (int s = 0; s < S; ++s)
+      part[(((int64_t)chunk * nslots + slot) * S + s) * Mr + m] = acc[s];
+  }
+}
+
+// qpart[slot][s][m] = sum_chunk part[chunk][slot][s][m], chunks ascending
+__global__ void k_green_reduce(int nchunk, int64_t per_chunk, const cplx* __restrict__ part,
+                               cplx* __restrict__ qpart) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < per_chunk;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    cplx a = cmk(0.0, 0.0);
+    for (int c = 0; c < nchunk; ++c) a = cadd(a, part[c * per_chunk + t]);
+    qpart[t] = a;
+  }
+}
+
+// x[slot][j][s] = sum_m Z[slot][j][m] wa[slot][s][m]   (warp per row)
+template <int NR>
+__global__ void __launch_bounds__(256) k_green_vjp(int64_t N, int Mr, int S, SlotPtrs Z,
+                                                   const cplx* __restrict__ wa, SlotPtrs x) {
+  extern __shared__ cplx wsm[];   // [S][Mr]
+  const int slot = blockIdx.y;
+  const cplx* z = Z.p[slot];
+  cplx* xs = x.p[slot];
+  for (int e = threadIdx.x; e < S * Mr; e += blockDim.x) wsm[e] = wa[(int64_t)slot * S * Mr + e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); j < N; j += nw) {
+    cplx acc[NR];
+#pragma unroll
+    for (int s = 0; s < NR; ++s) acc[s] = cmk(0.0, 0.0);
+    for (int m = lane; m < Mr; m += 32) {
+      const cplx zv = __ldg(z + j * Mr + m);
+#pragma unroll
+      for (int s = 0; s < NR; ++s)
+        if (s < S) acc[s] = cfma(zv, wsm[s * Mr + m], acc[s]);
+    }
+#pragma unroll
+    for (int s = 0; s < NR; ++s) {
+      double a = acc[s].x, b = acc[s].y;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+      }
+      acc[s] = cmk(a, b);
+    }
+    if (lane < NR) {
+      cplx v = cmk(0.0, 0.0);
+#pragma unroll
+      for (int s = 0; s < NR; ++s)
+        if (s == lane && s < S) v = acc[s];
+      xs[j * NR + lane] = v;
+    }
+  }
+}
+
+void launch_green_rhs(cudaStream_t st, int nslots, int64_t N, int64_t m0, int nb, int NR,
+                      const int64_t* qtptr, const int32_t* qtcol, const double* qtval,
+                      const SlotPtrs& x) {
+  dim3 grid(grid_for(N), nslots);
+  k_green_rhs<<<grid, 256, 0, st>>>(N, m0, nb, NR, qtptr, qtcol, qtval, x);
+}
+void launch_green_store(cudaStream_t st, int nslots, int64_t N, int64_t Mr, int64_t m0, int nb,
+                        int NR, const SlotPtrs& x, const SlotPtrs& Z) {
+  dim3 grid(grid_for(N * nb), nslots);
+  k_green_store<<<grid, 256, 0, st>>>(N, Mr, m0, nb, NR, x, Z);
+}
+void launch_green_jvp(cudaStream_t st, int nslots, int64_t N, int Mr, int S, int NR, int nchunk,
+                      const SlotPtrs& Z, const SlotPtrs& h, cplx* part, cplx* qpart) {
+  const int64_t rpc = (N + nchunk - 1) / nchunk;
+  dim3 grid(nchunk, nslots);
+  switch (NR) {
+    case 1: k_green_jvp<1><<<grid, 128, 0, st>>>(N, Mr, S, rpc, Z, h, part); break;
+    case 2: k_green_jvp<2><<<grid, 128, 0, st>>>(N, Mr, S, rpc, Z, h, part); break;
+    case 4: k_green_jvp<4><<<grid, 128, 0, st>>>(N, Mr, S, rpc, Z, h, part); break;
+    default: k_green_jvp<8><<<grid, 128, 0, st>>>(N, Mr, S, rpc, Z, h, part); break;
+  }
+  const int64_t per = (int64_t)nslots * S * Mr;
+  k_green_reduce<<<grid_for(per), 256, 0, st>>>(nchunk, per, part, qpart);
+}
+void launch_walpha(cudaStream_t st, int nslots, const int32_t* pole_of_slot, int S, int Kt,
+                   int64_t Mr, const double* w, const cplx* residues, cplx* wa) {
+  const int64_t total = (int64_t)nslots * S * Mr;
+  if (total > 0)
+    k_walpha<<<grid_for(total), 256, 0, st>>>(nslots, pole_of_slot, S, Kt, Mr, w, residues, wa);
+}
+void launch_green_vjp(cudaStream_t st, int nslots, int64_t N, int Mr, int S, int NR,
+                      const SlotPtrs& Z, const cplx* wa, const SlotPtrs& x) {
+  dim3 grid(148 * 4, nslots);
+  const size_t smem = (size_t)S * Mr * sizeof(cplx);
+  if (smem > 48 * 1024) {
+    cudaFuncSetAttribute(k_green_vjp<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_green_vjp<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_green_vjp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_green_vjp<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  switch (NR) {
+    case 1: k_green_vjp<1><<<grid, 256, smem, st>>>(N, Mr, S, Z, wa, x); break;
+    case 2: k_green_vjp<2><<<grid, 256, smem, st>>>(N, Mr, S, Z, wa, x); break;
+    case 4: k_green_vjp<4><<<grid, 256, smem, st>>>(N, Mr, S, Z, wa, x); break;
+    default: k_green_vjp<8><<<grid, 256, smem, st>>>(N, Mr, S, Z, wa, x); break;
+  }
+}
+
 // tpart[slot][c] = sum_s 2 Re( xi_i * e^{m_c} sum_a z_a (M_c g)_a )
 template <int NR>
 __global__ void k_vjp_cells(const int32_t* __restrict__ pole_of_slot,

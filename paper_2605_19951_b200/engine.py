@@ -279,17 +279,18 @@ class Engine:
 
     # ------------------------------------------------------------ info
     def info(self) -> dict:
-        out = np.zeros(8, np.int64)
+        out = np.zeros(10, np.int64)
         check(self.lib.rba_info(self.ctx, ptr(out)))
         mem = np.zeros(3, np.int64)
         check(self.lib.rba_memory(self.ctx, ptr(mem)))
         return dict(factorizations=int(out[0]), solves=int(out[1]), N=int(out[2]),
                     P=int(out[3]), Mr=int(out[4]), S=int(out[5]), m=int(out[6]),
-                    n_local=int(out[7]), mem_factor=int(mem[0]), mem_work=int(mem[1]),
+                    n_local=int(out[7]), green=bool(out[8]), green_builds=int(out[9]),
+                    mem_factor=int(mem[0]), mem_work=int(mem[1]),
                     mem_other=int(mem[2]))
 
     KCLASSES = ("scatter", "extend_add", "diag", "trsm", "gemm", "solve_fwd", "solve_bwd",
-                "elem", "vec", "assembly")
+                "elem", "vec", "assembly", "green")
 
     def set_timing(self, mode):
         """True/1: record device time per kernel class; False/0: stop; 2: reset."""

@@ -123,3 +123,28 @@ def test_blocked_diag_matches_unblocked(gpu, monkeypatch):
         outs.append(buf)
         eng.close()
     assert rel(outs[1], outs[0]) <= 1e-10
+
+
+def test_receiver_green_matches_sweeps(gpu, monkeypatch):
+    """J v / J^T w through the receiver Green's functions Z_i = A_i^{-1} Q^T
+    (default) equal the per-action triangular sweeps (RBA_GREEN=0) to
+    rounding, and the logical solve counters are unchanged."""
+    prob, _ = rb.build_config("C3", n=8)
+    approx = rb.config_approximant("C3")
+    model = prob.true_model()
+    outs, counts = [], []
+    for green in ("1", "0"):
+        monkeypatch.setenv("RBA_GREEN", green)
+        cache = rb.ShiftedFactorCache()
+        opr = rb.JacobianOperator(prob, model, approx, cache)
+        assert opr.engine.info()["green"] == (green == "1")
+        v = np.random.default_rng(1).standard_normal(opr.shape[1])
+        w = np.random.default_rng(2).standard_normal(opr.shape[0])
+        outs.append((opr.jvp(v), opr.vjp(w), opr.jvp(2 * v)))
+        counts.append(cache.counters.snapshot())
+        if green == "1":
+            assert opr.engine.info()["green_builds"] == len(opr.engine.local)
+        cache.engine.close()
+    assert counts[0] == counts[1]
+    for a, b in zip(outs[0], outs[1]):
+        assert rel(a, b) <= 1e-9
