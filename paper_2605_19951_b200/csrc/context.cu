@@ -49,6 +49,7 @@ struct Step {
   int n;
   int ntiles;
   int schur;   // ST_GEMM: 1 = Schur-complement update (K = npiv), 0 = panel update
+  int level;
 };
 
 int nr_pad(int s) { return s <= 1 ? 1 : s <= 2 ? 2 : s <= 4 ? 4 : 8; }
@@ -152,7 +153,7 @@ struct rba_ctx {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // per-kernel-class device time (CUDA events around every launch, enabled
   // by rba_set_timing) and the launch count of this context's kernels
-  double cls_ms[128] = {0};   // 0-15 kernel classes; 16+L fwd, 48+L bwd, 80+L gemm per level
+  double cls_ms[128] = {0};   // 0-15 kernel classes; 16+L fwd, 48+L bwd, 80+L factor per level
   bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernels
   int gemm_v = 6;             // default 3M DMMA kernel (k_gemm6); RBA_GEMM=v1..v5 select
                               // the earlier kernels for A/B tests
@@ -278,6 +279,7 @@ int build_plans(rba_ctx* c) {
   std::vector<rba::GemmTask> gm;
   c->plan.clear();
   for (int L = 0; L < S.nlevels; ++L) {
+    const size_t plan0 = c->plan.size();
     const int q0 = S.level_ptr[L], q1 = S.level_ptr[L + 1];
     // extend-add / zeroing
     int64_t off = ea.size();
@@ -356,6 +358,7 @@ int build_plans(rba_ctx* c) {
         tiles += ntr * (ntr + 1) / 2;
     }
     if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles, 1});
+    for (size_t q = plan0; q < c->plan.size(); ++q) c->plan[q].level = L;
   }
   int rc;
   if ((rc = upload(c, c->allocs, &c->ea_tasks, ea.data(), ea.size()))) return rc;
@@ -490,6 +493,7 @@ int build_plans(rba_ctx* c) {
 
 int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
   for (const Step& s : c->plan) {
+    Timed tl(c, 80 + std::min(s.level, 31), 0);   // factor time per level
     switch (s.kind) {
       case ST_EA: { Timed t(c, KC_EA); rba::launch_extend_add(c->st, c->ea_tasks + s.off, s.n, c->F, pb); break; }
       case ST_DIAG: {

@@ -231,26 +231,53 @@ __global__ void k_green_store(int64_t N, int64_t Mr, int64_t m0, int nb, int NR,
 }
 
 // part[chunk][slot][s][m] = sum_{j in chunk} Z[slot][j][m] h[slot][j][s]
+// Thread per m (coalesced Z rows); the chunk's h rows are staged in shared
+// memory 128 at a time, 8 Z loads in flight per thread.
 template <int NR>
 __global__ void __launch_bounds__(128) k_green_jvp(int64_t N, int Mr, int S, int64_t rows_per_chunk,
                                                    SlotPtrs Z, SlotPtrs h, cplx* __restrict__ part) {
+  constexpr int TR = 128;
+  __shared__ cplx hs[TR][NR];
   const int slot = blockIdx.y, nslots = gridDim.y, chunk = blockIdx.x;
   const cplx* z = Z.p[slot];
-  const cplx* hs = h.p[slot];
+  const cplx* hg = h.p[slot];
   const int64_t j0 = chunk * rows_per_chunk, j1 = min(N, j0 + rows_per_chunk);
-  for (int m = threadIdx.x; m < Mr; m += blockDim.x) {
+  for (int mb = 0; mb < Mr; mb += blockDim.x) {
+    const int m = mb + threadIdx.x;
+    const bool on = m < Mr;
     cplx acc[NR];
 #pragma unroll
     for (int s = 0; s < NR; ++s) acc[s] = cmk(0.0, 0.0);
-#pragma unroll 4
-    for (int64_t j = j0; j < j1; ++j) {
-      const cplx zv = __ldg(z + j * Mr + m);
+    for (int64_t t0 = j0; t0 < j1; t0 += TR) {
+      const int nt = (int)min((int64_t)TR, j1 - t0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < nt * NR; e += blockDim.x)
+        hs[e / NR][e % NR] = __ldg(hg + t0 * NR + e);
+      __syncthreads();
+      if (on) {
+        const cplx* zp = z + t0 * Mr + m;
+        int jj = 0;
+        for (; jj + 8 <= nt; jj += 8) {
+          cplx zv[8];
 #pragma unroll
-      for (int s = 0; s < NR; ++s)
-        if (s < S) acc[s] = cfma(zv, __ldg(hs + j * NR + s), acc[s]);
+          for (int u = 0; u < 8; ++u) zv[u] = __ldg(zp + (int64_t)(jj + u) * Mr);
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+#pragma unroll
+            for (int s = 0; s < NR; ++s)
+              if (s < S) acc[s] = cfma(zv[u], hs[jj + u][s], acc[s]);
+        }
+        for (; jj < nt; ++jj) {
+          const cplx zv = __ldg(zp + (int64_t)jj * Mr);
+#pragma unroll
+          for (int s = 0; s < NR; ++s)
+            if (s < S) acc[s] = cfma(zv, hs[jj][s], acc[s]);
+        }
+      }
     }
-    for (int s = 0; s < S; ++s)
-      part[(((int64_t)chunk * nslots + slot) * S + s) * Mr + m] = acc[s];
+    if (on)
+      for (int s = 0; s < S; ++s)
+        part[(((int64_t)chunk * nslots + slot) * S + s) * Mr + m] = acc[s];
   }
 }
 
@@ -265,7 +292,10 @@ __global__ void k_green_reduce(int nchunk, int64_t per_chunk, const cplx* __rest
   }
 }
 
-// x[slot][j][s] = sum_m Z[slot][j][m] wa[slot][s][m]   (warp per row)
+// x[slot][j][s] = sum_m Z[slot][j][m] wa[slot][s][m]
+// A warp takes 8 rows at a time: lane = (row jr, m-group mg of 4), so each
+// load instruction reads 8 row segments of 4 consecutive m (64 B each); the
+// four m-groups are reduced with two shuffle levels.
 template <int NR>
 __global__ void __launch_bounds__(256) k_green_vjp(int64_t N, int Mr, int S, SlotPtrs Z,
                                                    const cplx* __restrict__ wa, SlotPtrs x) {
@@ -275,34 +305,42 @@ __global__ void __launch_bounds__(256) k_green_vjp(int64_t N, int Mr, int S, Slo
   cplx* xs = x.p[slot];
   for (int e = threadIdx.x; e < S * Mr; e += blockDim.x) wsm[e] = wa[(int64_t)slot * S * Mr + e];
   __syncthreads();
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, jr = lane >> 2, mg = lane & 3;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t j = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); j < N; j += nw) {
+  for (int64_t j0 = (blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 8; j0 < N;
+       j0 += nw * 8) {
+    const int64_t j = j0 + jr;
     cplx acc[NR];
 #pragma unroll
     for (int s = 0; s < NR; ++s) acc[s] = cmk(0.0, 0.0);
-    for (int m = lane; m < Mr; m += 32) {
-      const cplx zv = __ldg(z + j * Mr + m);
+    if (j < N) {
+      const cplx* zp = z + j * Mr;
+#pragma unroll 5
+      for (int m = mg; m < Mr; m += 4) {
+        const cplx zv = __ldg(zp + m);
 #pragma unroll
-      for (int s = 0; s < NR; ++s)
-        if (s < S) acc[s] = cfma(zv, wsm[s * Mr + m], acc[s]);
+        for (int s = 0; s < NR; ++s)
+          if (s < S) acc[s] = cfma(zv, wsm[s * Mr + m], acc[s]);
+      }
     }
 #pragma unroll
     for (int s = 0; s < NR; ++s) {
       double a = acc[s].x, b = acc[s].y;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        a += __shfl_xor_sync(0xffffffffu, a, o);
-        b += __shfl_xor_sync(0xffffffffu, b, o);
-      }
+      a += __shfl_xor_sync(0xffffffffu, a, 1);
+      b += __shfl_xor_sync(0xffffffffu, b, 1);
+      a += __shfl_xor_sync(0xffffffffu, a, 2);
+      b += __shfl_xor_sync(0xffffffffu, b, 2);
       acc[s] = cmk(a, b);
     }
-    if (lane < NR) {
-      cplx v = cmk(0.0, 0.0);
+    if (j < N) {
 #pragma unroll
-      for (int s = 0; s < NR; ++s)
-        if (s == lane && s < S) v = acc[s];
-      xs[j * NR + lane] = v;
+      for (int s = mg; s < NR; s += 4) {
+        cplx v = cmk(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < NR; ++q)
+          if (q == s && q < S) v = acc[q];
+        xs[j * NR + s] = v;
+      }
     }
   }
 }
