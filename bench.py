@@ -237,6 +237,7 @@ def run_ours(args, world, rank):
         drv.data.d_obs = d_dev.cpu().numpy()
         drv.iterate(nu)
         out_host.copy_(torch.from_numpy(drv.model.m))
+        m_host.copy_(out_host)          # the caller feeds the updated model back
         e2e_steps.append((time.perf_counter() - ts) * 1e3)
     e3.record(stream)
     torch.cuda.synchronize()

@@ -86,6 +86,15 @@ struct rba_ctx {
   rba::GemmTask* gm_tasks = nullptr;
   std::vector<std::pair<int64_t, int>> fwd_lv, bwd_lv, fwdb_lv, bwdb_lv, small_lv;
   std::vector<int> small_mb;   // per level: pivot blocks of the largest warp-per-front front
+  // host copies for the pruned forward sweeps of the receiver-Green build
+  std::vector<int32_t> smallf_h;
+  std::vector<rba::SolveTask> ftb_h;
+  std::vector<int64_t> q_ptr_h;
+  std::vector<int32_t> q_col_h;
+  int prune_nb = 0;                                            // batch width of the lists
+  std::vector<std::pair<int64_t, int>> pr_small_lv, pr_fwdb_lv;  // [batch * nlevels + L]
+  int32_t* pr_small = nullptr;
+  rba::SolveTask* pr_fwdb = nullptr;
   rba::SolveTask *fwdb_tasks = nullptr, *bwdb_tasks = nullptr;
   int32_t* small_fronts = nullptr;
   rba::SolveTask *fwd_tasks = nullptr, *bwd_tasks = nullptr, *bwd_all = nullptr;
@@ -123,6 +132,7 @@ struct rba_ctx {
   std::vector<char> green_valid;
   cplx* green_part = nullptr;
   int green_chunks = 64;
+  bool green_prune = true;        // RBA_GREEN_PRUNE=0: full forward sweeps in the Z build
   int64_t n_green = 0;            // Z builds (slots)
   std::vector<int*> flf, flb, dnf, dnb;
   std::vector<int> slot_epoch;    // solves issued per local slot (flags / counters)
@@ -443,6 +453,9 @@ int build_plans(rba_ctx* c) {
   if ((rc = upload(c, c->allocs, &c->fwdb_tasks, ftb.data(), ftb.size()))) return rc;
   if ((rc = upload(c, c->allocs, &c->bwdb_tasks, btb.data(), btb.size()))) return rc;
   if ((rc = upload(c, c->allocs, &c->small_fronts, smallf.data(), smallf.size()))) return rc;
+  c->smallf_h = smallf;
+  c->ftb_h = ftb;
+  c->prune_nb = 0;
   {
     // fused backward: levels top-down in one task list
     std::vector<rba::SolveTask> ba;
@@ -682,7 +695,9 @@ int ensure_slots(rba_ctx* c) {
   return RBA_OK;
 }
 
-int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR) {
+// prune_b >= 0: forward sweep only over the fronts on the paths of receiver
+// batch prune_b (right-hand sides Q^T e_m are zero elsewhere; see build_prune)
+int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR, int prune_b = -1) {
   const int ns = (int)slots.size();
   if (ns == 0) return RBA_OK;
   rba::SolveBatch b;
@@ -730,17 +745,20 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR) {
   } else {
     for (int L = 0; L < S.nlevels; ++L) {
       Timed tl(c, 16 + std::min(L, 31), 0);
-      if (c->small_lv[L].second > 0) {
+      const bool pr = prune_b >= 0;
+      const auto sl = pr ? c->pr_small_lv[(size_t)prune_b * S.nlevels + L] : c->small_lv[L];
+      const auto fl = pr ? c->pr_fwdb_lv[(size_t)prune_b * S.nlevels + L] : c->fwdb_lv[L];
+      if (sl.second > 0) {
         Timed tm(c, KC_FWD);
-        rba::launch_solve_small(c->st, true, NR, c->small_fronts + c->small_lv[L].first,
-                                c->small_lv[L].second, ns, c->F, b, c->small_mb[L]);
+        rba::launch_solve_small(c->st, true, NR, (pr ? c->pr_small : c->small_fronts) + sl.first,
+                                sl.second, ns, c->F, b, c->small_mb[L]);
         CKL();
       }
-      if (c->fwdb_lv[L].second > 0) {
+      if (fl.second > 0) {
         Timed tm(c, KC_FWD);
         const int nfr_lv = S.level_ptr[L + 1] - S.level_ptr[L];
-        rba::launch_solve_level(c->st, true, NR, c->fwdb_tasks + c->fwdb_lv[L].first,
-                                c->fwdb_lv[L].second, ns, c->F, b, c->tickets + L, c->epoch,
+        rba::launch_solve_level(c->st, true, NR, (pr ? c->pr_fwdb : c->fwdb_tasks) + fl.first,
+                                fl.second, ns, c->F, b, c->tickets + L, c->epoch,
                                 c->parent_d, c->need_u_d, false, nfr_lv <= 2);
         CKL();
       }
@@ -906,6 +924,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     if (v == "v5") { c->panel_v = 5; c->panel_var = 0; }
   }
   if (const char* e = getenv("RBA_GREEN")) c->green_req = std::string(e) != "0";
+  if (const char* e = getenv("RBA_GREEN_PRUNE")) c->green_prune = std::string(e) != "0";
   if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) == "fused";
   if (const char* e = getenv("RBA_SMALLP")) c->small_p = std::string(e) == "64" ? rba::PB : 2 * rba::PB;
   if (const char* e = getenv("RBA_DIAG")) c->diag_v1 = std::string(e) == "v1";
@@ -1038,6 +1057,9 @@ int rba_set_observation(rba_ctx* c, int64_t Mr, const int64_t* qp, const int32_t
     return rc;
   c->S = 0;       // sources live in obs_allocs: set them again
   c->Fsrc = nullptr;
+  c->q_ptr_h = ptr;
+  c->q_col_h = col;
+  c->prune_nb = 0;
   return RBA_OK;
 }
 
@@ -1281,6 +1303,49 @@ static rba::SlotPtrs slot_sub(const std::vector<cplx*>& v, const std::vector<int
   return p;
 }
 
+// Forward-sweep pruning for the Z build: the right-hand sides of receiver
+// batch b (columns m0..m0+nb of Q^T) are nonzero only in the fronts holding
+// those receivers' dofs, so L^{-1} Q^T is nonzero only on the paths from those
+// fronts to the root (C4: ~25% of the factor bytes per batch of 4).
+static int build_prune(rba_ctx* c, int nb) {
+  const rba::Symbolic& S = c->sym;
+  std::vector<int32_t> fr_of(c->N, -1);
+  for (int s = 0; s < S.nfront; ++s)
+    for (int k = 0; k < S.npiv[s]; ++k) fr_of[S.first[s] + k] = s;
+  const int nbat = (int)((c->Mr + nb - 1) / nb);
+  std::vector<int32_t> ps;
+  std::vector<rba::SolveTask> pf;
+  c->pr_small_lv.assign((size_t)nbat * S.nlevels, {0, 0});
+  c->pr_fwdb_lv.assign((size_t)nbat * S.nlevels, {0, 0});
+  std::vector<char> act(S.nfront);
+  for (int b = 0; b < nbat; ++b) {
+    std::fill(act.begin(), act.end(), 0);
+    for (int64_t m = (int64_t)b * nb; m < std::min<int64_t>(c->Mr, (int64_t)(b + 1) * nb); ++m)
+      for (int64_t e = c->q_ptr_h[m]; e < c->q_ptr_h[m + 1]; ++e)
+        for (int s = fr_of[c->q_col_h[e]]; s >= 0 && !act[s]; s = S.parent[s]) act[s] = 1;
+    for (int L = 0; L < S.nlevels; ++L) {
+      const int64_t o1 = ps.size(), o2 = pf.size();
+      for (int q = 0; q < c->small_lv[L].second; ++q) {
+        const int32_t f = c->smallf_h[c->small_lv[L].first + q];
+        if (act[f]) ps.push_back(f);
+      }
+      for (int q = 0; q < c->fwdb_lv[L].second; ++q) {
+        const rba::SolveTask t = c->ftb_h[c->fwdb_lv[L].first + q];
+        if (act[t.s]) pf.push_back(t);
+      }
+      c->pr_small_lv[(size_t)b * S.nlevels + L] = {o1, (int)(ps.size() - o1)};
+      c->pr_fwdb_lv[(size_t)b * S.nlevels + L] = {o2, (int)(pf.size() - o2)};
+    }
+  }
+  int rc;
+  if (ps.empty()) ps.push_back(0);   // keep the device lists non-empty
+  if (pf.empty()) pf.push_back({0, 0});
+  if ((rc = upload(c, c->obs_allocs, &c->pr_small, ps.data(), ps.size()))) return rc;
+  if ((rc = upload(c, c->obs_allocs, &c->pr_fwdb, pf.data(), pf.size()))) return rc;
+  c->prune_nb = nb;
+  return RBA_OK;
+}
+
 // Build Z = A^{-1} Q^T for every local slot whose factor changed: Mr/NRw
 // multi-RHS solves over all such slots at once, columns stored row-major.
 static int ensure_green(rba_ctx* c) {
@@ -1295,14 +1360,20 @@ static int ensure_green(rba_ctx* c) {
   const int ns = (int)slots.size(), nb = c->NRw;
   const rba::SlotPtrs xs = slot_sub(c->x, slots), zs = slot_sub(c->Z, slots);
   int rc;
+  const bool prune = !c->fused_sweep && c->green_prune;
+  if (prune && c->prune_nb != nb && (rc = build_prune(c, nb))) return rc;
+  const rba::Symbolic& S = c->sym;
+  const size_t uvn = (size_t)std::max<int64_t>(S.uvec_off[S.nfront], 1) * c->NRw;
   for (int64_t m0 = 0; m0 < c->Mr; m0 += nb) {
     const int n = (int)std::min<int64_t>(nb, c->Mr - m0);
+    if (prune)   // skipped fronts must contribute zero u-vectors to active parents
+      for (int l : slots) CK(cudaMemsetAsync(c->uvec[l], 0, uvn * sizeof(cplx), c->st));
     {
       Timed t(c, KC_GREEN);
       rba::launch_green_rhs(c->st, ns, c->N, m0, n, nb, c->qt_ptr, c->qt_col, c->qt_val, xs);
     }
     CKL();
-    if ((rc = solve_slots(c, slots, nb))) return rc;
+    if ((rc = solve_slots(c, slots, nb, prune ? (int)(m0 / nb) : -1))) return rc;
     {
       Timed t(c, KC_GREEN);
       rba::launch_green_store(c->st, ns, c->N, c->Mr, m0, n, nb, xs, zs);
