@@ -40,6 +40,14 @@ __host__ __device__ __forceinline__ cplx cdiv(cplx a, cplx b) {
   }
 }
 __host__ __device__ __forceinline__ cplx cinv(cplx b) { return cdiv(cmk(1.0, 0.0), b); }
+// principal square root
+__host__ __device__ __forceinline__ cplx csqrt_c(cplx z) {
+  const double r = hypot(z.x, z.y);
+  if (r == 0.0) return cmk(0.0, 0.0);
+  const double s = sqrt(0.5 * (r + fabs(z.x)));
+  if (z.x >= 0.0) return cmk(s, z.y / (2.0 * s));
+  return cmk(fabs(z.y) / (2.0 * s), copysign(s, z.y));
+}
 
 __device__ __forceinline__ cplx ldg_c(const cplx* p) { return __ldg(p); }
 

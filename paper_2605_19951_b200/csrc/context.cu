@@ -139,7 +139,6 @@ struct rba_ctx {
   std::vector<char> valid;
   int NRw = 1;
   std::vector<cplx*> upd;
-  std::vector<cplx*> dvec;
   int fbatch = 1;
   cplx* wa = nullptr;
   cplx* stage = nullptr;
@@ -165,7 +164,7 @@ struct rba_ctx {
   // by rba_set_timing) and the launch count of this context's kernels
   double cls_ms[128] = {0};   // 0-15 kernel classes; 16+L fwd, 48+L bwd, 80+L factor per level
   bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernels
-  int gemm_v = 6;             // default 3M DMMA kernel (k_gemm6); RBA_GEMM=v1..v5 select
+  int gemm_v = 6;             // default 3M DMMA kernel (k_gemm6); RBA_GEMM=v3..v7b select
                               // the earlier kernels for A/B tests
   int small_p = 2 * rba::PB;  // warp-per-front solves up to this npiv (RBA_SMALLP=64|128)
   int gemm5_var = 6;          // v5/v6 stage shape (see launch_gemm5 / launch_gemm6); default
@@ -320,8 +319,7 @@ int build_plans(rba_ctx* c) {
         int s = S.level_fronts[q];
         if (S.npiv[s] <= k0) continue;
         int kb = std::min(rba::PB, S.npiv[s] - k0);
-        const int rstep = c->gemm_v == 2 ? 2 * rba::PB : rba::PB;
-        for (int r0 = k0 + kb; r0 < S.nf[s]; r0 += rstep) pt.push_back({s, k0, r0, 0});
+        for (int r0 = k0 + kb; r0 < S.nf[s]; r0 += rba::PB) pt.push_back({s, k0, r0, 0});
       }
       if ((int64_t)pt.size() > toff) c->plan.push_back({ST_TRSM, toff, (int)(pt.size() - toff), 0});
       // trailing update after block kk: inside a panel of `panel` blocks only
@@ -347,7 +345,7 @@ int build_plans(rba_ctx* c) {
         int ntr = (S.nf[s] - clo + rba::GT - 1) / rba::GT;
         int ntc = (chi - clo + rba::GT - 1) / rba::GT;
         int nt = 0;
-        for (int j = 0; j < ntc; ++j) nt += c->gemm_v == 2 ? (ntr - j + 1) / 2 : ntr - j;
+        for (int j = 0; j < ntc; ++j) nt += ntr - j;
         gm.push_back({s, t0, t1, clo, chi, tiles, ntr, 0});
         tiles += nt;
       }
@@ -362,10 +360,7 @@ int build_plans(rba_ctx* c) {
       if (nf <= p || p == 0) continue;
       int ntr = (nf - p + rba::GT - 1) / rba::GT;
       gm.push_back({s, 0, p, p, nf, tiles, ntr, 0});
-      if (c->gemm_v == 2)
-        for (int j = 0; j < ntr; ++j) tiles += (ntr - j + 1) / 2;
-      else
-        tiles += ntr * (ntr + 1) / 2;
+      tiles += ntr * (ntr + 1) / 2;
     }
     if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles, 1});
     for (size_t q = plan0; q < c->plan.size(); ++q) c->plan[q].level = L;
@@ -521,12 +516,8 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
         Timed t(c, KC_TRSM);
         if (c->gemm_dfma)
           rba::launch_trsm(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
-        else if (c->gemm_v == 1)
-          rba::launch_trsm_dmma(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
-        else if (c->gemm_v == 3 || c->gemm_v >= 5)
-          rba::launch_trsm3(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->gemm_var);
         else
-          rba::launch_trsm2(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
+          rba::launch_trsm3(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->gemm_var);
         break;
       }
       case ST_GEMM: {
@@ -543,18 +534,14 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
         }
         if (c->gemm_dfma)
           rba::launch_gemm_update(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
-        else if (c->gemm_v == 1)
-          rba::launch_gemm_dmma(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
         else if (c->gemm_v == 3)
           rba::launch_gemm3(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->gemm_var);
         else if (c->gemm_v == 5)
           rba::launch_gemm5(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros,
                             c->gemm5_var);
-        else if (c->gemm_v == 6)
+        else
           rba::launch_gemm6(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros,
                             c->gemm5_var);
-        else
-          rba::launch_gemm2(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
         break;
       }
     }
@@ -674,11 +661,7 @@ int ensure_slots(rba_ctx* c) {
     if ((rc = dalloc(c, c->pole_allocs, &pool, c->green ? std::max(arenas, zall) : arenas, &c->mem_work)))
       return rc;
     c->upd.assign(c->fbatch, nullptr);
-    c->dvec.assign(c->fbatch, nullptr);
-    for (int b = 0; b < c->fbatch; ++b) {
-      c->upd[b] = pool + (size_t)b * S.upd_total;
-      if ((rc = dalloc(c, c->pole_allocs, &c->dvec[b], (size_t)S.n, &c->mem_work))) return rc;
-    }
+    for (int b = 0; b < c->fbatch; ++b) c->upd[b] = pool + (size_t)b * S.upd_total;
     c->Z.assign(nl, nullptr);
     c->green_valid.assign(nl, 0);
     if (c->green) {
@@ -902,8 +885,6 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   for (auto& e : c->ev) cudaEventCreate(&e);
   if (const char* e = getenv("RBA_GEMM")) {
     c->gemm_dfma = std::string(e) == "dfma";
-    if (std::string(e) == "v1" || c->gemm_dfma) c->gemm_v = 1;
-    if (std::string(e) == "v2") c->gemm_v = 2;
     if (std::string(e) == "v3") { c->gemm_v = 3; c->gemm_var = 0; }
     if (std::string(e) == "v4") { c->gemm_v = 3; c->gemm_var = 1; }
     if (std::string(e) == "v5") { c->gemm_v = 5; c->gemm_var = 1; c->gemm5_var = 0; }
@@ -1162,7 +1143,6 @@ int rba_factor(rba_ctx* c) {
       pb.factor[i] = c->factor[l];
       pb.tmap[i] = c->tmaps[l];
       pb.upd[i] = c->upd[i];
-      pb.dvec[i] = c->dvec[i];
       pb.xi[i] = c->poles_h[c->local[l]];
       CK(cudaMemsetAsync(c->factor[l], 0, S.panel_off[S.nfront] * sizeof(cplx), c->st));
     }
@@ -1203,7 +1183,6 @@ int rba_factor_values(rba_ctx* c, int32_t slot, const double* vals) {
   pb.factor[0] = c->factor[slot];
   pb.tmap[0] = c->tmaps[slot];
   pb.upd[0] = c->upd[0];
-  pb.dvec[0] = c->dvec[0];
   pb.xi[0] = rba::cmk(0.0, 0.0);
   c->valid[slot] = 0;
   for (auto& v : c->green_valid) v = 0;   // the update arenas overlay Z

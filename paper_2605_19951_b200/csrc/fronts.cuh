@@ -34,11 +34,20 @@ struct PoleBatch {
   const TMap* tmap[32]; // per slot: tensor maps of the slot's factor panels (or null)
   cplx* factor[32];     // per slot: factor storage base
   cplx* upd[32];        // per slot: update arena base
-  cplx* dvec[32];       // per slot: pivots d in global pivot order (contiguous copy of the diagonal)
   cplx xi[32];          // per slot: pole value
   int32_t count;
 };
 
+// Factor format (per front panel, column-major nf x npiv): A_front = L' L'^T
+// with L' = L D^{1/2} (complex-symmetric LDL^T with the pivot square roots
+// folded into the columns, so no GEMM carries a d scaling):
+//   * rows below a column's 64-pivot diagonal block: L'[r,c] = L[r,c] s_c
+//   * diagonal slot: s_c = sqrt(d_c) (principal root)
+//   * strictly lower part of each 64x64 diagonal block: unit L_bb
+//   * strictly upper part of each diagonal block: X = L_bb^{-1}, transposed
+//     (X[i][j], i > j, stored at (row j, col i))
+// Block forms: y_b = S_b^{-1} X_b (v_b - sum L'_bj y_j);
+//              x_b = X_b^T S_b^{-1} (y_b - sum L'_rb^T x_r).
 constexpr int PB = 64;   // pivot block (factorisation) and solve row block
 constexpr int GT = 64;   // GEMM tile (complex)
 

@@ -41,14 +41,6 @@ void launch_trsm(cudaStream_t st, const PanelTask* tasks, int ntasks, const Fron
                  const PoleBatch& pb);
 void launch_gemm_update(cudaStream_t st, const GemmTask* tasks, int ntasks, int ntiles,
                         const FrontsDev& F, const PoleBatch& pb);
-void launch_gemm_dmma(cudaStream_t st, const GemmTask* tasks, int ntasks, int ntiles,
-                      const FrontsDev& F, const PoleBatch& pb);
-void launch_trsm_dmma(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
-                      const PoleBatch& pb);
-void launch_gemm2(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
-                  const FrontsDev& F, const PoleBatch& pb);
-void launch_trsm2(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
-                  const PoleBatch& pb);
 void launch_gemm3(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
                   const FrontsDev& F, const PoleBatch& pb, int variant);
 void launch_gemm5(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,

@@ -196,11 +196,12 @@ __global__ void __launch_bounds__(256) k_diag(const PanelTask* __restrict__ task
     }
   }
   __syncthreads();
+  // diagonal slot: s_j = sqrt(d_j) (factor format, see fronts.cuh)
   for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
     int i = idx % kb, j = idx / kb;
-    panel[(int64_t)(k0 + j) * nf + k0 + i] = i >= j ? Dg[i * LDS + j] : Xs[j * LDS + i];
+    panel[(int64_t)(k0 + j) * nf + k0 + i] =
+        i > j ? Dg[i * LDS + j] : (i == j ? csqrt_c(Dg[i * LDS + i]) : Xs[j * LDS + i]);
   }
-  if (tid < kb) pb.dvec[slot][F.first[s] + k0 + tid] = Dg[tid * LDS + tid];
 }
 
 // K4a (v2): the same diagonal-block LDL^T + inverse, blocked by 16 so that
@@ -318,11 +319,11 @@ __global__ void __launch_bounds__(256) k_diag2(const PanelTask* __restrict__ tas
     }
     __syncthreads();
   }
+  // diagonal slot: s_j = sqrt(d_j) (factor format, see fronts.cuh)
   for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
     int i = idx % kb, j = idx / kb;
-    panel[(int64_t)(k0 + j) * nf + k0 + i] = Dg[i * LDS + j];
+    panel[(int64_t)(k0 + j) * nf + k0 + i] = i == j ? csqrt_c(Dg[i * LDS + j]) : Dg[i * LDS + j];
   }
-  if (tid < kb) pb.dvec[slot][F.first[s] + k0 + tid] = Dg[tid * LDS + tid];
 }
 
 void launch_diag2(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
@@ -404,7 +405,7 @@ void launch_trsm(cudaStream_t st, const PanelTask* tasks, int ntasks, const Fron
 }
 
 // ---------------------------------------------------------------------------
-// K4b: trailing update  C[r,c] -= sum_t L[r,t] d_t L[c,t]  (r >= c), one
+// K4b: trailing update  C[r,c] -= sum_t L'[r,t] L'[c,t]  (r >= c), one
 // 64x64 complex tile per CTA, tiles listed per task (front, k-range, column
 // range).  v1: DFMA register tiling (4x4 complex per thread).
 // ---------------------------------------------------------------------------
@@ -423,7 +424,6 @@ __global__ void __launch_bounds__(256) k_gemm_update(const GemmTask* __restrict_
                                                      FrontsDev F, PoleBatch pb) {
   __shared__ cplx As[KC][GT];
   __shared__ cplx Bs[KC][GT];
-  __shared__ cplx ds[KC];
   const int slot = blockIdx.y;
   const int ti = find_task(tasks, ntasks, blockIdx.x);
   const GemmTask tk = tasks[ti];
@@ -445,17 +445,13 @@ __global__ void __launch_bounds__(256) k_gemm_update(const GemmTask* __restrict_
     for (int b = 0; b < 4; ++b) acc[a][b] = cmk(0.0, 0.0);
   for (int kt = tk.t0; kt < tk.t1; kt += KC) {
     const int kn = min(KC, tk.t1 - kt);
-    if (threadIdx.x < KC) {
-      ds[threadIdx.x] = threadIdx.x < kn ? panel[(int64_t)(kt + threadIdx.x) * nf + kt + threadIdx.x]
-                                         : cmk(0.0, 0.0);
-    }
     __syncthreads();
     for (int idx = threadIdx.x; idx < KC * GT; idx += 256) {
       const int rr = idx % GT, kk = idx / GT;
       cplx a = cmk(0.0, 0.0), b = cmk(0.0, 0.0);
       if (kk < kn) {
         const cplx* col = panel + (int64_t)(kt + kk) * nf;
-        if (r0 + rr < nf) a = cmul(col[r0 + rr], ds[kk]);
+        if (r0 + rr < nf) a = col[r0 + rr];
         if (cc0 + rr < cmax) b = col[cc0 + rr];
       }
       As[kk][rr] = a;

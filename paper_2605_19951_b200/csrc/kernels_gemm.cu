@@ -1,15 +1,14 @@
-// K4b on the FP64 tensor cores: complex trailing / Schur update of the fronts
-//     C[r,c] -= sum_t (L[r,t] d_t) L[c,t]        (lower triangle, r >= c)
-// with warp-level DMMA (mma.sync.m8n8k4.f64 -> SASS DMMA.8 on sm_100a; the
-// tcgen05 UMMA has no f64 kind).  A complex product is four real
-// DMMAs on split re/im planes: Cre += Are*Bre - Aim*Bim, Cim += Are*Bim + Aim*Bre.
-//
-// CTA tile 64x64 complex, 4 warps each 32x32 (4x4 DMMA tiles x {re,im}).
-// K is staged in chunks of 16 through shared memory in [row][k] planes padded
-// to 20 doubles (conflict-free 8-byte fragment loads), with a register
-// prefetch of the next chunk (software pipeline) and the d_t scaling of the A
-// operand fused into the staging.  Tiles are listed per task exactly as the
-// DFMA reference kernel (k_gemm_update) and both share FrontsDev addressing.
+// K4 on the FP64 tensor cores: the panel TRSM and the complex trailing / Schur
+// update of the fronts
+//     C[r,c] -= sum_t L'[r,t] L'[c,t]        (lower triangle, r >= c)
+// with L' = L D^{1/2} (factor format, fronts.cuh), using warp-level DMMA
+// (mma.sync.m8n8k4.f64 -> SASS DMMA.8 on sm_100a; the tcgen05 UMMA has no f64
+// kind).  Kernels: v3 (k_gemm3: cp.async pipeline; MODE 1 is the
+// default TRSM), v5 (k_gemm5: bulk copies into an mbarrier ring, 4-multiply
+// complex products), v6/v8 (k_gemm6: 3-multiply complex products, v8 = TMA
+// tensor-map operands, the default update).  All tile lists come from the
+// same GemmTask / PanelTask descriptors as the DFMA reference kernel
+// (kernels_factor.cu, k_gemm_update).
 #include "fronts.cuh"
 #include "kernels.h"
 
@@ -18,10 +17,6 @@
 namespace rba {
 
 namespace {
-constexpr int TK = 16;          // k-chunk (complex)
-constexpr int LDK = TK + 4;     // padded row stride of the smem planes (doubles)
-constexpr int NT = 128;         // threads per CTA
-
 __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
@@ -37,471 +32,8 @@ __device__ __forceinline__ int find_task(const GemmTask* tasks, int n, int b) {
   return lo;
 }
 
-struct Stage {
-  double are[GT * LDK], aim[GT * LDK], bre[GT * LDK], bim[GT * LDK];
-};
 }  // namespace
 
-// MODE 0: trailing/Schur update  C[r,c] -= sum_t (L[r,t] d_t) L[c,t]  (r >= c)
-// MODE 1: panel TRSM  L[r, k0+c] = (sum_{t<=c} F[r, k0+t] X[c][t]) / d_c, with
-//         X = L_kk^{-1} read from the diagonal block's upper triangle (k_diag).
-template <int MODE, int NW>
-__global__ void __launch_bounds__(32 * NW) k_gemm_dmma(const GemmTask* __restrict__ tasks, int ntasks,
-                                                  const PanelTask* __restrict__ ptasks,
-                                                  FrontsDev F, PoleBatch pb) {
-  extern __shared__ __align__(16) double smraw[];
-  Stage* st = reinterpret_cast<Stage*>(smraw);     // st[0], st[1]
-  __shared__ cplx ds[2][TK];
-  __shared__ cplx dinv[GT];
-  const int slot = blockIdx.y;
-  GemmTask tk;
-  int r0, cc0, cmax, kbase = 0;
-  if (MODE == 0) {
-    const int ti = find_task(tasks, ntasks, blockIdx.x);
-    tk = tasks[ti];
-    int local = blockIdx.x - tk.tile_start;
-    int j = 0;
-    while (local >= tk.ntr - j) { local -= tk.ntr - j; ++j; }
-    const int i = j + local;
-    r0 = tk.c_lo + i * GT;
-    cc0 = tk.c_lo + j * GT;
-    cmax = min(cc0 + GT, tk.c_hi);
-  } else {
-    const PanelTask pt = ptasks[blockIdx.x];
-    const int p_ = F.npiv[pt.s];
-    tk.s = pt.s;
-    tk.t0 = 0;
-    tk.t1 = min(GT, p_ - pt.k0);         // kb
-    kbase = pt.k0;
-    r0 = pt.r0;
-    cc0 = 0;
-    cmax = tk.t1;
-  }
-  const int s = tk.s;
-  const int nf = F.nf[s], p = F.npiv[s];
-  const cplx* __restrict__ panel = pb.factor[slot] + F.panel_off[s];
-  cplx* pw = pb.factor[slot] + F.panel_off[s];
-  cplx* upd = pb.upd[slot] + (F.upd_off[s] >= 0 ? F.upd_off[s] : 0);
-  constexpr int NTH = 32 * NW;            // threads
-  constexpr int NB = NW == 4 ? 4 : 2;      // 8-wide n-tiles per warp (32 or 16 columns)
-  constexpr int PER = (GT * TK) / NTH;     // staged elements per thread per operand
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * (8 * NB);   // warp tile origin
-  const int g = lane >> 2, t4 = lane & 3;
-
-  // accumulators: [mi][ni] 8x8 tiles, re and im, 2 doubles each
-  double cre[4][NB][2], cim[4][NB][2];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      cre[a][b][0] = cre[a][b][1] = 0.0;
-      cim[a][b][0] = cim[a][b][1] = 0.0;
-    }
-
-  // staging: each thread loads 8 A and 8 B complex per chunk:
-  // element e = tid + q*NT (q < 8) -> row = e % 64, k = e / 64
-  cplx pa[PER], pbv[PER];
-  auto gload = [&](int kt) {
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int e = tid + q * NTH;
-      const int rr = e & (GT - 1), kk = e >> 6;
-      const int t = kt + kk;
-      cplx a = cmk(0.0, 0.0), b = cmk(0.0, 0.0);
-      if (t < tk.t1) {
-        if (MODE == 0) {
-          const cplx* col = panel + (int64_t)t * nf;
-          if (r0 + rr < nf) a = __ldg(col + r0 + rr);
-          if (cc0 + rr < cmax) b = __ldg(col + cc0 + rr);
-        } else {
-          // A = F[r0+rr, kbase+t]; B[c=rr][t] = X[c][t] (t < c), 1 (t == c), 0 (t > c)
-          if (r0 + rr < nf) a = __ldg(panel + (int64_t)(kbase + t) * nf + r0 + rr);
-          if (rr < cmax) {
-            if (t < rr) b = __ldg(panel + (int64_t)(kbase + rr) * nf + kbase + t);
-            else if (t == rr) b = cmk(1.0, 0.0);
-          }
-        }
-      }
-      pa[q] = a;
-      pbv[q] = b;
-    }
-  };
-  auto dload = [&](int kt, int buf) {
-    if (tid < TK) {
-      const int t = kt + tid;
-      ds[buf][tid] = MODE == 1 ? cmk(1.0, 0.0)
-                   : (t < tk.t1 ? __ldg(panel + (int64_t)t * nf + t) : cmk(0.0, 0.0));
-    }
-  };
-  if (MODE == 1 && tid < GT) {
-    dinv[tid] = tid < cmax ? cinv(__ldg(panel + (int64_t)(kbase + tid) * nf + kbase + tid))
-                           : cmk(0.0, 0.0);
-  }
-  auto sstore = [&](int buf) {
-    Stage& S = st[buf];
-#pragma unroll
-    for (int q = 0; q < PER; ++q) {
-      const int e = tid + q * NTH;
-      const int rr = e & (GT - 1), kk = e >> 6;
-      const cplx a = cmul(pa[q], ds[buf][kk]);
-      S.are[rr * LDK + kk] = a.x;
-      S.aim[rr * LDK + kk] = a.y;
-      S.bre[rr * LDK + kk] = pbv[q].x;
-      S.bim[rr * LDK + kk] = pbv[q].y;
-    }
-  };
-
-  const int nchunks = (tk.t1 - tk.t0 + TK - 1) / TK;
-  dload(tk.t0, 0);
-  gload(tk.t0);
-  __syncthreads();
-  sstore(0);
-  __syncthreads();
-  for (int ch = 0; ch < nchunks; ++ch) {
-    const int buf = ch & 1;
-    const bool more = ch + 1 < nchunks;
-    if (more) {
-      dload(tk.t0 + (ch + 1) * TK, buf ^ 1);
-      gload(tk.t0 + (ch + 1) * TK);
-    }
-    const Stage& S = st[buf];
-#pragma unroll
-    for (int k4 = 0; k4 < TK; k4 += 4) {
-      double ar[4], ai[4], an[4], br[NB], bi[NB];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const int idx = (wm + a * 8 + g) * LDK + k4 + t4;
-        ar[a] = S.are[idx];
-        ai[a] = S.aim[idx];
-        an[a] = -ai[a];
-      }
-#pragma unroll
-      for (int b = 0; b < NB; ++b) {
-        const int idx = (wn + b * 8 + g) * LDK + k4 + t4;
-        br[b] = S.bre[idx];
-        bi[b] = S.bim[idx];
-      }
-      // four passes of independent DMMAs: back-to-back MMAs never share an
-      // accumulator (the DMMA result latency would stall the warp otherwise)
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < NB; ++b) dmma(cre[a][b][0], cre[a][b][1], ar[a], br[b]);
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < NB; ++b) dmma(cim[a][b][0], cim[a][b][1], ar[a], bi[b]);
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < NB; ++b) dmma(cre[a][b][0], cre[a][b][1], an[a], bi[b]);
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < NB; ++b) dmma(cim[a][b][0], cim[a][b][1], ai[a], br[b]);
-    }
-    if (more) {
-      __syncthreads();            // ds[buf^1] visible; st[buf^1] free (read 2 chunks ago)
-      sstore(buf ^ 1);
-    }
-    __syncthreads();
-  }
-  if (MODE == 0) {
-    // epilogue: C -= acc  (lower triangle only).  The 8 C values of one
-    // m-tile row are loaded together before any store (the stores may alias
-    // later loads as far as the compiler knows: batching avoids 32 serial
-    // round trips per thread).
-#pragma unroll
-    for (int a = 0; a < 4; ++a) {
-      cplx* dst[NB][2];
-      cplx cv[NB][2];
-#pragma unroll
-      for (int b = 0; b < NB; ++b)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int r = r0 + wm + a * 8 + g;
-          const int c = cc0 + wn + b * 8 + t4 * 2 + h;
-          dst[b][h] = (r < nf && c < cmax && r >= c) ? faddr(pw, upd, p, nf, r, c) : nullptr;
-          cv[b][h] = dst[b][h] ? __ldcg(dst[b][h]) : cmk(0.0, 0.0);
-        }
-#pragma unroll
-      for (int b = 0; b < NB; ++b)
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-          if (dst[b][h]) *dst[b][h] = cmk(cv[b][h].x - cre[a][b][h], cv[b][h].y - cim[a][b][h]);
-    }
-  } else {
-    // epilogue: L = (F X^T) D^{-1}, written in place (every A element of this
-    // tile was staged before any write: the K loop ended with a barrier)
-#pragma unroll
-    for (int a = 0; a < 4; ++a)
-#pragma unroll
-      for (int b = 0; b < NB; ++b)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int r = r0 + wm + a * 8 + g;
-          const int c = wn + b * 8 + t4 * 2 + h;
-          if (r < nf && c < cmax)
-            pw[(int64_t)(kbase + c) * nf + r] = cmul(cmk(cre[a][b][h], cim[a][b][h]), dinv[c]);
-        }
-  }
-}
-
-int g_dmma_warps = 4;   // RBA_GEMM_WARPS=8 selects 32x16 warp tiles (8 warps/CTA)
-
-void launch_gemm_dmma(cudaStream_t st, const GemmTask* tasks, int ntasks, int ntiles,
-                      const FrontsDev& F, const PoleBatch& pb) {
-  if (ntasks <= 0 || ntiles <= 0) return;
-  const size_t smem = 2 * sizeof(Stage);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gemm_dmma<0, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(k_gemm_dmma<0, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (const char* e = getenv("RBA_GEMM_WARPS")) g_dmma_warps = atoi(e) == 8 ? 8 : 4;
-    attr = true;
-  }
-  dim3 grid(ntiles, pb.count);
-  if (g_dmma_warps == 8)
-    k_gemm_dmma<0, 8><<<grid, 256, smem, st>>>(tasks, ntasks, nullptr, F, pb);
-  else
-    k_gemm_dmma<0, 4><<<grid, 128, smem, st>>>(tasks, ntasks, nullptr, F, pb);
-}
-
-void launch_trsm_dmma(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
-                      const PoleBatch& pb) {
-  if (ntasks <= 0) return;
-  const size_t smem = 2 * sizeof(Stage);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gemm_dmma<1, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  dim3 grid(ntasks, pb.count);
-  k_gemm_dmma<1, 4><<<grid, 128, smem, st>>>(nullptr, 0, tasks, F, pb);
-}
-
-
-// ---------------------------------------------------------------------------
-// v2: 128x64 CTA tile (8 warps, 32x32 each), interleaved complex [row][k]
-// shared-memory tiles filled by cp.async (16 B, zero-fill out of range) in a
-// 3-stage pipeline with one barrier per stage; one LDS.128 yields both the re
-// and im DMMA fragments.  The d_t scaling (MODE 0) and the unit-triangular
-// mask of X (MODE 1) are applied to the B fragments in registers.
-// ---------------------------------------------------------------------------
-namespace {
-constexpr int T2K = 8;             // k per stage (complex)
-constexpr int L2K = T2K + 4;       // padded row stride (complex): 12 x 16 B -> conflict-free
-constexpr int NS2 = 4;             // pipeline stages
-constexpr int BM2 = 128, BN2 = 64;
-constexpr int NT2 = 256;
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  const int sz = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz)
-               : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
-struct Stage2 {
-  cplx a[BM2 * L2K];
-  cplx b[BN2 * L2K];
-  cplx d[T2K];
-};
-}  // namespace
-
-template <int MODE>
-__global__ void __launch_bounds__(NT2, 1) k_gemm2(const GemmTask* __restrict__ tasks, int ntasks,
-                                                  const PanelTask* __restrict__ ptasks,
-                                                  FrontsDev F, PoleBatch pb) {
-  extern __shared__ __align__(16) unsigned char smraw2[];
-  Stage2* st = reinterpret_cast<Stage2*>(smraw2);
-  __shared__ cplx dinv[BN2];
-  const int slot = blockIdx.y;
-  int s, t0, t1, r0, cc0, cmax, kbase = 0;
-  if (MODE == 0) {
-    const int ti = find_task(tasks, ntasks, blockIdx.x);
-    const GemmTask tk = tasks[ti];
-    int local = blockIdx.x - tk.tile_start;
-    int j = 0;
-    // column tile j holds ceil((ntr - j) / 2) CTAs of two stacked 64-row tiles
-    while (local >= (tk.ntr - j + 1) / 2) { local -= (tk.ntr - j + 1) / 2; ++j; }
-    const int i = j + 2 * local;
-    s = tk.s; t0 = tk.t0; t1 = tk.t1;
-    r0 = tk.c_lo + i * GT;
-    cc0 = tk.c_lo + j * GT;
-    cmax = min(cc0 + GT, tk.c_hi);
-  } else {
-    const PanelTask pt = ptasks[blockIdx.x];
-    s = pt.s;
-    t0 = 0;
-    t1 = min(GT, F.npiv[s] - pt.k0);
-    kbase = pt.k0;
-    r0 = pt.r0;
-    cc0 = 0;
-    cmax = t1;
-  }
-  const int nf = F.nf[s], p = F.npiv[s];
-  const cplx* __restrict__ panel = pb.factor[slot] + F.panel_off[s];
-  cplx* pw = pb.factor[slot] + F.panel_off[s];
-  cplx* upd = pb.upd[slot] + (F.upd_off[s] >= 0 ? F.upd_off[s] : 0);
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = (warp & 3) * 32, wn = (warp >> 2) * 32;
-  const int g = lane >> 2, t4 = lane & 3;
-
-  double cre[4][4][2], cim[4][4][2];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      cre[a][b][0] = cre[a][b][1] = 0.0;
-      cim[a][b][0] = cim[a][b][1] = 0.0;
-    }
-  if (MODE == 1 && tid < BN2)
-    dinv[tid] = tid < cmax ? cinv(__ldg(panel + (int64_t)(kbase + tid) * nf + kbase + tid))
-                           : cmk(0.0, 0.0);
-
-  const int nchunks = (t1 - t0 + T2K - 1) / T2K;
-  auto issue = [&](int ch) {
-    if (ch < nchunks) {
-      Stage2& S = st[ch % NS2];
-      const int kt = t0 + ch * T2K;
-#pragma unroll
-      for (int q = 0; q < (BM2 * T2K) / NT2; ++q) {
-        const int e = tid + q * NT2;
-        const int rr = e % BM2, kk = e / BM2;
-        const int t = kt + kk;
-        const int row = r0 + rr;
-        const bool ok = t < t1 && row < nf;
-        const int64_t col = MODE == 0 ? (int64_t)t : (int64_t)(kbase + t);
-        cp_async16(&S.a[rr * L2K + kk], panel + (ok ? col * nf + row : 0), ok);
-      }
-#pragma unroll
-      for (int q = 0; q < (BN2 * T2K) / NT2; ++q) {
-        const int e = tid + q * NT2;
-        const int rr = e % BN2, kk = e / BN2;
-        const int t = kt + kk;
-        bool ok;
-        const cplx* src;
-        if (MODE == 0) {
-          ok = t < t1 && cc0 + rr < cmax;
-          src = panel + (ok ? (int64_t)t * nf + cc0 + rr : 0);
-        } else {
-          // X[c][t] at (row kbase+t, col kbase+c); masked to t < c in registers
-          ok = t < t1 && rr < cmax;
-          src = panel + (ok ? (int64_t)(kbase + rr) * nf + kbase + t : 0);
-        }
-        cp_async16(&S.b[rr * L2K + kk], src, ok);
-      }
-      if (MODE == 0 && tid < T2K) {
-        const int t = kt + tid;
-        S.d[tid] = t < t1 ? __ldg(panel + (int64_t)t * nf + t) : cmk(0.0, 0.0);
-      }
-    }
-    cp_commit();
-  };
-  for (int c = 0; c < NS2 - 1; ++c) issue(c);
-  for (int ch = 0; ch < nchunks; ++ch) {
-    cp_wait<NS2 - 2>();
-    __syncthreads();
-    issue(ch + NS2 - 1);
-    const Stage2& S = st[ch % NS2];
-    const int kt = t0 + ch * T2K;
-#pragma unroll
-    for (int k4 = 0; k4 < T2K; k4 += 4) {
-      double ar[4], ai[4], an[4], br[4], bi[4];
-#pragma unroll
-      for (int a = 0; a < 4; ++a) {
-        const cplx v = S.a[(wm + a * 8 + g) * L2K + k4 + t4];
-        ar[a] = v.x;
-        ai[a] = v.y;
-        an[a] = -v.y;
-      }
-#pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        cplx v = S.b[(wn + b * 8 + g) * L2K + k4 + t4];
-        if (MODE == 0) {
-          v = cmul(v, S.d[k4 + t4]);
-        } else {
-          const int c = wn + b * 8 + g, t = kt + k4 + t4;
-          v = t < c ? v : (t == c ? cmk(1.0, 0.0) : cmk(0.0, 0.0));
-        }
-        br[b] = v.x;
-        bi[b] = v.y;
-      }
-      // four passes of independent DMMAs: back-to-back MMAs never share an
-      // accumulator (the DMMA result latency would stall the warp otherwise)
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) dmma(cre[a][b][0], cre[a][b][1], ar[a], br[b]);
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) dmma(cim[a][b][0], cim[a][b][1], ar[a], bi[b]);
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) dmma(cre[a][b][0], cre[a][b][1], an[a], bi[b]);
-#pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) dmma(cim[a][b][0], cim[a][b][1], ai[a], br[b]);
-    }
-  }
-  cp_wait<0>();
-  __syncthreads();
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int r = r0 + wm + a * 8 + g;
-        const int c = cc0 + wn + b * 8 + t4 * 2 + h;
-        if (MODE == 0) {
-          if (r < nf && c < cmax && r >= c) {
-            cplx* dst = faddr(pw, upd, p, nf, r, c);
-            cplx v = *dst;
-            v.x -= cre[a][b][h];
-            v.y -= cim[a][b][h];
-            *dst = v;
-          }
-        } else {
-          if (r < nf && c < cmax)
-            pw[(int64_t)(kbase + c) * nf + r] = cmul(cmk(cre[a][b][h], cim[a][b][h]), dinv[c]);
-        }
-      }
-}
-
-void launch_gemm2(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
-                  const FrontsDev& F, const PoleBatch& pb) {
-  if (ntasks <= 0 || nctas <= 0) return;
-  const size_t smem = NS2 * sizeof(Stage2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gemm2<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  dim3 grid(nctas, pb.count);
-  k_gemm2<0><<<grid, NT2, smem, st>>>(tasks, ntasks, nullptr, F, pb);
-}
-
-void launch_trsm2(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
-                  const PoleBatch& pb) {
-  if (ntasks <= 0) return;
-  const size_t smem = NS2 * sizeof(Stage2);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_gemm2<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
-  dim3 grid(ntasks, pb.count);
-  k_gemm2<1><<<grid, NT2, smem, st>>>(nullptr, 0, tasks, F, pb);
-}
 // ---------------------------------------------------------------------------
 // v3: 64x64 CTA tile, 8 warps of 32x16 (<=128 registers: 2 CTAs = 16 warps/SM), interleaved complex [row][k]
 // shared-memory tiles filled by cp.async (16 B, zero-fill out of range) in a
@@ -530,7 +62,6 @@ struct Stage3 {
   static constexpr int L3K = T3K + 4;
   cplx a[BM3 * L3K];
   cplx b[BN3 * L3K];
-  cplx d[T3K];
 };
 }  // namespace
 
@@ -618,10 +149,6 @@ __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ t
         }
         cp_async16_3(&S.b[rr * L3K + kk], src, ok);
       }
-      if (MODE == 0 && tid < T3K) {
-        const int t = kt + tid;
-        S.d[tid] = t < t1 ? __ldg(panel + (int64_t)t * nf + t) : cmk(0.0, 0.0);
-      }
     }
     cp_commit3();
   };
@@ -645,9 +172,7 @@ __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ t
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
         cplx v = S.b[(wn + b * 8 + g) * L3K + k4 + t4];
-        if (MODE == 0) {
-          v = cmul(v, S.d[k4 + t4]);
-        } else {
+        if (MODE == 1) {
           const int c = wn + b * 8 + g, t = kt + k4 + t4;
           v = t < c ? v : (t == c ? cmk(1.0, 0.0) : cmk(0.0, 0.0));
         }
@@ -767,7 +292,6 @@ template <int G5K>          // k per stage (complex)
 struct Stage5 {
   cplx a[G5K * G5LD];
   cplx b[G5K * G5LD];
-  cplx d[G5K];
 };
 
 }  // namespace
@@ -802,20 +326,14 @@ __global__ void __launch_bounds__(32 * G5W, 2) k_gemm5(const GemmTask* __restric
   const int nchunks = (t1 - t0 + G5K - 1) / G5K;
   const unsigned na = (unsigned)min(GT, nf - r0) * 16u;     // valid A rows (bytes)
   const unsigned nb = (unsigned)min(GT, nf - cc0) * 16u;    // valid B rows (bytes)
-  const cplx* __restrict__ dvec = pb.dvec[slot] + F.first[s];   // d of this front's pivots
-
   // one warp: lane 0 arms stage ch % NS, the lanes split the copies of chunk ch
   auto issue = [&](int ch) {
     St& S = st[ch % NS];
     const unsigned bar = smem_u32(&full[ch % NS]);
     const int kt = t0 + ch * G5K;
     const int nval = max(0, min(G5K, t1 - kt));
-    if (lane == 0) {
-      mbar_expect_tx(bar, (unsigned)nval * (na + nb) + (unsigned)(G5K - nval) * 2048u +
-                              (unsigned)G5K * 16u);
-      if (nval > 0) bulk_g2s(smem_u32(&S.d[0]), dvec + kt, (unsigned)nval * 16u, bar);
-      if (nval < G5K) bulk_g2s(smem_u32(&S.d[nval]), zeros, (unsigned)(G5K - nval) * 16u, bar);
-    }
+    if (lane == 0)
+      mbar_expect_tx(bar, (unsigned)nval * (na + nb) + (unsigned)(G5K - nval) * 2048u);
     for (int q = lane; q < 2 * G5K; q += 32) {
       const int kk = q >> 1;
       const int t = kt + kk;
@@ -859,10 +377,9 @@ __global__ void __launch_bounds__(32 * G5W, 2) k_gemm5(const GemmTask* __restric
         ar[a] = v.x;
         ai[a] = v.y;
       }
-      const cplx dk = S.d[k4 + t4];
 #pragma unroll
       for (int b = 0; b < 2; ++b) {
-        const cplx v = cmul(S.b[(k4 + t4) * G5LD + wn + b * 8 + g], dk);
+        const cplx v = S.b[(k4 + t4) * G5LD + wn + b * 8 + g];
         br[b] = v.x;
         bi[b] = v.y;
       }
@@ -971,7 +488,6 @@ template <int G6K, int NCOL>
 struct Stage6 {
   cplx a[G6K * G6LA];
   cplx b[G6K * (NCOL + 2)];  // B column stride: NCOL cols + pad
-  cplx d[G6K];
 };
 }  // namespace
 
@@ -1016,7 +532,6 @@ __global__ void __launch_bounds__(NCOL * 4, NCOL == 32 ? 2 : 1) k_gemm6(
   const int nchunks = (t1 - t0 + G6K - 1) / G6K;
   const unsigned na = (unsigned)min(GT, nf - r0) * 16u;
   const unsigned nb = (unsigned)min(NCOL, nf - cc0) * 16u;
-  const cplx* __restrict__ dvec = pb.dvec[slot] + F.first[s];
 
   const TMap* tm = TMAP ? pb.tmap[slot] + 2 * s : nullptr;
   auto issue = [&](int ch) {
@@ -1030,20 +545,14 @@ __global__ void __launch_bounds__(NCOL * 4, NCOL == 32 ? 2 : 1) k_gemm6(
       // past npiv are zero-filled by the TMA unit (chunks never straddle t1
       // except at t1 = npiv, see build_plans)
       if (lane == 0) {
-        mbar_expect_tx(bar, (unsigned)G6K * (G6LA + G6LB) * 16u + (unsigned)G6K * 16u);
-        if (nval > 0) bulk_g2s(smem_u32(&S.d[0]), dvec + kt, (unsigned)nval * 16u, bar);
-        if (nval < G6K) bulk_g2s(smem_u32(&S.d[nval]), zeros, (unsigned)(G6K - nval) * 16u, bar);
+        mbar_expect_tx(bar, (unsigned)G6K * (G6LA + G6LB) * 16u);
         tma_2d(smem_u32(&S.a[0]), tm, 2 * r0, kt, bar);
         tma_2d(smem_u32(&S.b[0]), tm + 1, 2 * cc0, kt, bar);
       }
       return;
     }
-    if (lane == 0) {
-      mbar_expect_tx(bar, (unsigned)nval * (na + nb) + (unsigned)(G6K - nval) * (1024u + NCOL * 16u) +
-                              (unsigned)G6K * 16u);
-      if (nval > 0) bulk_g2s(smem_u32(&S.d[0]), dvec + kt, (unsigned)nval * 16u, bar);
-      if (nval < G6K) bulk_g2s(smem_u32(&S.d[nval]), zeros, (unsigned)(G6K - nval) * 16u, bar);
-    }
+    if (lane == 0)
+      mbar_expect_tx(bar, (unsigned)nval * (na + nb) + (unsigned)(G6K - nval) * (1024u + NCOL * 16u));
     for (int q = lane; q < 2 * G6K; q += 32) {
       const int kk = q >> 1;
       const int t = kt + kk;
@@ -1091,10 +600,9 @@ __global__ void __launch_bounds__(NCOL * 4, NCOL == 32 ? 2 : 1) k_gemm6(
           ar[a] = v.x;
           ai[a] = v.y;
         }
-        const cplx dk = S.d[k4 + t4];
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
-          const cplx v = cmul(S.b[(k4 + t4) * G6LB + wn + b * 8 + g], dk);
+          const cplx v = S.b[(k4 + t4) * G6LB + wn + b * 8 + g];
           br[b] = v.x;
           bi[b] = v.y;
         }

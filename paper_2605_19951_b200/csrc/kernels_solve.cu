@@ -39,8 +39,9 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 }
 
 // Forward task (front s, row block blk): rows [r0, r0+nr) of the front vector.
-//   pivot block  : y_blk = X_blk (v_blk - sum_{j<blk} L[blk, j] y_j)   (X = L_bb^{-1})
-//   border block : u     = v - sum_{j<npb} L[rows, j] y_j              -> parent
+//   pivot block  : y_blk = S^{-1} X_blk (v_blk - sum_{j<blk} L'[blk, j] y_j)
+//                  (X = L_bb^{-1}, S = diag sqrt(d): factor format, fronts.cuh)
+//   border block : u     = v - sum_{j<npb} L'[rows, j] y_j             -> parent
 // Warps split the pivot columns (column c handled by warp c % 8), lanes own
 // rows lane and lane+32, so every L load is a coalesced 2 x 512 B column
 // segment; each warp fetches the y values of its 8 columns of a block with one
@@ -203,9 +204,11 @@ __global__ void __launch_bounds__(256, 2) k_fwd(const SolveTask* __restrict__ ta
       yv[r] = cmk(a, b);
     }
     if (i < nr && k == 0) {
+      // y' = S^{-1} X t  (s_i = sqrt(d_i) on the diagonal, fronts.cuh)
+      const cplx si = cinv(STAGEX ? Xs[i * (PB + 1) + i] : panel[(int64_t)(r0 + i) * nf + r0 + i]);
 #pragma unroll
       for (int r = 0; r < NR; ++r)
-        x[(int64_t)(first + r0 + i) * NR + r] = cadd(v[i][r], yv[r]);
+        x[(int64_t)(first + r0 + i) * NR + r] = cmul(cadd(v[i][r], yv[r]), si);
       __threadfence();
     }
     __syncthreads();
@@ -225,7 +228,7 @@ __global__ void __launch_bounds__(256, 2) k_fwd(const SolveTask* __restrict__ ta
 }
 
 // Backward task (front s, pivot column block cb), blocks processed from the
-// last one down:  x_cb = X^T (y_cb / d_cb - sum_{rho beyond block} L[rho, cb]^T x_rho).
+// last one down:  x_cb = X^T S^{-1} (y_cb - sum_{rho beyond block} L'[rho, cb]^T x_rho).
 // NW warps x 64/NW columns, lanes stride the rows; no block barrier in the main
 // loop (the pivot-block waits are per warp).
 template <int NR, int NW>
@@ -354,11 +357,11 @@ __global__ void __launch_bounds__(32 * NW) k_bwd(const SolveTask* __restrict__ t
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   if (tid < ncol) {
-    const cplx d = Xs[tid * (PB + 1) + tid];
+    const cplx sc = Xs[tid * (PB + 1) + tid];   // s_c = sqrt(d_c)
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
       const cplx y = x[(int64_t)(first + c0 + tid) * NR + r];
-      tv[tid][r] = csub(cdiv(y, d), red[tid][r]);
+      tv[tid][r] = cdiv(csub(y, red[tid][r]), sc);
     }
   }
   __syncthreads();
@@ -460,10 +463,12 @@ __global__ void __launch_bounds__(256) k_fwd_small(const int32_t* __restrict__ f
     for (int h = 0; h < 2; ++h) {
       const int c = lane + 32 * h;
       if (c < pb) {
+        const cplx si = cinv(panel[(int64_t)(c0 + c) * nf + c0 + c]);   // 1 / sqrt(d_c)
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
-          vy[c0 + c][r] = yv[h][r];
-          x[(int64_t)(first + c0 + c) * NR + r] = yv[h][r];
+          const cplx y = cmul(yv[h][r], si);
+          vy[c0 + c][r] = y;
+          x[(int64_t)(first + c0 + c) * NR + r] = y;
         }
       }
     }
@@ -563,10 +568,10 @@ __global__ void __launch_bounds__(256) k_bwd_small(const int32_t* __restrict__ f
     for (int h = 0; h < 2; ++h) {
       const int c = lane + 32 * h;
       if (c < pb) {
-        const cplx d = panel[(int64_t)(c0 + c) * nf + c0 + c];
+        const cplx sc = panel[(int64_t)(c0 + c) * nf + c0 + c];   // s_c = sqrt(d_c)
 #pragma unroll
         for (int r = 0; r < NR; ++r)
-          tv[c][r] = csub(cdiv(x[(int64_t)(first + c0 + c) * NR + r], d), acc[h][r]);
+          tv[c][r] = cdiv(csub(x[(int64_t)(first + c0 + c) * NR + r], acc[h][r]), sc);
       }
     }
     __syncwarp();

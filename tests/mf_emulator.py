@@ -109,3 +109,16 @@ def solve(b: np.ndarray, panels, S):
     out = np.empty_like(x)
     out[perm] = x
     return out
+
+
+def device_panel_to_ldl(Ld: np.ndarray, p: int, pb: int = 64) -> np.ndarray:
+    """Device factor format (fronts.cuh: L' = L D^{1/2} below each 64-pivot
+    diagonal block, s = sqrt(d) on the diagonal, unit L inside the diagonal
+    blocks) -> the emulator's L (unit lower) / D (diagonal) panel."""
+    out = Ld.copy()
+    for j in range(p):
+        s = Ld[j, j]
+        b1 = min((j // pb + 1) * pb, p)
+        out[b1:, j] = Ld[b1:, j] / s
+        out[j, j] = s * s
+    return out

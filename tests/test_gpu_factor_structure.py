@@ -31,7 +31,7 @@ def test_device_fronts_match_emulation(gpu, n):
     worst = []
     for s, Lh in enumerate(panels):
         nf, p = S["nf"][s], S["npiv"][s]
-        Ld = buf[S["panel_off"][s]:S["panel_off"][s] + nf * p].reshape(p, nf).T
+        Ld = mf.device_panel_to_ldl(buf[S["panel_off"][s]:S["panel_off"][s] + nf * p].reshape(p, nf).T, p)
         mask = np.tril(np.ones((nf, p), bool))
         e = np.abs(Ld[mask] - Lh[mask]).max() / max(np.abs(Lh[mask]).max(), 1e-300)
         worst.append((float(e), s, int(p), int(nf), int(S["level"][s])))
@@ -44,31 +44,44 @@ def test_device_fronts_match_emulation(gpu, n):
     assert rel(prob.Q @ x, prob.Q @ mf.solve(b, panels, S)) <= 1e-10
 
 
+def _worst_front_error(buf, panels, S):
+    worst = 0.0
+    for s, Lh in enumerate(panels):
+        nf, p = S["nf"][s], S["npiv"][s]
+        Ld = mf.device_panel_to_ldl(buf[S["panel_off"][s]:S["panel_off"][s] + nf * p].reshape(p, nf).T, p)
+        mask = np.tril(np.ones((nf, p), bool))
+        worst = max(worst, np.abs(Ld[mask] - Lh[mask]).max() / max(np.abs(Lh[mask]).max(), 1e-300))
+    return float(worst)
+
+
 def test_dmma_gemm_matches_dfma_reference(gpu, monkeypatch):
-    """The FP64 tensor-core (DMMA) trailing update equals the DFMA reference
-    kernel on the same fronts (C1 shape, n=10: multi-block fronts)."""
+    """Every GEMM variant (the DFMA reference kernel with the substitution TRSM,
+    the DMMA kernels v3..v8 with the inverted-diagonal TRSM) yields the host
+    emulation's factor front by front (C1 shape, n=10: multi-block fronts),
+    and the variants agree with one another."""
     prob, _ = rb.build_config("C1", n=10)
     approx = rb.config_approximant("C1")
     model = prob.true_model()
+    S = mf.analyze(prob.K, prob.dof_coords, 64)
+    A = (prob.K.astype(complex) - approx.poles[2] * orc.assemble_M(prob, model.m)).tocsr()
+    panels = mf.factor(A, S)
     out = []
-    modes = ("dfma", "v1", "v2", "v3", "v4", "v5", "v5b", "v6", "v6b", "v6c", "v6d", "v7", "v7b", "v8")
+    modes = ("dfma", "v3", "v4", "v5", "v5b", "v6", "v6b", "v6c", "v6d", "v7", "v7b", "v8")
     for mode in modes:
         monkeypatch.setenv("RBA_GEMM", mode)
         cache = rb.ShiftedFactorCache()
         rb.factorize_all_poles(prob, model, approx, cache)
         eng = cache.engine
-        S = mf.analyze(prob.K, prob.dof_coords, 64)
         tot = int(S["panel_off"][-1])
         buf = np.empty(tot, dtype=np.complex128)
         _lib.check(eng.lib.rba_get_factor(eng.ctx, 2, ptr(buf.view(np.float64)), tot))
         out.append(buf)
         eng.close()
-    # the DFMA reference path also keeps the substitution TRSM, the DMMA path
-    # uses the inverted diagonal block: rounding-level differences only
-    for mode, o in zip(modes[1:], out[1:]):
-        err = rel(o, out[0])
-        print(f"GEMM {mode}: factor vs DFMA reference {err:.2e}")
+        err = _worst_front_error(buf, panels, S)
+        print(f"GEMM {mode}: worst front vs emulation {err:.2e}, factor vs DFMA {rel(buf, out[0]):.2e}")
         assert err <= 1e-10, mode
+    for mode, o in zip(modes[1:], out[1:]):
+        assert rel(o, out[0]) <= 1e-7, mode
 
 
 def test_fused_sweep_equals_level_sweeps(gpu, monkeypatch):
@@ -107,22 +120,27 @@ def test_fused_sweep_equals_level_sweeps(gpu, monkeypatch):
 
 
 def test_blocked_diag_matches_unblocked(gpu, monkeypatch):
+    """Both diagonal-block kernels (k_diag: one barrier pair per pivot; k_diag2:
+    16x16 sub-blocks) yield the host emulation's factor front by front."""
     prob, _ = rb.build_config("C1", n=10)
     approx = rb.config_approximant("C1")
     model = prob.true_model()
+    S = mf.analyze(prob.K, prob.dof_coords, 64)
+    A = (prob.K.astype(complex) - approx.poles[1] * orc.assemble_M(prob, model.m)).tocsr()
+    panels = mf.factor(A, S)
     outs = []
     for mode in ("v1", "v2"):
         monkeypatch.setenv("RBA_DIAG", mode)
         cache = rb.ShiftedFactorCache()
         rb.factorize_all_poles(prob, model, approx, cache)
         eng = cache.engine
-        S = mf.analyze(prob.K, prob.dof_coords, 64)
         tot = int(S["panel_off"][-1])
         buf = np.empty(tot, dtype=np.complex128)
         _lib.check(eng.lib.rba_get_factor(eng.ctx, 1, ptr(buf.view(np.float64)), tot))
         outs.append(buf)
         eng.close()
-    assert rel(outs[1], outs[0]) <= 1e-10
+        assert _worst_front_error(buf, panels, S) <= 1e-10, mode
+    assert rel(outs[1], outs[0]) <= 1e-7
 
 
 def test_receiver_green_matches_sweeps(gpu, monkeypatch):
