@@ -569,7 +569,7 @@ int check_err(rba_ctx* c, int pole) {
 // Boxes: 66 complex rows (A operand) and 34 (B operand) by G8K columns, so a
 // box lands in shared memory with the padded strides the kernel reads
 // conflict-free.  Out-of-range rows / columns are zero-filled.
-int make_tmaps(rba_ctx* c, const cplx* base, rba::TMap** out) {
+int make_tmaps(rba_ctx* c, const cplx* base, rba::TMap** out, int boxk) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -593,7 +593,7 @@ int make_tmaps(rba_ctx* c, const cplx* base, rba::TMap** out) {
     const cuuint64_t strides[1] = {(cuuint64_t)nf * sizeof(cplx)};
     const cuuint32_t estr[2] = {1, 1};
     for (int w = 0; w < 2; ++w) {
-      const cuuint32_t box[2] = {(cuuint32_t)(w == 0 ? 132 : 68), (cuuint32_t)rba::G8K};
+      const cuuint32_t box[2] = {(cuuint32_t)(w == 0 ? 132 : 68), (cuuint32_t)boxk};
       CUresult r = encode(reinterpret_cast<CUtensorMap*>(&h[2 * s + w]), CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2,
                           (void*)(base + S.panel_off[s]), dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -623,8 +623,10 @@ int ensure_slots(rba_ctx* c) {
   c->NRw = c->NRs;
   for (int l = 0; l < nl; ++l) {
     if ((rc = dalloc(c, c->pole_allocs, &c->factor[l], S.panel_off[S.nfront], &c->mem_factor))) return rc;
-    if (c->gemm_v == 6 && c->gemm5_var == 6 || c->panel_v == 6 && c->panel_var == 6)
-      if ((rc = make_tmaps(c, c->factor[l], &c->tmaps[l]))) return rc;
+    if (c->gemm_v == 6 && c->gemm5_var >= 6 || c->panel_v == 6 && c->panel_var >= 6)
+      if ((rc = make_tmaps(c, c->factor[l], &c->tmaps[l],
+                           (c->gemm_v == 6 ? c->gemm5_var : c->panel_var) == 7 ? 12 : rba::G8K)))
+        return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->g[l], (size_t)c->N * c->NRw, &c->mem_work))) return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->x[l], (size_t)c->N * c->NRw, &c->mem_work))) return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->uvec[l], (size_t)std::max<int64_t>(S.uvec_off[S.nfront], 1) * c->NRw, &c->mem_work))) return rc;
@@ -896,6 +898,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     if (std::string(e) == "v7") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 4; }
     if (std::string(e) == "v7b") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 5; }
     if (std::string(e) == "v8") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 6; }
+    if (std::string(e) == "v8b") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 7; }
   }
   if (const char* e = getenv("RBA_GEMM_PANEL")) {
     const std::string v(e);

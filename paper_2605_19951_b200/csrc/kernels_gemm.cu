@@ -600,11 +600,14 @@ __global__ void __launch_bounds__(NCOL * 4, NCOL == 32 ? 2 : 1) k_gemm6(
           ar[a] = v.x;
           ai[a] = v.y;
         }
+        // boxes wider than the 64-column task boundaries (G6K not dividing 64)
+        // read real columns past t1: mask them in the B fragment
+        const bool kin = !(TMAP && (64 % G6K) != 0) || t0 + ch * G6K + k4 + t4 < t1;
 #pragma unroll
         for (int b = 0; b < 2; ++b) {
           const cplx v = S.b[(k4 + t4) * G6LB + wn + b * 8 + g];
-          br[b] = v.x;
-          bi[b] = v.y;
+          br[b] = kin ? v.x : 0.0;
+          bi[b] = kin ? v.y : 0.0;
         }
 #pragma unroll
         for (int a = 0; a < 4; ++a)
@@ -698,6 +701,7 @@ void launch_gemm6(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
   else if (variant == 4) launch_g6<16, 6, 64>(st, grid1, tasks, ntasks, F, pb, zeros);
   else if (variant == 5) launch_g6<16, 4, 64>(st, grid1, tasks, ntasks, F, pb, zeros);
   else if (variant == 6) launch_g6<G8K, 5, 32, true>(st, grid, tasks, ntasks, F, pb, zeros);
+  else if (variant == 7) launch_g6<12, 3, 32, true>(st, grid, tasks, ntasks, F, pb, zeros);
   else launch_g6<16, 4, 32>(st, grid, tasks, ntasks, F, pb, zeros);
 }
 
