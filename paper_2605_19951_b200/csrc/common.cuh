@@ -73,6 +73,20 @@ __device__ __forceinline__ void spin_wait_geq(const int* p, int target) {
   }
 }
 
+// FP64 tensor-core MMA (m8n8k4, SASS DMMA.8): {c0,c1} += a * b
+__device__ __forceinline__ void dmma_f64(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+// 16-byte cp.async global -> shared (zero-fill when !valid)
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz)
+               : "memory");
+}
+
 // mbarrier + bulk async copy (cp.async.bulk) helpers
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);

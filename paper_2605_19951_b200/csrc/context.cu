@@ -130,9 +130,12 @@ struct rba_ctx {
   bool green = false;
   std::vector<cplx*> Z;
   std::vector<char> green_valid;
+  std::vector<int*> zflags;       // per slot: [nblocks][Mr/32] completion flags of k_zbwd
+  std::vector<int> zepoch;
   cplx* green_part = nullptr;
   int green_chunks = 64;
   bool green_prune = true;        // RBA_GREEN_PRUNE=0: full forward sweeps in the Z build
+  bool green_gemm = true;         // RBA_GREEN_GEMM=0: per-batch backward sweeps in the Z build
   int64_t n_green = 0;            // Z builds (slots)
   std::vector<int*> flf, flb, dnf, dnb;
   std::vector<int> slot_epoch;    // solves issued per local slot (flags / counters)
@@ -668,6 +671,13 @@ int ensure_slots(rba_ctx* c) {
     c->green_valid.assign(nl, 0);
     if (c->green) {
       for (int l = 0; l < nl; ++l) c->Z[l] = pool + (size_t)l * zsz;
+      const size_t nzf = (size_t)(c->nblocks + 1) * ((c->Mr + 31) / 32);
+      c->zflags.assign(nl, nullptr);
+      c->zepoch.assign(nl, 0);
+      for (int l = 0; l < nl; ++l) {
+        if ((rc = dalloc(c, c->pole_allocs, &c->zflags[l], nzf, &c->mem_work))) return rc;
+        CK(cudaMemsetAsync(c->zflags[l], 0, nzf * sizeof(int), c->st));
+      }
       if ((rc = dalloc(c, c->pole_allocs, &c->green_part,
                        (size_t)c->green_chunks * nl * std::max(c->S, 1) * c->Mr, &c->mem_work)))
         return rc;
@@ -682,7 +692,8 @@ int ensure_slots(rba_ctx* c) {
 
 // prune_b >= 0: forward sweep only over the fronts on the paths of receiver
 // batch prune_b (right-hand sides Q^T e_m are zero elsewhere; see build_prune)
-int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR, int prune_b = -1) {
+int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR, int prune_b = -1,
+                bool fwd_only = false) {
   const int ns = (int)slots.size();
   if (ns == 0) return RBA_OK;
   rba::SolveBatch b;
@@ -749,7 +760,7 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR, int prune_b =
       }
     }
     if (c->timing) cudaEventRecord(c->ev[1], c->st);
-    for (int L = S.nlevels - 1; L >= 0; --L) {
+    for (int L = S.nlevels - 1; L >= 0 && !fwd_only; --L) {
       Timed tl(c, 48 + std::min(L, 31), 0);
       if (c->bwdb_lv[L].second > 0) {
         Timed tm(c, KC_BWD);
@@ -909,6 +920,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   }
   if (const char* e = getenv("RBA_GREEN")) c->green_req = std::string(e) != "0";
   if (const char* e = getenv("RBA_GREEN_PRUNE")) c->green_prune = std::string(e) != "0";
+  if (const char* e = getenv("RBA_GREEN_GEMM")) c->green_gemm = std::string(e) != "0";
   if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) == "fused";
   if (const char* e = getenv("RBA_SMALLP")) c->small_p = std::string(e) == "64" ? rba::PB : 2 * rba::PB;
   if (const char* e = getenv("RBA_DIAG")) c->diag_v1 = std::string(e) == "v1";
@@ -1343,6 +1355,7 @@ static int ensure_green(rba_ctx* c) {
   const rba::SlotPtrs xs = slot_sub(c->x, slots), zs = slot_sub(c->Z, slots);
   int rc;
   const bool prune = !c->fused_sweep && c->green_prune;
+  const bool zg = !c->fused_sweep && c->green_gemm;
   if (prune && c->prune_nb != nb && (rc = build_prune(c, nb))) return rc;
   const rba::Symbolic& S = c->sym;
   const size_t uvn = (size_t)std::max<int64_t>(S.uvec_off[S.nfront], 1) * c->NRw;
@@ -1355,12 +1368,40 @@ static int ensure_green(rba_ctx* c) {
       rba::launch_green_rhs(c->st, ns, c->N, m0, n, nb, c->qt_ptr, c->qt_col, c->qt_val, xs);
     }
     CKL();
-    if ((rc = solve_slots(c, slots, nb, prune ? (int)(m0 / nb) : -1))) return rc;
+    // forward sweep only (y' = L'^{-1} Q^T); the backward runs once over all
+    // receivers below, unless RBA_GREEN_GEMM=0
+    if ((rc = solve_slots(c, slots, nb, prune ? (int)(m0 / nb) : -1, zg))) return rc;
     {
       Timed t(c, KC_GREEN);
       rba::launch_green_store(c->st, ns, c->N, c->Mr, m0, n, nb, xs, zs);
     }
     CKL();
+  }
+  if (zg) {
+    // Z := L'^{-T} Z, level by level from the root, all receivers per task
+    rba::SolveBatch b;
+    for (int i = 0; i < ns; ++i) {
+      const int l = slots[i];
+      b.factor[i] = c->factor[l];
+      b.x[i] = c->x[l];
+      b.uvec[i] = c->uvec[l];
+      b.flags_f[i] = nullptr;
+      b.flags_b[i] = c->zflags[l];
+      b.done_f[i] = nullptr;
+      b.done_b[i] = nullptr;
+      if (c->zepoch[l] + 1 >= (1 << 30)) {
+        CK(cudaMemsetAsync(c->zflags[l], 0, (size_t)(c->nblocks + 1) * ((c->Mr + 31) / 32) * sizeof(int), c->st));
+        c->zepoch[l] = 0;
+      }
+      b.epoch[i] = ++c->zepoch[l];
+    }
+    CK(cudaMemsetAsync(c->tickets, 0, (2 * (size_t)S.nlevels + 2) * sizeof(int), c->st));
+    for (int L = S.nlevels - 1; L >= 0; --L) {
+      Timed t(c, KC_GREEN);
+      rba::launch_zbwd(c->st, c->bwd_tasks + c->bwd_lv[L].first, c->bwd_lv[L].second, ns, c->F, b,
+                       c->tickets + S.nlevels + L, (int)c->Mr, zs);
+      CKL();
+    }
   }
   for (int l : slots) c->green_valid[l] = 1;
   c->n_green += ns;

@@ -57,6 +57,9 @@ void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* 
                         bool fused, bool stagex = false);
 void launch_solve_small(cudaStream_t st, bool forward, int nr, const int32_t* fronts, int nfr,
                         int nslots, const FrontsDev& F, const SolveBatch& b, int mb);
+// receiver-Green build: backward sweep over Z (N x Mr) as DMMA GEMMs
+void launch_zbwd(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
+                 const FrontsDev& F, const SolveBatch& b, int* ticket, int Mr, const SlotPtrs& Z);
 void launch_perm_in(cudaStream_t st, int64_t n, int nrhs, int NR, const int32_t* perm,
                     const cplx* b, int64_t ldb, cplx* x);
 void launch_perm_out(cudaStream_t st, int64_t n, int nrhs, int NR, const int32_t* perm,

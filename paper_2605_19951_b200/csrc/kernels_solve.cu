@@ -719,6 +719,216 @@ void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* 
   }
 }
 
+// ---------------------------------------------------------------------------
+// Backward sweep of the receiver-Green build as FP64 tensor-core GEMMs: Z holds
+// y' = L'^{-1} Q^T (N x Mr, row-major, from the pruned forward sweeps); each
+// task (front s, pivot block cb) computes, for all Mr columns at once,
+//   T   = Z[block rows] - L'[rows beyond block, block]^T Z[rows beyond block]
+//   Z[block rows] = X^T S^{-1} T
+// i.e. the k_bwd recurrence with Mr right-hand sides, where the row reduction
+// is a DMMA GEMM (K = rows beyond the block) instead of a GEMV per RHS.  CTA
+// tile 64 (block columns) x 32 (receivers), 4 warps of 32x16, 4 real DMMAs per
+// complex product, operands staged by cp.async in a 3-stage pipeline; the CTA
+// walks the receiver chunks.  Rows beyond the block: border rows (ancestor
+// pivots, final before this launch) first, then the later pivot blocks of the
+// same front from the last one down (earlier tickets; flag waits).
+// ---------------------------------------------------------------------------
+namespace {
+constexpr int ZK = 8;             // k (rows) per stage
+constexpr int ZLK = ZK + 4;       // padded [row][k] stride (complex): conflict-free LDS.128
+constexpr int ZNS = 3;            // stages
+constexpr int ZMC = 32;           // receiver columns per chunk
+struct ZStage {
+  cplx a[PB * ZLK];               // [block column i][k]
+  cplx b[ZMC * ZLK];              // [receiver n][k]
+};
+}  // namespace
+
+__global__ void __launch_bounds__(128) k_zbwd(const SolveTask* __restrict__ tasks, int nslots,
+                                              FrontsDev F, SolveBatchDev sb, int* ticket, int Mr,
+                                              SlotPtrs Zp) {
+  extern __shared__ __align__(16) unsigned char zsm[];
+  ZStage* st = reinterpret_cast<ZStage*>(zsm);
+  cplx(*Ts)[ZMC + 1] = reinterpret_cast<cplx(*)[ZMC + 1]>(zsm);   // overlays the stages
+  __shared__ int s_t;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_t = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int t = s_t;
+  const int slot = t % nslots;
+  const int epoch = sb.epoch[slot];
+  const SolveTask tk = tasks[t / nslots];
+  const int s = tk.s, cb = tk.blk;
+  const int p = F.npiv[s], nf = F.nf[s], first = F.first[s];
+  const int npb = (p + PB - 1) / PB;
+  const cplx* panel = sb.factor[slot] + F.panel_off[s];
+  cplx* Z = Zp.p[slot];
+  // completion flags per (pivot block, receiver chunk): a chunk of block cb
+  // only waits for the same chunk of the later blocks, so the chains of the
+  // chunks pipeline
+  const int nmc = (Mr + ZMC - 1) / ZMC;
+  int* flags = sb.flags[slot] + F.blk_off[s] * nmc;
+  const int c0 = cb * PB, kb = min(PB, p - c0);
+  const int* rows = F.rows + F.rows_off[s];
+  const int nbord = nf - p;                    // border rows p .. nf-1
+  const int kbord = (nbord + ZK - 1) / ZK;     // border chunks (last one partial)
+  // later pivot blocks cb+1 .. npb-1, last (possibly partial) block first
+  const int clast = cb < npb - 1 ? (p - (npb - 1) * PB + ZK - 1) / ZK : 0;
+  const int nchunk = kbord + clast + (cb < npb - 1 ? (npb - 2 - cb) * (PB / ZK) : 0);
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  const int g = lane >> 2, t4 = lane & 3;
+
+  for (int m0 = 0; m0 < Mr; m0 += ZMC) {
+    const int nm = min(ZMC, Mr - m0), mc = m0 / ZMC;
+    // stage chunk ch: k rows rho_k, A[i][k] = L'[rho_k, c0+i], B[n][k] = Z[idx(rho_k)][m0+n]
+    auto issue = [&](int ch) {
+      if (ch >= nchunk) {
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+        return;
+      }
+      ZStage& S = st[ch % ZNS];
+      int rho0, nval;
+      if (ch < kbord) {
+        rho0 = p + ch * ZK;
+        nval = min(ZK, nf - rho0);
+      } else {
+        const int q = ch - kbord;
+        int rb, sub;
+        if (q < clast) {
+          rb = npb - 1;
+          sub = q;
+        } else {
+          rb = npb - 2 - (q - clast) / (PB / ZK);
+          sub = (q - clast) % (PB / ZK);
+        }
+        rho0 = rb * PB + sub * ZK;
+        nval = min(ZK, min(p, rb * PB + PB) - rho0);
+        if (sub == 0) {
+          // first chunk of block rb: its Z rows must be final
+          if (tid == 0) spin_wait_geq(flags + rb * nmc + mc, epoch);
+          __syncthreads();
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < (PB * ZK) / 128; ++q) {
+        const int e = tid + q * 128;
+        const int kk = e % ZK, i = e / ZK;
+        const bool ok = kk < nval && i < kb;
+        cp_async16(&S.a[i * ZLK + kk], panel + (ok ? (int64_t)(c0 + i) * nf + rho0 + kk : 0), ok);
+      }
+#pragma unroll
+      for (int q = 0; q < (ZMC * ZK) / 128; ++q) {
+        const int e = tid + q * 128;
+        const int n = e % ZMC, kk = e / ZMC;
+        const bool ok = kk < nval && n < nm;
+        const int rho = rho0 + kk;
+        const int64_t zr = ok ? (rho < p ? (int64_t)(first + rho) : (int64_t)__ldg(rows + rho)) : 0;
+        cp_async16(&S.b[n * ZLK + kk], Z + (ok ? zr * Mr + m0 + n : 0), ok);
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    double cre[4][2][2], cim[4][2][2];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        cre[a][b][0] = cre[a][b][1] = 0.0;
+        cim[a][b][0] = cim[a][b][1] = 0.0;
+      }
+    for (int c = 0; c < ZNS - 1; ++c) issue(c);
+    for (int ch = 0; ch < nchunk; ++ch) {
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(ZNS - 2) : "memory");
+      __syncthreads();
+      issue(ch + ZNS - 1);
+      const ZStage& S = st[ch % ZNS];
+#pragma unroll
+      for (int k4 = 0; k4 < ZK; k4 += 4) {
+        double ar[4], ai[4], an[4], br[2], bi[2];
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const cplx v = S.a[(wm + a * 8 + g) * ZLK + k4 + t4];
+          ar[a] = v.x;
+          ai[a] = v.y;
+          an[a] = -v.y;
+        }
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const cplx v = S.b[(wn + b * 8 + g) * ZLK + k4 + t4];
+          br[b] = v.x;
+          bi[b] = v.y;
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) dmma_f64(cre[a][b][0], cre[a][b][1], ar[a], br[b]);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) dmma_f64(cim[a][b][0], cim[a][b][1], ar[a], bi[b]);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) dmma_f64(cre[a][b][0], cre[a][b][1], an[a], bi[b]);
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 2; ++b) dmma_f64(cim[a][b][0], cim[a][b][1], ai[a], br[b]);
+      }
+    }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    // T = (Z[block rows] - acc) / s  -> shared memory
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int i = wm + a * 8 + g, n = wn + b * 8 + t4 * 2 + h;
+          if (i < kb && n < nm) {
+            const cplx y = Z[(int64_t)(first + c0 + i) * Mr + m0 + n];
+            const cplx sc = __ldg(panel + (int64_t)(c0 + i) * nf + c0 + i);
+            Ts[i][n] = cdiv(cmk(y.x - cre[a][b][h], y.y - cim[a][b][h]), sc);
+          }
+        }
+    __syncthreads();
+    // Z[block rows] = X^T T :  out_i = T_i + sum_{j > i} X[j][i] T_j, X[j][i] at (row c0+i, col c0+j)
+    {
+      const int n = tid % ZMC, ig = tid / ZMC;
+      for (int i = ig; i < kb; i += 128 / ZMC) {
+        cplx acc = Ts[i][n];
+        const cplx* xr = panel + (int64_t)c0 * nf + c0 + i;
+        for (int j = i + 1; j < kb; ++j) acc = cfma(__ldg(xr + (int64_t)j * nf), Ts[j][n], acc);
+        if (n < nm) Z[(int64_t)(first + c0 + i) * Mr + m0 + n] = acc;
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) st_release(flags + cb * nmc + mc, epoch);
+  }
+}
+
+void launch_zbwd(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
+                 const FrontsDev& F, const SolveBatch& b, int* ticket, int Mr, const SlotPtrs& Z) {
+  if (ntasks <= 0) return;
+  SolveBatchDev sb;
+  for (int i = 0; i < nslots; ++i) {
+    sb.factor[i] = b.factor[i];
+    sb.x[i] = b.x[i];
+    sb.uvec[i] = b.uvec[i];
+    sb.flags[i] = b.flags_b[i];
+    sb.done[i] = b.done_b[i];
+    sb.epoch[i] = b.epoch[i];
+  }
+  const size_t smem = std::max(ZNS * sizeof(ZStage), PB * (ZMC + 1) * sizeof(cplx));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_zbwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_zbwd<<<ntasks * nslots, 128, smem, st>>>(tasks, nslots, F, sb, ticket, Mr, Z);
+}
+
 // original-order (column-major N x nrhs complex) <-> permuted padded layout
 __global__ void k_perm_in(int64_t n, int nrhs, int NR, const int32_t* __restrict__ perm,
                           const cplx* __restrict__ b, int64_t ldb, cplx* __restrict__ x) {
