@@ -734,19 +734,21 @@ void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* 
 // same front from the last one down (earlier tickets; flag waits).
 // ---------------------------------------------------------------------------
 namespace {
-constexpr int ZK = 8;             // k (rows) per stage
-constexpr int ZLK = ZK + 4;       // padded [row][k] stride (complex): conflict-free LDS.128
-constexpr int ZNS = 3;            // stages
 constexpr int ZMC = 32;           // receiver columns per chunk
+template <int ZK>                 // k (rows) per stage
 struct ZStage {
+  static constexpr int ZLK = ZK + 4;   // padded [row][k] stride (complex): conflict-free LDS.128
   cplx a[PB * ZLK];               // [block column i][k]
   cplx b[ZMC * ZLK];              // [receiver n][k]
 };
 }  // namespace
 
+template <int ZK, int ZNS>
 __global__ void __launch_bounds__(128) k_zbwd(const SolveTask* __restrict__ tasks, int nslots,
                                               FrontsDev F, SolveBatchDev sb, int* ticket, int Mr,
                                               SlotPtrs Zp) {
+  using ZStage = ::rba::ZStage<ZK>;
+  constexpr int ZLK = ZStage::ZLK;
   extern __shared__ __align__(16) unsigned char zsm[];
   ZStage* st = reinterpret_cast<ZStage*>(zsm);
   cplx(*Ts)[ZMC + 1] = reinterpret_cast<cplx(*)[ZMC + 1]>(zsm);   // overlays the stages
@@ -908,6 +910,19 @@ __global__ void __launch_bounds__(128) k_zbwd(const SolveTask* __restrict__ task
   }
 }
 
+template <int ZK, int ZNS>
+static void zbwd_go(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
+                    const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int Mr,
+                    const SlotPtrs& Z) {
+  const size_t smem = std::max(ZNS * sizeof(ZStage<ZK>), PB * (ZMC + 1) * sizeof(cplx));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_zbwd<ZK, ZNS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_zbwd<ZK, ZNS><<<ntasks * nslots, 128, smem, st>>>(tasks, nslots, F, sb, ticket, Mr, Z);
+}
+
 void launch_zbwd(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
                  const FrontsDev& F, const SolveBatch& b, int* ticket, int Mr, const SlotPtrs& Z) {
   if (ntasks <= 0) return;
@@ -920,13 +935,15 @@ void launch_zbwd(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots
     sb.done[i] = b.done_b[i];
     sb.epoch[i] = b.epoch[i];
   }
-  const size_t smem = std::max(ZNS * sizeof(ZStage), PB * (ZMC + 1) * sizeof(cplx));
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_zbwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+  static int var = -1;
+  if (var < 0) {
+    const char* e = getenv("RBA_ZBWD");
+    var = e ? atoi(e) : 1;
   }
-  k_zbwd<<<ntasks * nslots, 128, smem, st>>>(tasks, nslots, F, sb, ticket, Mr, Z);
+  // 1 (default): 16 rows x 2 stages; 0: 8 x 3; 2: 16 x 3
+  if (var == 1) zbwd_go<16, 2>(st, tasks, ntasks, nslots, F, sb, ticket, Mr, Z);
+  else if (var == 2) zbwd_go<16, 3>(st, tasks, ntasks, nslots, F, sb, ticket, Mr, Z);
+  else zbwd_go<8, 3>(st, tasks, ntasks, nslots, F, sb, ticket, Mr, Z);
 }
 
 // original-order (column-major N x nrhs complex) <-> permuted padded layout
