@@ -170,9 +170,9 @@ struct rba_ctx {
   int gemm_v = 6;             // default 3M DMMA kernel (k_gemm6); RBA_GEMM=v3..v7b select
                               // the earlier kernels for A/B tests
   int small_p = 2 * rba::PB;  // warp-per-front solves up to this npiv (RBA_SMALLP=64|128)
-  int gemm5_var = 6;          // v5/v6 stage shape (see launch_gemm5 / launch_gemm6); default
-                              // v8 = 64x32 half tiles, 8 k x 5 stages, 3 CTAs/SM, operands
-                              // by TMA tensor copies
+  int gemm5_var = 8;          // v5/v6 stage shape (see launch_gemm5 / launch_gemm6); default
+                              // v8c = 64x32 half tiles, 16 k x 2 stages, 3 CTAs/SM,
+                              // operands by TMA tensor copies
   int panel_v = 0;            // RBA_GEMM_PANEL: kernel for the panel updates (0 = as RBA_GEMM)
   int panel_var = 0;
   int gemm_var = 1;           // v3 stage shape: 1 (default, RBA_GEMM=v4) = 16 k x 2 stages,
@@ -611,6 +611,13 @@ int make_tmaps(rba_ctx* c, const cplx* base, rba::TMap** out, int boxk) {
   return RBA_OK;
 }
 
+// k-width of the TMA boxes for the selected tensor-map GEMM variant
+// (launch_gemm6: 6 -> 8 columns, 7 -> 12, 8 -> 16)
+int tmap_boxk(const rba_ctx* c) {
+  const int v = std::max(c->gemm_v == 6 ? c->gemm5_var : 0, c->panel_v == 6 ? c->panel_var : 0);
+  return v == 7 ? 12 : v == 8 ? 16 : rba::G8K;
+}
+
 int ensure_slots(rba_ctx* c) {
   if (!c->factor.empty()) return RBA_OK;
   const int nl = (int)c->local.size();
@@ -627,9 +634,7 @@ int ensure_slots(rba_ctx* c) {
   for (int l = 0; l < nl; ++l) {
     if ((rc = dalloc(c, c->pole_allocs, &c->factor[l], S.panel_off[S.nfront], &c->mem_factor))) return rc;
     if (c->gemm_v == 6 && c->gemm5_var >= 6 || c->panel_v == 6 && c->panel_var >= 6)
-      if ((rc = make_tmaps(c, c->factor[l], &c->tmaps[l],
-                           (c->gemm_v == 6 ? c->gemm5_var : c->panel_var) == 7 ? 12 : rba::G8K)))
-        return rc;
+      if ((rc = make_tmaps(c, c->factor[l], &c->tmaps[l], tmap_boxk(c)))) return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->g[l], (size_t)c->N * c->NRw, &c->mem_work))) return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->x[l], (size_t)c->N * c->NRw, &c->mem_work))) return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->uvec[l], (size_t)std::max<int64_t>(S.uvec_off[S.nfront], 1) * c->NRw, &c->mem_work))) return rc;
@@ -910,6 +915,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     if (std::string(e) == "v7b") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 5; }
     if (std::string(e) == "v8") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 6; }
     if (std::string(e) == "v8b") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 7; }
+    if (std::string(e) == "v8c") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 8; }
   }
   if (const char* e = getenv("RBA_GEMM_PANEL")) {
     const std::string v(e);

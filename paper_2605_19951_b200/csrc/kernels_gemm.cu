@@ -702,6 +702,7 @@ void launch_gemm6(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
   else if (variant == 5) launch_g6<16, 4, 64>(st, grid1, tasks, ntasks, F, pb, zeros);
   else if (variant == 6) launch_g6<G8K, 5, 32, true>(st, grid, tasks, ntasks, F, pb, zeros);
   else if (variant == 7) launch_g6<12, 3, 32, true>(st, grid, tasks, ntasks, F, pb, zeros);
+  else if (variant == 8) launch_g6<16, 2, 32, true>(st, grid, tasks, ntasks, F, pb, zeros);
   else launch_g6<16, 4, 32>(st, grid, tasks, ntasks, F, pb, zeros);
 }
 

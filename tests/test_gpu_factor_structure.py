@@ -66,7 +66,7 @@ def test_dmma_gemm_matches_dfma_reference(gpu, monkeypatch):
     A = (prob.K.astype(complex) - approx.poles[2] * orc.assemble_M(prob, model.m)).tocsr()
     panels = mf.factor(A, S)
     out = []
-    modes = ("dfma", "v3", "v4", "v5", "v5b", "v6", "v6b", "v6c", "v6d", "v7", "v7b", "v8", "v8b")
+    modes = ("dfma", "v3", "v4", "v5", "v5b", "v6", "v6b", "v6c", "v6d", "v7", "v7b", "v8", "v8b", "v8c")
     for mode in modes:
         monkeypatch.setenv("RBA_GEMM", mode)
         cache = rb.ShiftedFactorCache()
