@@ -76,6 +76,38 @@ __global__ void dmma16_kernel(double* out, int iters) {
   if (s == 12345.678) out[0] = s;
 }
 
+// mixed: even warps run DMMA chains, odd warps DFMA chains -- do the two
+// share one FP64 datapath (combined rate ~ one peak) or not (~ the sum)?
+__global__ void mixed_kernel(double* out, int it_mma, int it_fma) {
+  const int warp = threadIdx.x >> 5;
+  double s = 0;
+  if (warp & 1) {
+    double acc[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) acc[c] = threadIdx.x * 1e-3 + c;
+    for (int it = 0; it < it_fma; ++it) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = fma(acc[c], 1.0000001, 1e-9);
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) s += acc[c];
+  } else {
+    double a = 1.0 + threadIdx.x * 1e-6, b = 0.999;
+    double c[8][2];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { c[k][0] = 0; c[k][1] = 0; }
+    for (int it = 0; it < it_mma; ++it) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                     : "+d"(c[k][0]), "+d"(c[k][1]) : "d"(a), "d"(b));
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += c[k][0] + c[k][1];
+  }
+  if (s == 12345.678) out[0] = s;
+}
+
 template <int K>
 static double time16(double* d, int blocks, int threads, int iters) {
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
@@ -114,7 +146,19 @@ int main() {
   const double t4 = time16<4>(d, blocks, threads, iters / 4);
   const double t8 = time16<8>(d, blocks, threads, iters / 8);
   const double t16 = time16<16>(d, blocks, threads, iters / 16);
-  printf("{\"dfma_tflops\": %.3f, \"dmma_tflops\": %.3f, \"dmma_m16n8k4_tflops\": %.3f, \"dmma_m16n8k8_tflops\": %.3f, \"dmma_m16n8k16_tflops\": %.3f, \"sms\": %d, \"dfma_ms\": %.3f, \"dmma_ms\": %.3f, \"clock_khz\": %d}\n",
+  // mixed: DMMA iterations scaled so each half alone would take about the same time
+  const int it_mma = iters, it_fma = (int)(iters * 8.0 * dfma_tf / dmma_tf);
+  mixed_kernel<<<blocks, threads>>>(d, 100, 100);
+  CK(cudaDeviceSynchronize());
+  cudaEventRecord(e0);
+  mixed_kernel<<<blocks, threads>>>(d, it_mma, it_fma);
+  cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+  float ms3; cudaEventElapsedTime(&ms3, e0, e1);
+  const double half_warps = (threads / 64.0) * blocks;
+  const double mixed_tf = (2.0 * 256 * 8 * (double)it_mma * half_warps +
+                           2.0 * 8 * (double)it_fma * 32 * half_warps) / (ms3 * 1e-3) / 1e12;
+  printf("{\"mixed_dmma_dfma_tflops\": %.3f, ", mixed_tf);
+  printf("\"dfma_tflops\": %.3f, \"dmma_tflops\": %.3f, \"dmma_m16n8k4_tflops\": %.3f, \"dmma_m16n8k8_tflops\": %.3f, \"dmma_m16n8k16_tflops\": %.3f, \"sms\": %d, \"dfma_ms\": %.3f, \"dmma_ms\": %.3f, \"clock_khz\": %d}\n",
          dfma_tf, dmma_tf, t4, t8, t16, sms, ms, ms2, clk);
   return 0;
 }
