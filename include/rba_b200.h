@@ -128,7 +128,11 @@ int rba_vjp_partial(rba_ctx* ctx, const double* w_d, double* tpart_d);
 int rba_get_g(rba_ctx* ctx, int32_t slot, double* out_h);
 /* Copy the factor storage of a local slot (panel_total complex entries;
  * per-front nf x npiv column-major panels at symbolic panel_off) -- used by
- * the structure-level parity tests against the host emulation. */
+ * the structure-level parity tests against the host emulation.  Format
+ * (A_front = L' L'^T, L' = L D^{1/2}): rows below a column's 64-pivot diagonal
+ * block hold L' = L sqrt(d), the diagonal holds sqrt(d), the strictly lower
+ * part of each 64x64 diagonal block the unit L, its strictly upper part
+ * X = L_bb^{-1} transposed (tests/mf_emulator.py: device_panel_to_ldl). */
 int rba_get_factor(rba_ctx* ctx, int32_t slot, double* out_h, int64_t count);
 /* Ordered pole sums (forward.py:61-63; sensitivity.py:77-78,95-96):
  *   data: d[s][j][r] = sum_i 2 Re(alpha_ij q_i [* xi_i])  (times_pole = 1 for J v)
