@@ -133,6 +133,7 @@ struct rba_ctx {
   std::vector<int*> zflags;       // per slot: [nblocks][Mr/32] completion flags of k_zbwd
   std::vector<int> zepoch;
   cplx* green_part = nullptr;
+  cplx* jvp_w = nullptr;          // two-pass J v workspace (in the pool, past Z), or null
   int green_chunks = 64;
   bool green_prune = true;        // RBA_GREEN_PRUNE=0: full forward sweeps in the Z build
   bool green_gemm = true;         // RBA_GREEN_GEMM=0: per-batch backward sweeps in the Z build
@@ -674,6 +675,15 @@ int ensure_slots(rba_ctx* c) {
     for (int b = 0; b < c->fbatch; ++b) c->upd[b] = pool + (size_t)b * S.upd_total;
     c->Z.assign(nl, nullptr);
     c->green_valid.assign(nl, 0);
+    // the J v cell workspace also lives in the pool (not live during a
+    // factorisation), past Z when Green mode is on
+    {
+      const size_t wn = (size_t)nl * c->P * 6 * c->NRs;
+      const size_t z0 = c->green ? zall : 0;
+      const size_t cap = c->green ? std::max(arenas, zall) : arenas;
+      const char* e = getenv("RBA_JVP2");
+      c->jvp_w = (z0 + wn <= cap && !(e && std::string(e) == "0")) ? pool + z0 : nullptr;
+    }
     if (c->green) {
       for (int l = 0; l < nl; ++l) c->Z[l] = pool + (size_t)l * zsz;
       const size_t nzf = (size_t)(c->nblocks + 1) * ((c->Mr + 31) / 32);
@@ -1421,8 +1431,12 @@ int rba_jvp_partial(rba_ctx* c, const double* v_d, double* qpart) {
   int rc;
   if (c->green && (rc = ensure_green(c))) return rc;
   {
-    Timed t(c, KC_ELEM);
-    rba::launch_jvp_rhs(c->st, nl, elem(c), v_d, slot_ptrs(c->g), slot_ptrs(c->x), c->NRs, c->S);
+    Timed t(c, KC_ELEM, c->jvp_w ? 2 : 1);
+    if (c->jvp_w)
+      rba::launch_jvp_rhs2(c->st, nl, elem(c), v_d, slot_ptrs(c->g), slot_ptrs(c->x), c->NRs, c->S,
+                           c->jvp_w);
+    else
+      rba::launch_jvp_rhs(c->st, nl, elem(c), v_d, slot_ptrs(c->g), slot_ptrs(c->x), c->NRs, c->S);
   }
   CKL();
   if (c->green) {

@@ -74,6 +74,8 @@ struct ElemDev {
   const int64_t* dc_ptr;     // N+1 (permuted dof -> items)
   const int32_t* dc_item;    // c*6 + a
 };
+void launch_jvp_rhs2(cudaStream_t st, int nslots, const ElemDev& E, const double* v,
+                     const SlotPtrs& g, const SlotPtrs& out, int NR, int S, cplx* w);
 void launch_jvp_rhs(cudaStream_t st, int nslots, const ElemDev& E, const double* v,
                     const SlotPtrs& g, const SlotPtrs& out, int NR, int S);
 void launch_q_apply(cudaStream_t st, int nslots, int64_t Mr, const int64_t* qptr,

@@ -62,6 +62,82 @@ __global__ void k_jvp_rhs(ElemDev E, const double* __restrict__ v, SlotPtrs g, S
   }
 }
 
+// Two-pass variant (a workspace of nslots*P*6*NR complex is given):
+// pass 1, one thread per cell: w[c][a][r] = e^{m_c} v_c (M_c g|_c)_a -- the
+// cell's g rows are gathered once (the dof-parallel kernel gathers them once
+// per cell dof, 6x); pass 2, one thread per dof: the item sum in dc order.
+template <int NR>
+__global__ void k_jvp_cells(ElemDev E, const double* __restrict__ v, SlotPtrs g, cplx* __restrict__ w,
+                            int S) {
+  const int slot = blockIdx.y;
+  const cplx* gs = g.p[slot];
+  cplx* ws = w + (int64_t)slot * E.P * 6 * NR;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < E.P;
+       c += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t* dofs = E.cell_dofs + c * 6;
+    const double* M = E.mass + c * 36;
+    int dd[6];
+#pragma unroll
+    for (int b = 0; b < 6; ++b) dd[b] = __ldg(dofs + b);
+    const double sc = __ldg(E.expm + c) * __ldg(v + c);
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      cplx gl[6];
+#pragma unroll
+      for (int b = 0; b < 6; ++b)
+        gl[b] = (dd[b] >= 0 && r < S) ? gs[(int64_t)dd[b] * NR + r] : cmk(0.0, 0.0);
+#pragma unroll
+      for (int a = 0; a < 6; ++a) {
+        cplx loc = cmk(0.0, 0.0);
+#pragma unroll
+        for (int b = 0; b < 6; ++b) {
+          const double mab = __ldg(M + a * 6 + b);
+          loc.x = fma(mab, gl[b].x, loc.x);
+          loc.y = fma(mab, gl[b].y, loc.y);
+        }
+        ws[(c * 6 + a) * NR + r] = cmk(loc.x * sc, loc.y * sc);
+      }
+    }
+  }
+}
+
+template <int NR>
+__global__ void k_jvp_gather(ElemDev E, const cplx* __restrict__ w, SlotPtrs out) {
+  const int slot = blockIdx.y;
+  const cplx* ws = w + (int64_t)slot * E.P * 6 * NR;
+  cplx* o = out.p[slot];
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < E.N;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    cplx acc[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) acc[r] = cmk(0.0, 0.0);
+    for (int64_t q = E.dc_ptr[k]; q < E.dc_ptr[k + 1]; ++q) {
+      const cplx* wi = ws + (int64_t)E.dc_item[q] * NR;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) acc[r] = cadd(acc[r], wi[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) o[k * NR + r] = acc[r];
+  }
+}
+
+template <int NR>
+static void jvp2_nr(cudaStream_t st, int nslots, const ElemDev& E, const double* v,
+                    const SlotPtrs& g, const SlotPtrs& out, int S, cplx* w) {
+  k_jvp_cells<NR><<<dim3(grid_for(E.P), nslots), 256, 0, st>>>(E, v, g, w, S);
+  k_jvp_gather<NR><<<dim3(grid_for(E.N), nslots), 256, 0, st>>>(E, w, out);
+}
+
+void launch_jvp_rhs2(cudaStream_t st, int nslots, const ElemDev& E, const double* v,
+                     const SlotPtrs& g, const SlotPtrs& out, int NR, int S, cplx* w) {
+  switch (NR) {
+    case 1: jvp2_nr<1>(st, nslots, E, v, g, out, S, w); break;
+    case 2: jvp2_nr<2>(st, nslots, E, v, g, out, S, w); break;
+    case 4: jvp2_nr<4>(st, nslots, E, v, g, out, S, w); break;
+    default: jvp2_nr<8>(st, nslots, E, v, g, out, S, w); break;
+  }
+}
+
 void launch_jvp_rhs(cudaStream_t st, int nslots, const ElemDev& E, const double* v,
                     const SlotPtrs& g, const SlotPtrs& out, int NR, int S) {
   dim3 grid(grid_for(E.N), nslots);
