@@ -176,8 +176,9 @@ struct rba_ctx {
                               // operands by TMA tensor copies
   int panel_v = 0;            // RBA_GEMM_PANEL: kernel for the panel updates (0 = as RBA_GEMM)
   int panel_var = 0;
-  int gemm_var = 1;           // v3 stage shape: 1 (default, RBA_GEMM=v4) = 16 k x 2 stages,
-                              // 0 (RBA_GEMM=v3) = 8 k x 3 stages
+  int gemm_var = 0;           // k_gemm3 stage shape (TRSM; the v3/v4 GEMM): 0 (default TRSM,
+                              // RBA_GEMM=v3) = 8 k x 3 stages, 1 (RBA_GEMM=v4) = 16 k x 2;
+                              // RBA_TRSM_VAR overrides
   int64_t launches = 0;
   std::vector<cudaEvent_t> evpool;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
@@ -915,17 +916,17 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     c->gemm_dfma = std::string(e) == "dfma";
     if (std::string(e) == "v3") { c->gemm_v = 3; c->gemm_var = 0; }
     if (std::string(e) == "v4") { c->gemm_v = 3; c->gemm_var = 1; }
-    if (std::string(e) == "v5") { c->gemm_v = 5; c->gemm_var = 1; c->gemm5_var = 0; }
-    if (std::string(e) == "v5b") { c->gemm_v = 5; c->gemm_var = 1; c->gemm5_var = 1; }
-    if (std::string(e) == "v6") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 0; }
-    if (std::string(e) == "v6b") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 1; }
-    if (std::string(e) == "v6c") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 2; }
-    if (std::string(e) == "v6d") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 3; }
-    if (std::string(e) == "v7") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 4; }
-    if (std::string(e) == "v7b") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 5; }
-    if (std::string(e) == "v8") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 6; }
-    if (std::string(e) == "v8b") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 7; }
-    if (std::string(e) == "v8c") { c->gemm_v = 6; c->gemm_var = 1; c->gemm5_var = 8; }
+    if (std::string(e) == "v5") { c->gemm_v = 5; c->gemm5_var = 0; }
+    if (std::string(e) == "v5b") { c->gemm_v = 5; c->gemm5_var = 1; }
+    if (std::string(e) == "v6") { c->gemm_v = 6; c->gemm5_var = 0; }
+    if (std::string(e) == "v6b") { c->gemm_v = 6; c->gemm5_var = 1; }
+    if (std::string(e) == "v6c") { c->gemm_v = 6; c->gemm5_var = 2; }
+    if (std::string(e) == "v6d") { c->gemm_v = 6; c->gemm5_var = 3; }
+    if (std::string(e) == "v7") { c->gemm_v = 6; c->gemm5_var = 4; }
+    if (std::string(e) == "v7b") { c->gemm_v = 6; c->gemm5_var = 5; }
+    if (std::string(e) == "v8") { c->gemm_v = 6; c->gemm5_var = 6; }
+    if (std::string(e) == "v8b") { c->gemm_v = 6; c->gemm5_var = 7; }
+    if (std::string(e) == "v8c") { c->gemm_v = 6; c->gemm5_var = 8; }
   }
   if (const char* e = getenv("RBA_GEMM_PANEL")) {
     const std::string v(e);
@@ -935,6 +936,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     if (v == "v5") { c->panel_v = 5; c->panel_var = 0; }
   }
   if (const char* e = getenv("RBA_GREEN")) c->green_req = std::string(e) != "0";
+  if (const char* e = getenv("RBA_TRSM_VAR")) c->gemm_var = atoi(e) ? 1 : 0;
   if (const char* e = getenv("RBA_GREEN_PRUNE")) c->green_prune = std::string(e) != "0";
   if (const char* e = getenv("RBA_GREEN_GEMM")) c->green_gemm = std::string(e) != "0";
   if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) == "fused";
