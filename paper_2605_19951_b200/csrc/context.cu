@@ -166,7 +166,8 @@ struct rba_ctx {
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // per-kernel-class device time (CUDA events around every launch, enabled
   // by rba_set_timing) and the launch count of this context's kernels
-  double cls_ms[128] = {0};   // 0-15 kernel classes; 16+L fwd, 48+L bwd, 80+L factor per level
+  double cls_ms[128] = {0};   // 0-15 kernel classes; 16+L fwd, 48+L bwd, 80+L factor,
+                              // 112+L GEMM per level
   bool gemm_dfma = false;     // RBA_GEMM=dfma selects the DFMA reference kernels
   int gemm_v = 6;             // default 3M DMMA kernel (k_gemm6); RBA_GEMM=v3..v7b select
                               // the earlier kernels for A/B tests
@@ -527,6 +528,7 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
       }
       case ST_GEMM: {
         Timed t(c, KC_GEMM);
+        Timed tg(c, 112 + std::min(s.level, 15), 0);   // GEMM time per level
         if (!s.schur && c->panel_v > 0) {
           // panel (look-ahead / aggregated) updates: short K, own kernel choice
           if (c->panel_v == 5)

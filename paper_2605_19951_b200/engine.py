@@ -308,7 +308,8 @@ class Engine:
         check(self.lib.rba_timings_detail(self.ctx, ptr(out)))
         return {"solve_fwd_by_level": out[16:48].round(3).tolist(),
                 "solve_bwd_by_level": out[48:80].round(3).tolist(),
-                "factor_by_level": out[80:112].round(3).tolist()}
+                "factor_by_level": out[80:112].round(3).tolist(),
+                "gemm_by_level": out[112:128].round(3).tolist()}
 
     def sync(self):
         check(self.lib.rba_sync(self.ctx))
