@@ -688,6 +688,8 @@ int ensure_slots(rba_ctx* c) {
       c->jvp_w = (z0 + wn <= cap && !(e && std::string(e) == "0")) ? pool + z0 : nullptr;
     }
     if (c->green) {
+      // enough J v row chunks to fill the GPU when few poles are local
+      c->green_chunks = std::max(64, (148 * 8 + nl - 1) / nl);
       for (int l = 0; l < nl; ++l) c->Z[l] = pool + (size_t)l * zsz;
       const size_t nzf = (size_t)(c->nblocks + 1) * ((c->Mr + 31) / 32);
       c->zflags.assign(nl, nullptr);

@@ -306,7 +306,10 @@ __global__ void __launch_bounds__(32 * NW) k_bwd(const SolveTask* __restrict__ t
   }
   // later pivot blocks of this front (produced by earlier tickets in this
   // launch): per-warp wait, L2 reads
-  for (int rb = npb - 1; rb > cb; --rb) {
+  // with two column passes the dependent block cb+1 is handled after both
+  // passes (below), so the second pass does not re-stream every later block
+  // after the chain wait
+  for (int rb = npb - 1; rb > (NPASS > 1 ? cb + 1 : cb); --rb) {
     const int q0 = rb * PB, q1 = min(q0 + PB, p);
     // the block's 64 rows = 2 per lane: load L before waiting for x
     cplx lv[2][CPW];
@@ -353,6 +356,58 @@ __global__ void __launch_bounds__(32 * NW) k_bwd(const SolveTask* __restrict__ t
         for (int r = 0; r < NR; ++r) red[cw + k][r] = acc[k][r];
   }
   __syncthreads();
+  }
+  if (NPASS > 1 && cb + 1 < npb) {
+    const int q0 = (cb + 1) * PB, q1 = min(q0 + PB, p);
+    if (lane == 0)
+      spin_wait_geq(flags + cb + 1, epoch);
+    __syncwarp();
+    for (int pass = 0; pass < NPASS; ++pass) {
+      const int cw = (pass * NW + warp) * CPW;
+      const int nk = max(0, min(CPW, ncol - cw));
+      const cplx* colp = panel + (int64_t)(c0 + cw) * nf;
+      cplx acc[CPW][NR];
+#pragma unroll
+      for (int k = 0; k < CPW; ++k)
+#pragma unroll
+        for (int r = 0; r < NR; ++r) acc[k][r] = cmk(0.0, 0.0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int rho = q0 + lane + 32 * h;
+        if (rho < q1) {
+          cplx lv[CPW];
+#pragma unroll
+          for (int k = 0; k < CPW; ++k)
+            lv[k] = k < nk ? __ldg(colp + (int64_t)k * nf + rho) : cmk(0.0, 0.0);
+#pragma unroll
+          for (int r = 0; r < NR; ++r) {
+            const cplx xv = ldcg_c(x + (int64_t)(first + rho) * NR + r);
+#pragma unroll
+            for (int k = 0; k < CPW; ++k) acc[k][r] = cfma(lv[k], xv, acc[k][r]);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < CPW; ++k)
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+          double re = acc[k][r].x, im = acc[k][r].y;
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            re += __shfl_xor_sync(0xffffffffu, re, o);
+            im += __shfl_xor_sync(0xffffffffu, im, o);
+          }
+          acc[k][r] = cmk(re, im);
+        }
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < CPW; ++k)
+          if (k < nk)
+#pragma unroll
+            for (int r = 0; r < NR; ++r) red[cw + k][r] = cadd(red[cw + k][r], acc[k][r]);
+      }
+    }
+    __syncthreads();
   }
   asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
