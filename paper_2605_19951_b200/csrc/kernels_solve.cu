@@ -48,7 +48,7 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 // L2 load per lane (they were produced by other CTAs) and broadcasts them with
 // shuffles.  16 L loads per lane are in flight per block.
 template <int NR, bool STAGEX>
-__global__ void __launch_bounds__(256, 2) k_fwd(const SolveTask* __restrict__ tasks, int nslots,
+__global__ void __launch_bounds__(256, NR >= 8 ? 1 : 2) k_fwd(const SolveTask* __restrict__ tasks, int nslots,
                                              FrontsDev F, SolveBatchDev sb, int* ticket,
                                              int /*unused*/, SweepDeps dep) {
   __shared__ int s_t;
