@@ -938,6 +938,12 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     for (int q = 0; q < 7; ++q)
       if (v == names[q]) { c->panel_v = 6; c->panel_var = q; }
     if (v == "v5") { c->panel_v = 5; c->panel_var = 0; }
+    // the per-front tensor maps have one box width: two tensor-map variants
+    // with different boxes cannot share them -> the panel updates follow RBA_GEMM
+    auto boxk = [](int var) { return var == 7 ? 12 : var == 8 ? 16 : var == 6 ? 8 : 0; };
+    if (c->panel_v == 6 && c->gemm_v == 6 && boxk(c->panel_var) && boxk(c->gemm5_var) &&
+        boxk(c->panel_var) != boxk(c->gemm5_var))
+      c->panel_v = 0;
   }
   if (const char* e = getenv("RBA_GREEN")) c->green_req = std::string(e) != "0";
   if (const char* e = getenv("RBA_TRSM_VAR")) c->gemm_var = atoi(e) ? 1 : 0;
