@@ -314,12 +314,20 @@ int build_plans(rba_ctx* c) {
     for (int q = q0; q < q1; ++q) kmax = std::max(kmax, (S.npiv[S.level_fronts[q]] + rba::PB - 1) / rba::PB);
     for (int kk = 0; kk < kmax; ++kk) {
       const int k0 = kk * rba::PB;
+      // diagonal blocks of at most 32 pivots first (k_diag2<32>: 128 threads,
+      // 4x less shared memory), then the full ones
       int64_t doff = pt.size();
       for (int q = q0; q < q1; ++q) {
         int s = S.level_fronts[q];
-        if (S.npiv[s] > k0) pt.push_back({s, k0, k0, 0});
+        if (S.npiv[s] > k0 && S.npiv[s] - k0 <= 32) pt.push_back({s, k0, k0, 0});
       }
-      if ((int64_t)pt.size() > doff) c->plan.push_back({ST_DIAG, doff, (int)(pt.size() - doff), 0});
+      const int nsmall = (int)(pt.size() - doff);
+      for (int q = q0; q < q1; ++q) {
+        int s = S.level_fronts[q];
+        if (S.npiv[s] - k0 > 32) pt.push_back({s, k0, k0, 0});
+      }
+      if ((int64_t)pt.size() > doff)
+        c->plan.push_back({ST_DIAG, doff, (int)(pt.size() - doff), c->diag_v1 ? 0 : nsmall});
       int64_t toff = pt.size();
       for (int q = q0; q < q1; ++q) {
         int s = S.level_fronts[q];
@@ -511,11 +519,11 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
     switch (s.kind) {
       case ST_EA: { Timed t(c, KC_EA); rba::launch_extend_add(c->st, c->ea_tasks + s.off, s.n, c->F, pb); break; }
       case ST_DIAG: {
-        Timed t(c, KC_DIAG);
+        Timed t(c, KC_DIAG, (s.ntiles > 0 && s.ntiles < s.n) ? 2 : 1);
         if (c->diag_v1)
           rba::launch_diag(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d);
         else
-          rba::launch_diag2(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d);
+          rba::launch_diag2(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d, s.ntiles);
         break;
       }
       case ST_TRSM: {

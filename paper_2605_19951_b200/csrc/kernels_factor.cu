@@ -211,21 +211,24 @@ __global__ void __launch_bounds__(256) k_diag(const PanelTask* __restrict__ task
 // (X_ij = -X_ii sum_k L_ik X_kj).
 constexpr int SB = 16;
 
-__global__ void __launch_bounds__(256) k_diag2(const PanelTask* __restrict__ tasks, FrontsDev F,
+template <int BK>   // maximum block size: 64 (PB), or 32 (small fronts: 128 threads,
+                   // 4x less shared memory, several more CTAs per SM)
+__global__ void __launch_bounds__(BK == 32 ? 128 : 256) k_diag2(const PanelTask* __restrict__ tasks, FrontsDev F,
                                                PoleBatch pb, int* err) {
   // Dg holds L (lower) and, transposed in the free upper triangle, X = L^{-1}
   // (X[i][j], i > j, at Dg[j][i]) -- exactly the panel layout written back.
   // Ts is one 16-row block row of T; 85 KB in all -> 2 CTAs per SM.
+  constexpr int LDS = BK + 1;
   extern __shared__ cplx sm[];
-  cplx* Dg = sm;                   // [PB][LDS]
-  cplx* Ts = sm + PB * LDS;        // [SB][LDS]
-  cplx* dv = Ts + SB * LDS;        // [PB]
-  cplx* di = dv + PB;              // [PB]
+  cplx* Dg = sm;                   // [BK][LDS]
+  cplx* Ts = sm + BK * LDS;        // [SB][LDS]
+  cplx* dv = Ts + SB * LDS;        // [BK]
+  cplx* di = dv + BK;              // [BK]
   const int slot = blockIdx.y;
   const PanelTask tk = tasks[blockIdx.x];
   const int s = tk.s, k0 = tk.k0;
   const int nf = F.nf[s], p = F.npiv[s];
-  const int kb = min(PB, p - k0);
+  const int kb = min(BK, p - k0);
   cplx* panel = pb.factor[slot] + F.panel_off[s];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int idx = tid; idx < kb * kb; idx += blockDim.x) {
@@ -326,17 +329,25 @@ __global__ void __launch_bounds__(256) k_diag2(const PanelTask* __restrict__ tas
   }
 }
 
-void launch_diag2(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
-                  const PoleBatch& pb, int* err) {
+template <int BK>
+static void diag2_go(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
+                     const PoleBatch& pb, int* err) {
   if (ntasks <= 0) return;
-  size_t smem = ((PB + SB) * LDS + 2 * PB) * sizeof(cplx);
+  const size_t smem = ((BK + SB) * (BK + 1) + 2 * BK) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_diag2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_diag2<BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
   dim3 grid(ntasks, pb.count);
-  k_diag2<<<grid, 256, smem, st>>>(tasks, F, pb, err);
+  k_diag2<BK><<<grid, BK == 32 ? 128 : 256, smem, st>>>(tasks, F, pb, err);
+}
+
+// the first nsmall tasks have blocks of at most 32 pivots (build_plans)
+void launch_diag2(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
+                  const PoleBatch& pb, int* err, int nsmall) {
+  diag2_go<32>(st, tasks, nsmall, F, pb, err);
+  diag2_go<PB>(st, tasks + nsmall, ntasks - nsmall, F, pb, err);
 }
 
 // K4a': panel TRSM  L_r = F_r L_kk^{-T} D^{-1}  for one 64-row tile per CTA
