@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ t
     issue(ch + NS3 - 1);
     const St& S = st[ch % NS3];
     const int kt = t0 + ch * T3K;
+    if (cc0 + wn >= cmax) continue;     // warp's 16 columns all past the block / tile edge
 #pragma unroll
     for (int k4 = 0; k4 < T3K; k4 += 4) {
       double ar[4], ai[4], an[4], br[2], bi[2];
@@ -528,7 +529,7 @@ __global__ void __launch_bounds__(NCOL * 4, NCOL == 32 ? 2 : 1) k_gemm6(
   const int g = lane >> 2, t4 = lane & 3;
   // a warp whose 32x16 block lies strictly above the diagonal only keeps the
   // stage protocol going
-  const bool active = r0 + wm + 31 >= cc0 + wn && r0 + wm < nf;
+  const bool active = r0 + wm + 31 >= cc0 + wn && r0 + wm < nf && cc0 + wn < cmax;
   const int nchunks = (t1 - t0 + G6K - 1) / G6K;
   const unsigned na = (unsigned)min(GT, nf - r0) * 16u;
   const unsigned nb = (unsigned)min(NCOL, nf - cc0) * 16u;
