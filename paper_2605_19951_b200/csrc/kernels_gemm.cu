@@ -159,7 +159,8 @@ __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ t
     issue(ch + NS3 - 1);
     const St& S = st[ch % NS3];
     const int kt = t0 + ch * T3K;
-    if (cc0 + wn >= cmax) continue;     // warp's 16 columns all past the block / tile edge
+    // warp's 16 columns all past the block / tile edge, or 32 rows past the front
+    if (cc0 + wn >= cmax || r0 + wm >= nf) continue;
 #pragma unroll
     for (int k4 = 0; k4 < T3K; k4 += 4) {
       double ar[4], ai[4], an[4], br[2], bi[2];

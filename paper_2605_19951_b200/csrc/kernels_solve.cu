@@ -898,6 +898,7 @@ __global__ void __launch_bounds__(128) k_zbwd(const SolveTask* __restrict__ task
       __syncthreads();
       issue(ch + ZNS - 1);
       const ZStage& S = st[ch % ZNS];
+      if (wm >= kb || wn >= nm) continue;   // warp tile entirely outside the block / chunk
 #pragma unroll
       for (int k4 = 0; k4 < ZK; k4 += 4) {
         double ar[4], ai[4], an[4], br[2], bi[2];
