@@ -105,8 +105,10 @@ int rba_factor_values(rba_ctx* ctx, int32_t slot, const double* values_h);
  * rows/cols (int32) and the assembled K / M values in that order. */
 int rba_pattern(rba_ctx* ctx, int64_t* nnz, int32_t* rows_h, int32_t* cols_h, double* K_h,
                 double* M_h);
-/* x = A_i^{-1} rhs (trans 'N' or 'T': identical, A_i is complex symmetric);
- * rhs/out: column-major N x nrhs complex (cache.solve, shifted.py:107-116). */
+/* x = A_i^{-1} rhs, trans 0 'N' / 1 'T' (identical: A_i is complex symmetric)
+ * or 2 'H' (conj(A_i^{-1} conj(rhs))); other values -> RBA_ERR_INVALID
+ * (_Factor.solve(rhs, trans), shifted.py:58-61; cache.solve :107-116).
+ * rhs/out: column-major N x nrhs complex. */
 int rba_solve(rba_ctx* ctx, int32_t slot, const double* rhs_h, double* out_h, int32_t nrhs,
               int32_t trans);
 int rba_solve_d(rba_ctx* ctx, int32_t slot, const double* rhs_d, double* out_d, int32_t nrhs,
@@ -126,6 +128,18 @@ int rba_vjp_partial(rba_ctx* ctx, const double* w_d, double* tpart_d);
 /* g_i of local slot `slot` after rba_forward_partial: column-major N x S
  * complex, original dof order (ForwardResult fields / pole_solutions). */
 int rba_get_g(rba_ctx* ctx, int32_t slot, double* out_h);
+/* Same into a device buffer (N x S complex, column-major): the per-rank
+ * pole solutions all-gathered by solve_all_poles at G > 1 (shifted.py:176-199). */
+int rba_get_g_d(rba_ctx* ctx, int32_t slot, double* out_d);
+/* Replace g_i of a local slot by caller-supplied pole solutions (host,
+ * N x S complex column-major, original order): JacobianOperator built from
+ * given pole_solutions (sensitivity.py:43-59) contracts dM with those. */
+int rba_set_g(rba_ctx* ctx, int32_t slot, const double* g_h);
+/* Stability report of a local slot's pivot-free LDL^T (no SciPy analogue;
+ * SuperLU pivots, shifted.py:54): out[4] = max |L'| (L' = L D^{1/2}),
+ * min |sqrt(d)|, max |sqrt(d)|, number of non-finite factor entries.
+ * Growth = max|L'|^2 / max|A|, smallest pivot = min|sqrt(d)|^2 / max|A|. */
+int rba_factor_stats(rba_ctx* ctx, int32_t slot, double* out_h);
 /* Copy the factor storage of a local slot (panel_total complex entries;
  * per-front nf x npiv column-major panels at symbolic panel_off) -- used by
  * the structure-level parity tests against the host emulation.  Format
@@ -149,6 +163,14 @@ int rba_set_reg(rba_ctx* ctx, int64_t nrows, const int64_t* indptr_h, const int3
 /* y = alpha R x (+ y if accumulate), transpose=1: y = alpha R^T x (+ y) */
 int rba_reg_apply(rba_ctx* ctx, int32_t transpose, const double* x_d, double alpha, double* y_d,
                   int32_t accumulate);
+/* The regulariser operator L = D Mdiv^-1 D^T + eps diag(meas) (P x P CSR,
+ * regularization.py:55-63) and y = alpha L x (+ y): reg_value_grad
+ * (regularization.py:71-75) and the GN gradient term lambda L (m - m_ref)
+ * (inversion.py:250) on the device. */
+int rba_set_reg_L(rba_ctx* ctx, int64_t n, const int64_t* indptr_h, const int32_t* indices_h,
+                  const double* data_h);
+int rba_reg_L_apply(rba_ctx* ctx, const double* x_d, double alpha, double* y_d,
+                    int32_t accumulate);
 /* LSQR vector kernels (SciPy lsqr recurrences, inversion.py:153) */
 int rba_vec_axpby(rba_ctx* ctx, int64_t n, double a, const double* x_d, double b,
                   const double* y_d, double* out_d);
@@ -164,6 +186,15 @@ int rba_info(rba_ctx* ctx, int64_t* out_h);
 /* bytes of device memory held by the context: factors, workspace, other */
 int rba_memory(rba_ctx* ctx, int64_t* out_h);
 int rba_sync(rba_ctx* ctx);
+/* Context options:
+ *  "green" 0|1        -- 0 disables the receiver-Green mode (per-action
+ *                        sweeps); ranks of one job agree on the mode
+ *  "lazy_factors" 0|1 -- allocate a slot's factor storage on its first
+ *                        factorisation (generic mode: the reference's
+ *                        cache.factorize(i, A), shifted.py:98-105, where the
+ *                        pole count is not known up front); set before
+ *                        rba_set_poles. */
+int rba_set_option(rba_ctx* ctx, const char* name, int64_t value);
 /* Device time per kernel class (ms, CUDA events around every launch while
  * timing is enabled), out[16]: scatter, extend-add, diag, trsm, gemm,
  * solve-fwd, solve-bwd, element/observation, vector/SpMV, M assembly, ...,

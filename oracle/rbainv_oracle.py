@@ -21,6 +21,7 @@ in ascending order.
 from __future__ import annotations
 
 import hashlib
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 import scipy.linalg as la
@@ -78,8 +79,12 @@ class PoleFactors:
     """shifted.py:44-122: SuperLU factor per pole of A_i = K - xi_i M(m),
     keyed by the model tag; counters as CacheCounters (shifted.py:64-70)."""
 
-    def __init__(self, permc_spec: str = "COLAMD"):
+    def __init__(self, permc_spec: str = "COLAMD", workers: int = 1):
         self.permc_spec = permc_spec     # SuperLU ordering (reference default: COLAMD)
+        # PoleWorkerPool (shifted.py:129-155): worker p owns poles i mod W;
+        # SuperLU releases the GIL, so threads factorise/solve poles in parallel
+        self.workers = max(1, int(workers))
+        self._pool = ThreadPoolExecutor(self.workers) if self.workers > 1 else None
         self.tag = None
         self.lu = {}
         self.A = {}
@@ -96,6 +101,20 @@ class PoleFactors:
         self.solves += 1
         return self.lu[i].solve(np.asarray(rhs, dtype=complex), trans=trans)
 
+    def map_poles(self, fn, count):
+        """shifted.py:140-155: pole-indexed results, worker p runs i = p, p+W, ..."""
+        if self._pool is None:
+            return [fn(i) for i in range(count)]
+        W = self.workers
+
+        def run(p):
+            return [(i, fn(i)) for i in range(p, count, W)]
+        out = [None] * count
+        for chunk in self._pool.map(run, range(W)):
+            for i, r in chunk:
+                out[i] = r
+        return out
+
 
 def factorize_all_poles(problem, m, poles, fac: PoleFactors):
     """shifted.py:158-173"""
@@ -105,13 +124,18 @@ def factorize_all_poles(problem, m, poles, fac: PoleFactors):
         return
     M = assemble_M(problem, m).astype(complex).tocsc()
     K = problem.K.astype(complex).tocsc()
-    for i in missing:
+
+    def one(k):
+        i = missing[k]
         A = K - poles[i] * M
         try:
-            fac.lu[i] = spla.splu(A.tocsc(), permc_spec=fac.permc_spec)
+            lu = spla.splu(A.tocsc(), permc_spec=fac.permc_spec)
         except Exception as exc:  # shifted.py:55-56
             raise RuntimeError(f"factorization of shifted matrix failed: {exc}") from exc
-        fac.A[i] = A.tocsr()
+        return i, lu, A.tocsr()
+    for i, lu, A in fac.map_poles(one, len(missing)):
+        fac.lu[i] = lu
+        fac.A[i] = A
         fac.factorizations += 1
 
 
@@ -121,8 +145,9 @@ def solve_all_poles(problem, m, poles, rhs, fac: PoleFactors, check_residuals=Fa
     rhs = np.asarray(rhs)
     out = []
     nrm = np.linalg.norm(rhs)
+    gs = fac.map_poles(lambda i: fac.solve(i, rhs), len(poles))
     for i in range(len(poles)):
-        g = fac.solve(i, rhs)
+        g = gs[i]
         if check_residuals and nrm > 0:
             res = np.linalg.norm(fac.A[i] @ g - rhs) / nrm
             if res > 1e-8:
@@ -180,10 +205,10 @@ class Jacobian:
         out = []
         for s in range(self.S):
             D = np.zeros((self.n_chan, self.n_recv))
+            qs = self.fac.map_poles(
+                lambda i: self.problem.Q @ self.fac.solve(i, self.dM[s][i] @ v), len(self.poles))
             for i in range(len(self.poles)):
-                h = self.fac.solve(i, self.dM[s][i] @ v)
-                q = self.problem.Q @ h
-                D += 2.0 * np.real(self.poles[i] * np.outer(self.residues[i], q))
+                D += 2.0 * np.real(self.poles[i] * np.outer(self.residues[i], qs[i]))
             out.append(D.ravel())
         return np.concatenate(out)
 
@@ -194,10 +219,11 @@ class Jacobian:
         for s in range(self.S):
             Qt_w = self.problem.Q.T @ w[s].T
             out = np.zeros(self.shape[1])
+            ts = self.fac.map_poles(
+                lambda i: self.dM[s][i].T @ self.fac.solve(i, Qt_w @ self.residues[i], trans="T"),
+                len(self.poles))
             for i in range(len(self.poles)):
-                y = Qt_w @ self.residues[i]
-                z = self.fac.solve(i, y, trans="T")
-                out += 2.0 * np.real(self.poles[i] * (self.dM[s][i].T @ z))
+                out += 2.0 * np.real(self.poles[i] * ts[i])
             total = total + out if s else out
         return total
 
@@ -299,8 +325,41 @@ def gn_step(problem, m, m_ref, poles, residues, R, weights, d_obs, lam, tol, max
     return dm, itn, istop, d_pred
 
 
+def gn_iteration(problem, m, m_ref, poles, residues, R, L, weights, d_obs, lam, iters,
+                 fac: PoleFactors, d_pred=None, g=None, c1=1e-4, eta_min=2.0 ** -6):
+    """One Gauss-Newton iteration of run_inversion (inversion.py:240-300):
+    operator from the current g, gradient J^T(W^2 (d - d_obs)) + lam L (m - m_ref),
+    LSQR (tol 0, `iters` iterations), Armijo line search whose every trial
+    refactorises all poles (forward_at, inversion.py:223-228).  Returns
+    (m_new, accepted, eta, n_evals, d_new, g_new)."""
+    W = weights
+    if d_pred is None or g is None:
+        d_pred, g = forward_response(problem, m, poles, residues, fac)
+    J = Jacobian(problem, m, poles, residues, fac, g=g)
+    grad = J.vjp(W * W * (d_pred - d_obs)) + lam * (L @ (m - m_ref))
+    dm, _, _ = augmented_lsqr(J, R, W, d_obs, d_pred, m, m_ref, lam, 0.0, iters)
+    slope = float(grad @ dm)
+
+    def phi_of(mm, d):
+        r = mm - m_ref
+        return 0.5 * float(np.sum((W * (d - d_obs)) ** 2)) + lam * 0.5 * float(r @ (L @ r))
+    phi0 = phi_of(m, d_pred)
+    evals = {}
+
+    def ev(eta):
+        mm = m + eta * dm
+        d, gg = forward_response(problem, mm, poles, residues, fac)
+        evals[eta] = (mm, d, gg)
+        return phi_of(mm, d)
+    eta, ok, _, n = line_search(phi0, slope, ev, c1=c1, eta_min=eta_min)
+    if ok:
+        mm, d, gg = evals[eta]
+        return mm, True, eta, n, d, gg
+    return m, False, eta, n, d_pred, g
+
+
 def lsqr_floor(problem, m, poles, residues, R, weights, d_obs, lam, iters, orderings=(
-        "COLAMD", "MMD_AT_PLUS_A")):
+        "COLAMD", "MMD_AT_PLUS_A"), m_ref=None):
     """The reference's own solver-to-solver floor on the GN update:
     relative difference of dm computed with two SuperLU orderings."""
     out = []
@@ -308,7 +367,8 @@ def lsqr_floor(problem, m, poles, residues, R, weights, d_obs, lam, iters, order
         fac = PoleFactors(spec)
         d, g = forward_response(problem, m, poles, residues, fac)
         J = Jacobian(problem, m, poles, residues, fac, g=g)
-        dm, _, _ = augmented_lsqr(J, R, weights, d_obs, d, m, m, lam, 0.0, iters)
+        dm, _, _ = augmented_lsqr(J, R, weights, d_obs, d, m, m if m_ref is None else m_ref,
+                                  lam, 0.0, iters)
         out.append(dm)
     return float(np.linalg.norm(out[0] - out[1]) / np.linalg.norm(out[0])), out[0]
 

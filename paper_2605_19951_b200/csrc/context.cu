@@ -153,6 +153,15 @@ struct rba_ctx {
   int32_t *r_idx = nullptr, *rt_idx = nullptr;
   double *r_val = nullptr, *rt_val = nullptr;
   std::vector<void*> reg_allocs;
+  // regulariser operator L (P x P CSR): reg_value_grad on the device
+  int64_t L_n = 0;
+  int64_t* l_ptr = nullptr;
+  int32_t* l_idx = nullptr;
+  double* l_val = nullptr;
+  std::vector<void*> regl_allocs;
+  // factor buffers allocated on first use of a slot (generic mode: the
+  // reference's factorize(i, A) with an unknown pole count); one update arena
+  bool lazy = false;
   // misc
   double* red_part = nullptr;
   double* red_res = nullptr;
@@ -630,6 +639,16 @@ int tmap_boxk(const rba_ctx* c) {
   return v == 7 ? 12 : v == 8 ? 16 : rba::G8K;
 }
 
+int ensure_factor(rba_ctx* c, int l) {
+  if (c->factor[l]) return RBA_OK;
+  const rba::Symbolic& S = c->sym;
+  int rc;
+  if ((rc = dalloc(c, c->pole_allocs, &c->factor[l], S.panel_off[S.nfront], &c->mem_factor))) return rc;
+  if ((c->gemm_v == 6 && c->gemm5_var >= 6) || (c->panel_v == 6 && c->panel_var >= 6))
+    if ((rc = make_tmaps(c, c->factor[l], &c->tmaps[l], tmap_boxk(c)))) return rc;
+  return RBA_OK;
+}
+
 int ensure_slots(rba_ctx* c) {
   if (!c->factor.empty()) return RBA_OK;
   const int nl = (int)c->local.size();
@@ -644,9 +663,7 @@ int ensure_slots(rba_ctx* c) {
   c->valid.assign(nl, 0);
   c->NRw = c->NRs;
   for (int l = 0; l < nl; ++l) {
-    if ((rc = dalloc(c, c->pole_allocs, &c->factor[l], S.panel_off[S.nfront], &c->mem_factor))) return rc;
-    if (c->gemm_v == 6 && c->gemm5_var >= 6 || c->panel_v == 6 && c->panel_var >= 6)
-      if ((rc = make_tmaps(c, c->factor[l], &c->tmaps[l], tmap_boxk(c)))) return rc;
+    if (!c->lazy && (rc = ensure_factor(c, l))) return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->g[l], (size_t)c->N * c->NRw, &c->mem_work))) return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->x[l], (size_t)c->N * c->NRw, &c->mem_work))) return rc;
     if ((rc = dalloc(c, c->pole_allocs, &c->uvec[l], (size_t)std::max<int64_t>(S.uvec_off[S.nfront], 1) * c->NRw, &c->mem_work))) return rc;
@@ -670,6 +687,7 @@ int ensure_slots(rba_ctx* c) {
     for (int k = 2; k <= 8 && k <= nl; ++k)
       if (fr > k * need + ((size_t)8 << 30)) c->fbatch = k;
     if (const char* e = getenv("RBA_FACTOR_BATCH")) c->fbatch = std::max(1, std::min(atoi(e), nl));
+    if (c->lazy) c->fbatch = 1;
     // The receiver Green's functions Z_l (needed between a factorisation and
     // the next one: J v / J^T w) and the update arenas (needed only inside a
     // factorisation) are never live together, so they share one allocation;
@@ -678,7 +696,8 @@ int ensure_slots(rba_ctx* c) {
     const size_t zsz = (size_t)c->N * std::max<int64_t>(c->Mr, 1);
     const size_t zall = (size_t)nl * zsz;
     const size_t extra = zall > arenas ? (zall - arenas) * sizeof(cplx) : 0;
-    c->green = c->green_req && c->Mr > 0 && fr > (size_t)c->fbatch * need + extra + ((size_t)8 << 30);
+    c->green = c->green_req && !c->lazy && c->Mr > 0 &&
+               fr > (size_t)c->fbatch * need + extra + ((size_t)8 << 30);
     cplx* pool = nullptr;
     if ((rc = dalloc(c, c->pole_allocs, &pool, c->green ? std::max(arenas, zall) : arenas, &c->mem_work)))
       return rc;
@@ -696,8 +715,10 @@ int ensure_slots(rba_ctx* c) {
       c->jvp_w = (z0 + wn <= cap && !(e && std::string(e) == "0")) ? pool + z0 : nullptr;
     }
     if (c->green) {
-      // enough J v row chunks to fill the GPU when few poles are local
-      c->green_chunks = std::max(64, (148 * 8 + nl - 1) / nl);
+      // J v row chunks of a fixed 2048 rows: the partial-sum order depends on
+      // N only, never on the poles per GPU, so J v is bitwise independent of
+      // the GPU count (C4: 324 chunks -> 648 CTAs with 2 poles per GPU)
+      c->green_chunks = (int)std::max<int64_t>(1, (c->N + 2047) / 2048);
       for (int l = 0; l < nl; ++l) c->Z[l] = pool + (size_t)l * zsz;
       const size_t nzf = (size_t)(c->nblocks + 1) * ((c->Mr + 31) / 32);
       c->zflags.assign(nl, nullptr);
@@ -981,6 +1002,7 @@ void rba_ctx_destroy(rba_ctx* c) {
   free_slots(c);
   free_list(c->obs_allocs);
   free_list(c->reg_allocs);
+  free_list(c->regl_allocs);
   free_list(c->allocs);
   if (c->stage) cudaFree(c->stage);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
@@ -1161,6 +1183,7 @@ int rba_set_model_d(rba_ctx* c, const double* m_d) {
   }
   CKL();
   for (auto& v : c->valid) v = 0;
+  for (auto& v : c->green_valid) v = 0;   // Z_i belong to the previous model
   c->model_set = true;
   return RBA_OK;
 }
@@ -1190,6 +1213,7 @@ int rba_factor(rba_ctx* c) {
     pb.count = std::min(c->fbatch, nl - b0);
     for (int i = 0; i < pb.count; ++i) {
       int l = b0 + i;
+      if ((rc = ensure_factor(c, l))) return rc;
       c->valid[l] = 0;
       pb.factor[i] = c->factor[l];
       pb.tmap[i] = c->tmaps[l];
@@ -1224,6 +1248,7 @@ int rba_factor_values(rba_ctx* c, int32_t slot, const double* vals) {
   int rc;
   if ((rc = ensure_slots(c))) return rc;
   if ((rc = ensure_stage(c, c->nnzA))) return rc;
+  if ((rc = ensure_factor(c, slot))) return rc;
   const rba::Symbolic& S = c->sym;
   CK(cudaMemcpyAsync(c->stage, vals, c->nnzA * sizeof(cplx), cudaMemcpyHostToDevice, c->st));
   CK(cudaMemsetAsync(c->factor[slot], 0, S.panel_off[S.nfront] * sizeof(cplx), c->st));
@@ -1274,24 +1299,37 @@ static int solve_common(rba_ctx* c, int32_t slot, const cplx* rhs_d, cplx* out_d
   return RBA_OK;
 }
 
+// trans: 0 'N', 1 'T' (A complex symmetric: A^T = A, same solve), 2 'H'
+// (A^{-H} b = conj(A^{-1} conj(b))); anything else is invalid.
 int rba_solve_d(rba_ctx* c, int32_t slot, const double* rhs_d, double* out_d, int32_t nrhs,
                 int32_t trans) {
   if (!c || !rhs_d || !out_d || nrhs < 1) return fail(RBA_ERR_INVALID, "bad arguments");
-  (void)trans;  // complex symmetric: A^T = A
+  if (trans < 0 || trans > 2) return fail(RBA_ERR_INVALID, "trans must be 'N', 'T' or 'H'");
   CK(cudaSetDevice(c->device));
-  return solve_common(c, slot, (const cplx*)rhs_d, (cplx*)out_d, nrhs);
+  if (trans != 2) return solve_common(c, slot, (const cplx*)rhs_d, (cplx*)out_d, nrhs);
+  const int64_t n = c->N * (int64_t)nrhs;
+  int rc;
+  if ((rc = ensure_stage(c, n))) return rc;
+  rba::launch_conj(c->st, n, (const cplx*)rhs_d, c->stage);
+  CKL();
+  if ((rc = solve_common(c, slot, c->stage, (cplx*)out_d, nrhs))) return rc;
+  rba::launch_conj(c->st, n, (const cplx*)out_d, (cplx*)out_d);
+  CKL();
+  return RBA_OK;
 }
 
 int rba_solve(rba_ctx* c, int32_t slot, const double* rhs_h, double* out_h, int32_t nrhs,
               int32_t trans) {
   if (!c || !rhs_h || !out_h || nrhs < 1) return fail(RBA_ERR_INVALID, "bad arguments");
-  (void)trans;
+  if (trans < 0 || trans > 2) return fail(RBA_ERR_INVALID, "trans must be 'N', 'T' or 'H'");
   CK(cudaSetDevice(c->device));
   int rc;
   const int64_t n = c->N * (int64_t)nrhs;
   if ((rc = ensure_stage(c, 2 * n))) return rc;
   CK(cudaMemcpyAsync(c->stage, rhs_h, n * sizeof(cplx), cudaMemcpyHostToDevice, c->st));
+  if (trans == 2) rba::launch_conj(c->st, n, c->stage, c->stage);
   if ((rc = solve_common(c, slot, c->stage, c->stage + n, nrhs))) return rc;
+  if (trans == 2) rba::launch_conj(c->st, n, c->stage + n, c->stage + n);
   CK(cudaMemcpyAsync(out_h, c->stage + n, n * sizeof(cplx), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
   return RBA_OK;
@@ -1629,9 +1667,93 @@ int rba_get_factor(rba_ctx* c, int32_t slot, double* out_h, int64_t count) {
   if (!c || !out_h || slot < 0 || slot >= (int)c->local.size()) return fail(RBA_ERR_INVALID, "bad slot");
   const int64_t tot = c->sym.panel_off[c->sym.nfront];
   if (count < tot) return fail(RBA_ERR_INVALID, "buffer too small");
+  if (!c->factor[slot]) return fail(RBA_ERR_CACHE_MISS, "slot has no factor storage yet");
   CK(cudaSetDevice(c->device));
   CK(cudaMemcpyAsync(out_h, c->factor[slot], tot * sizeof(cplx), cudaMemcpyDeviceToHost, c->st));
   CK(cudaStreamSynchronize(c->st));
+  return RBA_OK;
+}
+
+int rba_get_g_d(rba_ctx* c, int32_t slot, double* out_d) {
+  if (!c || !out_d || slot < 0 || slot >= (int)c->local.size()) return fail(RBA_ERR_INVALID, "bad slot");
+  CK(cudaSetDevice(c->device));
+  rba::launch_perm_out(c->st, c->N, c->S, c->NRs, c->perm_d, c->g[slot], (cplx*)out_d, c->N);
+  CKL();
+  return RBA_OK;
+}
+
+int rba_set_g(rba_ctx* c, int32_t slot, const double* g_h) {
+  if (!c || !g_h || slot < 0 || slot >= (int)c->local.size()) return fail(RBA_ERR_INVALID, "bad slot");
+  CK(cudaSetDevice(c->device));
+  int rc;
+  const int64_t n = c->N * (int64_t)c->S;
+  if ((rc = ensure_stage(c, n))) return rc;
+  CK(cudaMemcpyAsync(c->stage, g_h, n * sizeof(cplx), cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemsetAsync(c->g[slot], 0, (size_t)c->N * c->NRs * sizeof(cplx), c->st));
+  rba::launch_perm_in(c->st, c->N, c->S, c->NRs, c->perm_d, c->stage, c->N, c->g[slot]);
+  CKL();
+  CK(cudaStreamSynchronize(c->st));
+  return RBA_OK;
+}
+
+int rba_factor_stats(rba_ctx* c, int32_t slot, double* out_h) {
+  if (!c || !out_h || slot < 0 || slot >= (int)c->local.size()) return fail(RBA_ERR_INVALID, "bad slot");
+  if (c->valid.empty() || !c->valid[slot])
+    return fail(RBA_ERR_CACHE_MISS, "no factorization for pole " + std::to_string(c->local[slot]));
+  CK(cudaSetDevice(c->device));
+  const double init[4] = {0.0, __builtin_inf(), 0.0, 0.0};
+  CK(cudaMemcpyAsync(c->red_part, init, sizeof(init), cudaMemcpyHostToDevice, c->st));
+  rba::launch_factor_stats(c->st, c->F, c->sym.nfront, c->factor[slot], c->red_part);
+  CKL();
+  CK(cudaMemcpyAsync(out_h, c->red_part, 4 * sizeof(double), cudaMemcpyDeviceToHost, c->st));
+  CK(cudaStreamSynchronize(c->st));
+  return RBA_OK;
+}
+
+int rba_set_option(rba_ctx* c, const char* name, int64_t value) {
+  if (!c || !name) return fail(RBA_ERR_INVALID, "null argument");
+  const std::string n(name);
+  if (n == "green") {
+    // 0: stream per-action sweeps instead of the receiver Green's functions
+    // (ranks of a multi-GPU job agree on the mode so J v / J^T w round the
+    // same way everywhere); 1: request Green mode (only if it was allocated)
+    if (value == 0) { c->green = false; c->green_req = false; return RBA_OK; }
+    if (!c->factor.empty() && !c->green)
+      return fail(RBA_ERR_STATE, "receiver-Green storage was not allocated (memory)");
+    c->green_req = true;
+    return RBA_OK;
+  }
+  if (n == "lazy_factors") {
+    if (!c->factor.empty()) return fail(RBA_ERR_STATE, "set lazy_factors before set_poles");
+    c->lazy = value != 0;
+    return RBA_OK;
+  }
+  return fail(RBA_ERR_INVALID, "unknown option " + n);
+}
+
+int rba_set_reg_L(rba_ctx* c, int64_t n, const int64_t* lp, const int32_t* li, const double* lx) {
+  if (!c || !c->have_mesh || n != c->P || !lp || !li || !lx)
+    return fail(RBA_ERR_INVALID, "L must be P x P CSR");
+  CK(cudaSetDevice(c->device));
+  free_list(c->regl_allocs);
+  const int64_t nnz = lp[n];
+  for (int64_t e = 0; e < nnz; ++e)
+    if (li[e] < 0 || li[e] >= c->P) return fail(RBA_ERR_INVALID, "L index out of range");
+  int rc;
+  if ((rc = upload(c, c->regl_allocs, &c->l_ptr, lp, n + 1)) ||
+      (rc = upload(c, c->regl_allocs, &c->l_idx, li, nnz)) ||
+      (rc = upload(c, c->regl_allocs, &c->l_val, lx, nnz)))
+    return rc;
+  c->L_n = n;
+  CK(cudaStreamSynchronize(c->st));
+  return RBA_OK;
+}
+
+int rba_reg_L_apply(rba_ctx* c, const double* x, double alpha, double* y, int32_t accumulate) {
+  if (!c || !c->l_ptr || !x || !y) return fail(RBA_ERR_STATE, "set_reg_L first");
+  Timed t(c, KC_VEC);
+  rba::launch_spmv(c->st, c->L_n, c->l_ptr, c->l_idx, c->l_val, x, alpha, y, accumulate != 0);
+  CKL();
   return RBA_OK;
 }
 

@@ -117,5 +117,8 @@ void launch_dot(cudaStream_t st, int64_t n, const double* x, const double* y, do
 void launch_lsqr_xw(cudaStream_t st, int64_t n, double t1, double t2, const double* v,
                     double* w, double* x, double* part, double* result);
 void launch_zero_c(cudaStream_t st, int64_t n, cplx* p);
+void launch_conj(cudaStream_t st, int64_t n, const cplx* src, cplx* dst);
+void launch_factor_stats(cudaStream_t st, const FrontsDev& F, int nfront, const cplx* fac,
+                         double* out /* [4] */);
 
 }  // namespace rba

@@ -51,10 +51,14 @@ __global__ void k_jvp_rhs(ElemDev E, const double* __restrict__ v, SlotPtrs g, S
         }
       }
       const double sc = __ldg(E.expm + c) * __ldg(v + c);
+      // rounded product, then add (no FMA contraction): bit-identical to the
+      // two-pass k_jvp_cells + k_jvp_gather, so the choice between the two
+      // (it depends on free memory, i.e. on the poles per GPU) never changes
+      // J v -- results stay bitwise independent of the GPU count
 #pragma unroll
       for (int r = 0; r < NR; ++r) {
-        acc[r].x = fma(loc[r].x, sc, acc[r].x);
-        acc[r].y = fma(loc[r].y, sc, acc[r].y);
+        acc[r].x = __dadd_rn(acc[r].x, __dmul_rn(loc[r].x, sc));
+        acc[r].y = __dadd_rn(acc[r].y, __dmul_rn(loc[r].y, sc));
       }
     }
 #pragma unroll
@@ -95,7 +99,7 @@ __global__ void k_jvp_cells(ElemDev E, const double* __restrict__ v, SlotPtrs g,
           loc.x = fma(mab, gl[b].x, loc.x);
           loc.y = fma(mab, gl[b].y, loc.y);
         }
-        ws[(c * 6 + a) * NR + r] = cmk(loc.x * sc, loc.y * sc);
+        ws[(c * 6 + a) * NR + r] = cmk(__dmul_rn(loc.x, sc), __dmul_rn(loc.y, sc));
       }
     }
   }
@@ -114,7 +118,8 @@ __global__ void k_jvp_gather(ElemDev E, const cplx* __restrict__ w, SlotPtrs out
     for (int64_t q = E.dc_ptr[k]; q < E.dc_ptr[k + 1]; ++q) {
       const cplx* wi = ws + (int64_t)E.dc_item[q] * NR;
 #pragma unroll
-      for (int r = 0; r < NR; ++r) acc[r] = cadd(acc[r], wi[r]);
+      for (int r = 0; r < NR; ++r)
+        acc[r] = cmk(__dadd_rn(acc[r].x, wi[r].x), __dadd_rn(acc[r].y, wi[r].y));
     }
 #pragma unroll
     for (int r = 0; r < NR; ++r) o[k * NR + r] = acc[r];
@@ -664,6 +669,72 @@ __global__ void k_scatter_vals(int64_t nnz, const int64_t* __restrict__ tgt,
 void launch_scatter_vals(cudaStream_t st, int64_t nnz, const int64_t* tgt, const cplx* vals,
                          cplx* factor) {
   k_scatter_vals<<<grid_for(nnz), 256, 0, st>>>(nnz, tgt, vals, factor);
+}
+
+// dst = conj(src)  (trans 'H' solves: A^{-H} b = conj(A^{-1} conj(b)))
+__global__ void k_conj(int64_t n, const cplx* __restrict__ src, cplx* __restrict__ dst) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const cplx v = src[i];
+    dst[i] = cmk(v.x, -v.y);
+  }
+}
+void launch_conj(cudaStream_t st, int64_t n, const cplx* src, cplx* dst) {
+  if (n <= 0) return;
+  k_conj<<<grid_for(n), 256, 0, st>>>(n, src, dst);
+}
+
+// Factor statistics of one pole (stability report of the pivot-free LDL^T):
+// out[0] = max |L'| over the stored factor (L' = L D^{1/2}; inside a diagonal
+// block |L'(r,c)| = |L_bb(r,c)| |s_c|), out[1] = min |s_c|, out[2] = max |s_c|
+// (s_c = sqrt(d_c), so |d_c| = |s_c|^2), out[3] = non-finite entries.
+// Non-negative doubles order like their bit patterns, so max/min are 64-bit
+// integer atomics.
+__global__ void k_factor_stats(FrontsDev F, int nfront, const cplx* __restrict__ fac,
+                               double* __restrict__ out) {
+  double mx = 0.0, mn = __longlong_as_double(0x7ff0000000000000LL), ms = 0.0, bad = 0.0;
+  const int nsplit = gridDim.y;
+  for (int s = blockIdx.x; s < nfront; s += gridDim.x) {
+    const int p = F.npiv[s], nf = F.nf[s];
+    const cplx* pan = fac + F.panel_off[s];
+    for (int c = blockIdx.y; c < p; c += nsplit) {
+      const cplx* col = pan + (int64_t)c * nf;
+      const cplx sc = col[c];
+      const double as = hypot(sc.x, sc.y);
+      const int bend = min(p, (c / PB + 1) * PB);
+      for (int r = c + threadIdx.x; r < nf; r += blockDim.x) {
+        const cplx v = col[r];
+        double a;
+        if (r == c) {
+          a = as;
+          mn = fmin(mn, as);
+          ms = fmax(ms, as);
+        } else {
+          a = hypot(v.x, v.y);
+          if (r < bend) a *= as;
+        }
+        if (!isfinite(a)) bad += 1.0;
+        else mx = fmax(mx, a);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    ms = fmax(ms, __shfl_xor_sync(0xffffffffu, ms, o));
+    bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax((unsigned long long*)out, (unsigned long long)__double_as_longlong(mx));
+    atomicMin((unsigned long long*)(out + 1), (unsigned long long)__double_as_longlong(mn));
+    atomicMax((unsigned long long*)(out + 2), (unsigned long long)__double_as_longlong(ms));
+    if (bad > 0) atomicAdd(out + 3, bad);
+  }
+}
+void launch_factor_stats(cudaStream_t st, const FrontsDev& F, int nfront, const cplx* fac,
+                         double* out) {
+  k_factor_stats<<<dim3(std::min(nfront, 148 * 8), 16), 256, 0, st>>>(F, nfront, fac, out);
 }
 
 }  // namespace rba

@@ -42,7 +42,8 @@ class Engine:
     """Device state for one (problem, approximant) pair."""
 
     def __init__(self, problem, approx=None, device: int | None = None, leaf: int = 64,
-                 comm: parallel.PoleComm | None = None, n_slots: int | None = None):
+                 comm: parallel.PoleComm | None = None, n_slots: int | None = None,
+                 lazy_factors: bool = False):
         self.lib = _lib.load()
         if not torch.cuda.is_available():
             raise RuntimeError("the B200 shifted-solve path needs a CUDA device "
@@ -91,6 +92,8 @@ class Engine:
         self.factored = False
         self.g_valid = False
         self.reg_rows = 0
+        if lazy_factors:
+            self.set_option("lazy_factors", 1)
         if approx is not None:
             self.set_poles(approx)
         elif n_slots:
@@ -129,6 +132,15 @@ class Engine:
         self.qpart = torch.zeros((nl, self.S, max(self.Mr, 1)), dtype=torch.complex128, device=dev)
         self.tpart = torch.zeros((nl, self.P), dtype=torch.float64, device=dev)
         self.slot_of_pole = self.comm.slot_of_pole(self.m)
+        if self.comm.world > 1:
+            # every rank must round J v / J^T w the same way: receiver-Green
+            # mode only if it fits on every rank (it depends on free memory)
+            on = bool(self.info()["green"])
+            if self.comm.agree_min(int(on)) == 0 and on:
+                self.set_option("green", 0)
+
+    def set_option(self, name: str, value: int):
+        check(self.lib.rba_set_option(self.ctx, name.encode(), int(value)))
 
     def _set_dummy_poles(self, n):
         class _A:
@@ -160,6 +172,7 @@ class Engine:
                 raise ValueError("model size does not match grid")
             check(self.lib.rba_set_model(self.ctx, ptr(mh)))
         self.model_tag = tag
+        self.last_m = m                 # the model the current factors belong to
         self.factored = False
         self.g_valid = False
 
@@ -184,22 +197,33 @@ class Engine:
         return rows, cols, Kv, Mv
 
     # ------------------------------------------------------------- operators
+    TRANS = {"N": 0, "T": 1, "H": 2}
+
+    @classmethod
+    def _trans(cls, trans: str) -> int:
+        """_Factor.solve's trans (shifted.py:58-61): 'N', 'T' (= 'N', A complex
+        symmetric) or 'H' (conjugate transpose); anything else is an error."""
+        try:
+            return cls.TRANS[trans]
+        except (KeyError, TypeError):
+            raise ValueError(f"trans must be 'N', 'T' or 'H', got {trans!r}") from None
+
     def solve(self, slot: int, rhs: np.ndarray, trans: str = "N") -> np.ndarray:
+        t = self._trans(trans)
         rhs = np.asarray(rhs, dtype=np.complex128)
         one = rhs.ndim == 1
         B = np.ascontiguousarray(rhs.reshape(self.N, -1).T)       # (nrhs, N) = col-major N x nrhs
         out = np.empty_like(B)
         check(self.lib.rba_solve(self.ctx, int(slot), ptr(B.view(np.float64)),
-                                 ptr(out.view(np.float64)), B.shape[0],
-                                 1 if trans != "N" else 0))
+                                 ptr(out.view(np.float64)), B.shape[0], t))
         return out[0] if one else out.T.copy()
 
     def solve_d(self, slot: int, rhs: torch.Tensor, trans: str = "N") -> torch.Tensor:
+        t = self._trans(trans)
         rhs = rhs.to(self.device, torch.complex128).contiguous()
         out = torch.empty_like(rhs)
         nrhs = 1 if rhs.dim() == 1 else rhs.shape[0]
-        check(self.lib.rba_solve_d(self.ctx, int(slot), ptr(rhs), ptr(out), nrhs,
-                                   1 if trans != "N" else 0))
+        check(self.lib.rba_solve_d(self.ctx, int(slot), ptr(rhs), ptr(out), nrhs, t))
         return out
 
     def download_g(self, slot: int) -> np.ndarray:
@@ -207,6 +231,38 @@ class Engine:
         out = np.empty((self.S, self.N), dtype=np.complex128)
         check(self.lib.rba_get_g(self.ctx, int(slot), ptr(out.view(np.float64))))
         return out.T.copy()
+
+    def g_device(self, slot: int) -> torch.Tensor:
+        """g of a local slot as a (S, N) complex device tensor, original order."""
+        out = torch.empty((self.S, self.N), dtype=torch.complex128, device=self.device)
+        check(self.lib.rba_get_g_d(self.ctx, int(slot), ptr(out)))
+        return out
+
+    def upload_g(self, slot: int, g: np.ndarray):
+        """Replace g of a local slot by given pole solutions, (N,) or (N, S)."""
+        g = np.asarray(g, dtype=np.complex128).reshape(self.N, -1)
+        if g.shape[1] != self.S:
+            raise ValueError(f"pole solutions need {self.S} source column(s)")
+        h = np.ascontiguousarray(g.T)
+        check(self.lib.rba_set_g(self.ctx, int(slot), ptr(h.view(np.float64))))
+
+    def gather_fields(self) -> torch.Tensor:
+        """g_i of ALL poles (m, S, N) on every rank: per-rank local fields,
+        all-gathered (rank-major) and put in global pole order."""
+        nmax = self.comm.n_max(self.m)
+        loc = torch.zeros((nmax, self.S, self.N), dtype=torch.complex128, device=self.device)
+        for slot in range(len(self.local)):
+            loc[slot] = self.g_device(slot)
+        allg = self._gather(loc)
+        idx = torch.as_tensor(self.slot_of_pole.astype(np.int64), device=self.device)
+        return allg.index_select(0, idx)
+
+    def factor_stats(self, slot: int) -> dict:
+        """Pivot-free LDL^T stability report of a local slot (rba_factor_stats)."""
+        out = np.zeros(4)
+        check(self.lib.rba_factor_stats(self.ctx, int(slot), ptr(out)))
+        return {"max_abs_Lp": float(out[0]), "min_abs_sqrt_d": float(out[1]),
+                "max_abs_sqrt_d": float(out[2]), "nonfinite": int(out[3])}
 
     def _gather(self, part):
         return self.comm.gather_partials(part)
@@ -249,6 +305,21 @@ class Engine:
         ri = np.ascontiguousarray(R.indices, dtype=np.int32)
         rx = np.ascontiguousarray(R.data, dtype=np.float64)
         check(self.lib.rba_set_reg(self.ctx, R.shape[0], ptr(rp), ptr(ri), ptr(rx)))
+
+    def set_reg_L(self, L: sp.spmatrix):
+        L = sp.csr_matrix(L)
+        L.sort_indices()
+        if L.shape != (self.P, self.P):
+            raise ValueError("L must be P x P")
+        lp = np.ascontiguousarray(L.indptr, dtype=np.int64)
+        li = np.ascontiguousarray(L.indices, dtype=np.int32)
+        lx = np.ascontiguousarray(L.data, dtype=np.float64)
+        check(self.lib.rba_set_reg_L(self.ctx, self.P, ptr(lp), ptr(li), ptr(lx)))
+
+    def reg_L_apply(self, x: torch.Tensor, out: torch.Tensor, alpha=1.0, accumulate=False):
+        check(self.lib.rba_reg_L_apply(self.ctx, ptr(x), float(alpha), ptr(out),
+                                       1 if accumulate else 0))
+        return out
 
     def reg_apply(self, x: torch.Tensor, out: torch.Tensor, alpha=1.0, transpose=False,
                   accumulate=False):

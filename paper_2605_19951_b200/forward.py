@@ -58,7 +58,7 @@ def forward_response(problem, model, approx, cache: ShiftedFactorCache,
     eng = cache.engine
     fields = None
     if retain_fields or check_residuals:
-        g = eng_fields(eng)                                   # (m, N, S)
+        g = eng_fields(eng)                                   # (m_local, N, S)
         if check_residuals:
             F = problem.source_matrix() if hasattr(problem, "source_matrix") else \
                 np.asarray(problem.f, dtype=float)[None, :]
@@ -72,5 +72,8 @@ def forward_response(problem, model, approx, cache: ShiftedFactorCache,
                             raise SolveError(f"pole {eng.local[i]}: relative residual "
                                              f"{res:.3e} exceeds 1e-8")
         if retain_fields:
-            d, fields = response_from_pole_solutions(problem, approx, g[:, :, 0], True)
+            # every pole's field, gathered across ranks in pole order
+            gall = eng.gather_fields()[:, 0, :].cpu().numpy() if eng.comm.world > 1 \
+                else g[:, :, 0]
+            d, fields = response_from_pole_solutions(problem, approx, gall, True)
     return ForwardResult(data=d, fields=fields, solve_stats=cache.counters.snapshot())

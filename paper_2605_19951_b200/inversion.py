@@ -259,36 +259,59 @@ def lsqr_device(A: _AugmentedOp, b: torch.Tensor, atol: float, btol: float, iter
     return x, istop, itn
 
 
-def _device_reg(opr: JacobianOperator, reg: RegOperator):
-    eng = opr.engine
+def _device_reg(opr, reg: RegOperator):
+    """Upload R (LSQR's square root) and L (reg_value_grad, the gradient term)
+    once per (engine, regulariser)."""
+    eng = getattr(opr, "engine", opr)
     if getattr(eng, "_reg_obj", None) is not reg:
         eng.set_reg(reg.R_factor)
+        eng.set_reg_L(reg.L)
         eng._reg_obj = reg
     return eng.reg_rows
+
+
+def reg_value_grad_device(eng, reg: RegOperator, r: torch.Tensor):
+    """regularization.py:71-75 on the device for r = m - m_ref (device):
+    returns (1/2 r^T L r, L r as a device tensor)."""
+    _device_reg(eng, reg)
+    Lr = torch.empty_like(r)
+    eng.reg_L_apply(r, Lr)
+    return 0.5 * eng.dot(r, Lr), Lr
 
 
 def _augmented_lsqr(opr: JacobianOperator, reg: RegOperator, data, d_pred, model, lam: float,
                     lsqr_cfg: LsqrConfig):
     """inversion.py:133-155 on the device; returns (dm, itn, istop)."""
+    x, itn, istop = _augmented_lsqr_d(opr, reg, data, d_pred, model, lam, lsqr_cfg)
+    return x.cpu().numpy(), itn, istop
+
+
+def _augmented_lsqr_d(opr: JacobianOperator, reg: RegOperator, data, d_pred, model, lam: float,
+                      lsqr_cfg: LsqrConfig, W: torch.Tensor | None = None,
+                      dobs: torch.Tensor | None = None, r: torch.Tensor | None = None):
+    """Same, with dm left on the device (the GN driver's path)."""
     if not isinstance(opr, JacobianOperator):
         raise TypeError("the device LSQR needs the device JacobianOperator")
     eng = opr.engine
     dev = eng.device
     R_rows = _device_reg(opr, reg)
-    W = torch.as_tensor(np.asarray(data.weights, dtype=float), device=dev)
+    if W is None:
+        W = torch.as_tensor(np.asarray(data.weights, dtype=float), device=dev)
     sql = float(np.sqrt(lam))
     A = _AugmentedOp(opr, R_rows, W, sql)
     n_data = W.numel()
     b = torch.empty(n_data + R_rows, dtype=torch.float64, device=dev)
     dp = torch.as_tensor(np.asarray(d_pred, dtype=float) if not isinstance(d_pred, torch.Tensor)
                          else d_pred, device=dev, dtype=torch.float64)
-    dobs = torch.as_tensor(np.asarray(data.d_obs, dtype=float), device=dev)
+    if dobs is None:
+        dobs = torch.as_tensor(np.asarray(data.d_obs, dtype=float), device=dev)
     eng.axpby(1.0, dp, -1.0, dobs, b[:n_data])
     eng.mul(W, b[:n_data], b[:n_data], alpha=-1.0)
-    r = torch.as_tensor(np.asarray(model.m - model.m_ref, dtype=float), device=dev)
+    if r is None:
+        r = torch.as_tensor(np.asarray(model.m - model.m_ref, dtype=float), device=dev)
     eng.reg_apply(r, b[n_data:], alpha=-sql)
     x, istop, itn = lsqr_device(A, b, lsqr_cfg.tol, lsqr_cfg.tol, lsqr_cfg.max_iters)
-    return x.cpu().numpy(), int(itn), int(istop)
+    return x, int(itn), int(istop)
 
 
 def gn_step(state: InversionState, problem, approx, reg: RegOperator, data,
@@ -348,20 +371,44 @@ class GNDriver:
         self.model = Model(np.asarray(m_start, dtype=float), ref.m_ref)
         self.W = data.weights
         self.n_data = data.size
+        self._dv_key = None
         self.g_tag, self.d_pred, self.misfit, self.reg_val = self.forward_at(self.model)
         cfg = self.cfg
         self.lam = cfg.lambda0 if cfg.lambda0 is not None else default_lambda0(
-            problem, data, self.reg, self.d_pred, self.model)
+            problem, data, self.reg, self.d_pred.cpu().numpy(), self.model)
         self.lam_min = self.lam * cfg.lambda_min_factor
         self.phi = self.misfit + self.lam * self.reg_val
         self.chi2 = 2.0 * self.misfit / self.n_data
         self.state = InversionState(model=self.model, lam=self.lam, phi=self.phi, chi2=self.chi2)
         self.increase_streak = 0
 
+    def _vectors(self, eng):
+        """W, W*W and d_obs resident on the device (refreshed when the caller
+        hands in new data arrays)."""
+        key = (id(eng), id(self.W), id(self.data.d_obs))
+        if self._dv_key != key:
+            dev = eng.device
+            self._W_d = torch.as_tensor(np.asarray(self.W, dtype=float), device=dev)
+            self._W2_d = torch.empty_like(self._W_d)
+            eng.mul(self._W_d, self._W_d, self._W2_d)
+            self._dobs_d = torch.as_tensor(np.asarray(self.data.d_obs, dtype=float), device=dev)
+            self._tmp_d = torch.empty_like(self._W_d)
+            self._dv_key = key
+        return self._W_d, self._W2_d, self._dobs_d
+
     def forward_at(self, mdl: Model):
-        d = forward_device(self.problem, mdl, self.approx, self.cache).cpu().numpy()
-        mis = 0.5 * float(np.sum((self.W * (d - self.data.d_obs)) ** 2))
-        rv, _ = reg_value_grad(self.reg, mdl)
+        """inversion.py:223-228 with every vector operation on the device:
+        d (kept in HBM), misfit 1/2|W(d - d_obs)|^2 and reg_value_grad
+        (1/2 r^T L r, device SpMV)."""
+        d = forward_device(self.problem, mdl, self.approx, self.cache)
+        eng = self.cache.engine
+        W, _, dobs = self._vectors(eng)
+        t = self._tmp_d
+        eng.axpby(1.0, d, -1.0, dobs, t)
+        eng.mul(W, t, t)
+        mis = 0.5 * eng.dot(t, t)
+        r = torch.as_tensor(np.asarray(mdl.m - mdl.m_ref, dtype=float), device=eng.device)
+        rv, _ = reg_value_grad_device(eng, self.reg, r)
         return mdl.version_tag(), d, mis, rv
 
     def iterate(self, nu: int) -> bool:
@@ -371,12 +418,21 @@ class GNDriver:
         t0 = time.perf_counter()
         counters0 = cache.counters.snapshot()
         opr = JacobianOperator(self.problem, model, self.approx, cache, self.pool)
-        dev = opr.engine.device
-        residual = torch.as_tensor(self.W * self.W * (self.d_pred - self.data.d_obs), device=dev)
-        grad = opr.vjp_d(residual).cpu().numpy() + self.lam * (self.reg.L @ (model.m - model.m_ref))
-        dm, lsqr_iters, istop = _augmented_lsqr(opr, self.reg, self.data, self.d_pred, model,
-                                                self.lam, cfg.lsqr)
-        slope = float(grad @ dm)
+        eng = opr.engine
+        dev = eng.device
+        W, W2, dobs = self._vectors(eng)
+        # gradient (inversion.py:250): J^T (W*W*(d - d_obs)) + lambda L (m - m_ref)
+        residual = torch.empty_like(W)
+        eng.axpby(1.0, self.d_pred, -1.0, dobs, residual)
+        eng.mul(W2, residual, residual)
+        r = torch.as_tensor(np.asarray(model.m - model.m_ref, dtype=float), device=dev)
+        _, Lr = reg_value_grad_device(eng, self.reg, r)
+        grad = opr.vjp_d(residual)
+        eng.axpby(1.0, grad, self.lam, Lr, grad)
+        dm_d, lsqr_iters, istop = _augmented_lsqr_d(opr, self.reg, self.data, self.d_pred, model,
+                                                    self.lam, cfg.lsqr, W=W, dobs=dobs, r=r)
+        slope = eng.dot(grad, dm_d)
+        dm = dm_d.cpu().numpy()
         evals: dict[float, tuple] = {}
 
         def phi_eval(eta: float) -> float:

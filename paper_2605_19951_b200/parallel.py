@@ -18,7 +18,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-__all__ = ["PoleComm", "owned_poles", "gathered_slot_of_pole"]
+__all__ = ["PoleComm", "ShardComm", "owned_poles", "gathered_slot_of_pole"]
 
 
 def owned_poles(m: int, world: int, rank: int) -> list[int]:
@@ -64,9 +64,34 @@ class PoleComm:
         dist.all_gather_into_tensor(out, src, group=self.group)
         return torch.view_as_complex(out) if part.is_complex() else out
 
+    def agree_min(self, value: int) -> int:
+        """Minimum of an integer over the ranks (mode decisions all ranks share)."""
+        if self.world == 1:
+            return int(value)
+        t = torch.tensor([int(value)], dtype=torch.int64,
+                         device="cuda" if dist.get_backend(self.group) == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.group)
+        return int(t.item())
+
     def n_max(self, m: int) -> int:
         return math.ceil(m / self.world)
 
     def barrier(self):
         if self.world > 1:
             dist.barrier(group=self.group)
+
+
+class ShardComm(PoleComm):
+    """Rank `rank` of a G-rank pole sharding run inside ONE process (no
+    collective): used to time or check each rank's share on one device --
+    scaling_benchmark's per-shard timings, the bitwise multi-GPU tests.  The
+    caller concatenates the shards' partials rank-major itself."""
+
+    def agree_min(self, value: int) -> int:
+        return int(value)
+
+    def gather_partials(self, part):
+        raise RuntimeError("ShardComm has no collective: concatenate the shards' partials")
+
+    def barrier(self):
+        pass

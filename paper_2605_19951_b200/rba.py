@@ -94,6 +94,11 @@ def load_approximant(path) -> RationalApproximant:
 
 
 def config_approximant(name: str) -> RationalApproximant:
-    """Frozen approximant of a BASELINE config (C1: 8 poles; C2-C4: 16; C5: 20)."""
-    key = {"C1": "C1", "C2": "C2", "C3": "C2", "C4": "C2", "C5": "C5"}[name.upper()]
+    """Frozen approximant of a BASELINE config (C1: 8 poles; C2-C4: 16; C5: 20),
+    each fitted by the reference's ``fit_common_pole`` on its own config's
+    spectral interval (tests/golden/make_golden.py: C2 without air reaches
+    8.4e10; C1, C3, C4, C5 with 1e-8 S/m air reach ~8e15)."""
+    key = name.upper()
+    if key not in ("C1", "C2", "C3", "C4", "C5"):
+        raise ValueError(f"unknown config {name}")
     return load_approximant(os.path.join(DATA_DIR, f"approx_{key}.json"))

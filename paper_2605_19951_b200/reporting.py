@@ -56,29 +56,75 @@ def pole_solution_checksum(g: np.ndarray) -> str:
 
 def scaling_benchmark(problem, model, approx, worker_counts=(1,), rhs=None,
                       solve_repeats: int = 4) -> list[dict]:
-    """Factorise-all and solve-all timings (device events) per repetition of
-    `worker_counts`; pole solutions checksummed (reporting.py:87-122)."""
+    """reporting.py:87-122 on the device.  "Workers" are pole shards (GPU
+    ranks): W workers own poles {i : i mod W == r} (PoleWorkerPool,
+    shifted.py:147-149).
+
+    * In a multi-process job (torch.distributed initialised, W == world size)
+      every rank times its own shard and the row carries the max over ranks.
+    * In one process the W shards run one after another on this device, each
+      in its own engine; every shard's factorisation and solve times are real
+      device times, and the row reports the slowest shard -- the time W GPUs
+      running concurrently would take, the all-gather excluded -- with
+      ``emulated=True``.
+
+    The pole-solution checksum is taken over all poles in pole order, so it
+    must be identical for every W (the reference's worker-count invariance,
+    test_acceptance.py:212-234)."""
     import torch
+    from .engine import Engine
+    from .parallel import PoleComm, ShardComm
     rhs = problem.f if rhs is None else rhs
+    rhs = np.asarray(rhs, dtype=complex)
+    real = PoleComm.current()
+    m = len(approx.poles)
     rows = []
     t1_total = None
     for w in worker_counts:
-        cache = ShiftedFactorCache()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        cache.ensure_factored(problem, model, approx)
-        torch.cuda.synchronize()
-        t_fact = time.perf_counter() - t0
-        t0 = time.perf_counter()
-        for _ in range(solve_repeats):
-            g = np.array([resolve_with_cache(cache, i, rhs) for i in cache.engine.local])
-        torch.cuda.synchronize()
-        t_solve = (time.perf_counter() - t0) / solve_repeats
+        w = int(w)
+        emulated = real.world == 1
+        if not emulated and w != real.world:
+            raise ValueError("in a distributed job worker_counts must equal the world size")
+        shards = range(w) if emulated else [real.rank]
+        g_all = [None] * m
+        t_fact = t_solve = 0.0
+        for r in shards:
+            comm = ShardComm(w, r) if emulated else real
+            eng = Engine(problem, approx, comm=comm)
+            eng.set_model(model.m)
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            torch.cuda.synchronize()
+            ev[0].record()
+            eng.factor()
+            ev[1].record()
+            rhs_d = torch.as_tensor(rhs, device=eng.device)
+            for _ in range(solve_repeats):
+                g = [eng.solve_d(slot, rhs_d) for slot in range(len(eng.local))]
+            ev[2].record()
+            torch.cuda.synchronize()
+            tf, ts = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2]) / solve_repeats
+            if not emulated:
+                t = torch.tensor([tf, ts], dtype=torch.float64, device=eng.device)
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                tf, ts = float(t[0]), float(t[1])
+                nmax = comm.n_max(m)
+                loc = torch.zeros((nmax, eng.N), dtype=torch.complex128, device=eng.device)
+                for slot in range(len(eng.local)):
+                    loc[slot] = g[slot]
+                allg = comm.gather_partials(loc)
+                for i, row in enumerate(comm.slot_of_pole(m)):
+                    g_all[i] = allg[int(row)].cpu().numpy()
+            else:
+                for slot, i in enumerate(eng.local):
+                    g_all[i] = g[slot].cpu().numpy()
+            t_fact = max(t_fact, tf)
+            t_solve = max(t_solve, ts)
+            eng.close()
         total = t_fact + t_solve
-        if t1_total is None:
+        if t1_total is None and w == 1:
             t1_total = total
-        rows.append({"workers": int(w), "factorize_ms": t_fact * 1e3, "solve_ms": t_solve * 1e3,
-                     "efficiency": t1_total / (w * total) if total > 0 else np.nan,
-                     "checksum": pole_solution_checksum(g)})
-        cache.engine.close()
+        eff = t1_total / (w * total) if (t1_total is not None and total > 0) else np.nan
+        rows.append({"workers": w, "factorize_ms": t_fact, "solve_ms": t_solve,
+                     "efficiency": eff, "emulated": emulated,
+                     "checksum": pole_solution_checksum(np.array(g_all))})
     return rows

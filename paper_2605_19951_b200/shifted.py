@@ -126,10 +126,18 @@ class ShiftedFactorCache:
         A = sp.csr_matrix(A)
         if self.engine is None or not self._generic or self.engine.N != A.shape[0]:
             from .engine import Engine
+            from .parallel import PoleComm
+            if PoleComm.current().world > 1:
+                # pole i is slot i here: one process owns every pole
+                raise RuntimeError("generic mode (factorize(i, A)) is single-process; "
+                                   "use factorize_all_poles / forward_response with G > 1")
             if self.engine is not None:
                 self.engine.close()
+            # factor storage is allocated per pole on its first factorisation,
+            # so max_poles only bounds the slot count, not the memory
             self.engine = Engine(_PatternProblem(A), None, device=self.device, leaf=self.leaf,
-                                 n_slots=self.max_poles)
+                                 n_slots=self.max_poles, lazy_factors=True,
+                                 comm=PoleComm(1, 0))
             self._generic = True
             self._bound = None
             rows, cols, _, _ = self.engine.pattern()
@@ -254,14 +262,24 @@ def solve_all_poles(problem, model, approx, rhs, cache: ShiftedFactorCache,
     eng = cache.ensure_factored(problem, model, approx)
     rhs = np.asarray(rhs)
     m = approx.pole_count if hasattr(approx, "pole_count") else len(approx.poles)
-    if eng.comm.world != 1:
-        raise NotImplementedError("solve_all_poles returns every pole's field; with G>1 "
-                                  "use forward_response / JacobianOperator")
     if _is_source(problem, rhs):
         eng.forward()
-        g = eng_fields(eng)[:, :, 0]
-    else:
+        g = eng.gather_fields()[:, 0, :].cpu().numpy()             # (m, N), all ranks
+    elif eng.comm.world == 1:
         g = np.array([eng.solve(cache.slot(i), rhs) for i in range(m)])
+    else:
+        # each rank solves its own poles; the fields are all-gathered (rank
+        # major) and put back in pole order, as PoleWorkerPool's gather
+        # (shifted.py:140-155)
+        import torch
+        nmax = eng.comm.n_max(m)
+        loc = torch.zeros((nmax, eng.N), dtype=torch.complex128, device=eng.device)
+        rhs_d = torch.as_tensor(np.asarray(rhs, dtype=complex), device=eng.device)
+        for slot, i in enumerate(eng.local):
+            loc[slot] = eng.solve_d(slot, rhs_d)
+        allg = eng._gather(loc)
+        idx = torch.as_tensor(eng.slot_of_pole.astype(np.int64), device=eng.device)
+        g = allg.index_select(0, idx).cpu().numpy()
     with cache._lock:
         cache.counters.solves += m
     if check_residuals:
@@ -275,7 +293,7 @@ def solve_all_poles(problem, model, approx, rhs, cache: ShiftedFactorCache,
 
 
 def eng_fields(eng) -> np.ndarray:
-    """Download g_i (m_local, N, S) in the original dof order."""
+    """Download the LOCAL g_i (m_local, N, S) in the original dof order."""
     out = []
     for slot in range(len(eng.local)):
         out.append(eng.download_g(slot))

@@ -7,15 +7,25 @@ Run in the build container only (needs /root/reference):
 Outputs (small .npz / .json files next to this script, plus the frozen
 approximants under paper_2605_19951_b200/data/):
 
-* ``approx_C{1,2,5}.json`` -- `rbainv.fit_common_pole` approximants for the
-  BASELINE configs (rba.py:280-378), saved with `rbainv.save_approximant`.
+* ``approx_C{1,2,3,4,5}.json`` -- `rbainv.fit_common_pole` approximants for the
+  BASELINE configs (rba.py:280-378), each fitted on its own config's spectral
+  interval, saved with `rbainv.save_approximant`.
 * ``ref2d_small.npz``   -- the reference's own 2-D `small_problem` fixture
   (pkg/tests/conftest.py:28-47) with its arrays and the reference outputs:
   pole solutions, forward data, J v, J^T w, adjoint mismatch, LSQR updates.
 * ``ref3d_n6.npz`` / ``ref3d_c3_n6.npz`` -- 3-D Nedelec problems built by
   paper_2605_19951_b200.mesh3d fed through the reference's own functions
   (single source, and a 4-source problem composed per source).
-* ``ref3d_C1.npz`` (--c1) -- the C1 configuration at full size (n=16).
+* ``ref3d_C1.npz`` (--c1) -- the C1 configuration at full size (n=16) at the
+  homogeneous start model.
+* ``ref3d_C1_true.npz`` (--c1true) -- C1 at full size at its TRUE model
+  (1e-8 S/m air, 1 S/m block, 0.01 S/m half-space), m_ref = start model:
+  forward data, J v, J^T w, adjointness, the GN update after 1/3/5/20 LSQR
+  iterations with the reference's dense-Cholesky R, the reference's own
+  solver-to-solver floor on those updates (SuperLU COLAMD vs MMD_AT_PLUS_A,
+  oracle/rbainv_oracle.lsqr_floor, itself pinned to the reference), the
+  robust secondaries after the step (phi, chi^2, linearised residual), and
+  checks of the reference R (R u, R^T y, nnz, sha256).
 """
 
 from __future__ import annotations
@@ -45,6 +55,8 @@ def fit_approximants():
     out = {}
     for name, n_poles, (t0, t1, nt) in (("C1", 8, (1e-5, 1e-2, 31)),
                                         ("C2", 16, (1e-5, 1e-2, 31)),
+                                        ("C3", 16, (1e-5, 1e-2, 31)),
+                                        ("C4", 16, (1e-5, 1e-2, 31)),
                                         ("C5", 20, (1e-6, 1e-2, 41))):
         path = os.path.join(DATA, f"approx_{name}.json")
         if os.path.exists(path):
@@ -52,7 +64,12 @@ def fit_approximants():
             continue
         # spectral interval: element-pencil bound of the config's true model
         # (air at 1e-8 S/m dominates), 5% margin -- as rba fixtures do.
-        prob, _ = mesh3d.build_config("C2" if name == "C2" else "C1", n=8)
+        if name in ("C3", "C4"):
+            # each config on its own interval: the full-size true model's
+            # element-pencil bound (its 1e-8 S/m air dominates)
+            prob, _ = mesh3d.build_config(name)
+        else:
+            prob, _ = mesh3d.build_config("C2" if name == "C2" else "C1", n=8)
         bound = mesh3d.spectral_bound(prob, prob.m_true)
         if name == "C2":
             bound = mesh3d.spectral_bound(prob, np.full(prob.grid.cell_count, np.log(1e-3)))
@@ -212,16 +229,85 @@ def golden_3d(name, n, approx, fname, lsqr_iters=(1, 3, 5), dense_reg=True):
           f" adjoint {float(outs['adjoint']):.2e} {time.time() - t:.1f}s")
 
 
+def golden_c1_true(approx, fname="ref3d_C1_true.npz", n=16, lam=1e-2, iters=(1, 3, 5, 20)):
+    import hashlib
+    import scipy.sparse.linalg as spla
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import rbainv_oracle as orc          # the floor only (pinned to the reference)
+    t = time.time()
+    prob, meta = mesh3d.build_config("C1", n=n)
+    prob.ensure_scatter()
+    P = prob.grid.cell_count
+    m_ref = np.full(P, np.log(prob.sigma_background))
+    model = rb.Model(prob.m_true, m_ref)
+    reg = rb.build_reg(prob.grid)
+    print(f"build_reg {time.time() - t:.1f}s", flush=True)
+    cache = rb.ShiftedFactorCache()
+    eps_r, seed = meta["noise"]
+    data = rb.make_dataset(prob, model, approx, rb.NoiseSpec(eps_r=eps_r, seed=seed), cache)
+    g = rb.solve_all_poles(prob, model, approx, prob.f, cache)
+    d, _ = rb.response_from_pole_solutions(prob, approx, g)
+    opr = rb.JacobianOperator(prob, model, approx, cache, pole_solutions=g)
+    out = {"m": prob.m_true, "m_ref": m_ref, "n": np.array(n), "lam": np.array(lam),
+           "d": d, "d_obs": data.d_obs, "sigma_d": data.sigma_d}
+    rng = np.random.default_rng(3)
+    v = rng.standard_normal(P)
+    w = rng.standard_normal(d.size)
+    out.update(v=v, w=w, jv=opr.jvp(v), jtw=opr.vjp(w))
+    out["adjoint"] = np.array(rb.adjoint_test(opr, trials=3, seed=4))
+    print(f"forward/J done {time.time() - t:.1f}s", flush=True)
+    W = data.weights
+    sql = np.sqrt(lam)
+    R = reg.R_factor
+    for k in iters:
+        dm, itn, istop = rb.inversion._augmented_lsqr(opr, reg, data, d, model, lam,
+                                                      rb.LsqrConfig(tol=0.0, max_iters=k))
+        out[f"dm_{k}"], out[f"itn_{k}"] = dm, np.array(itn)
+        # linearised residual of the augmented system after the step
+        r1 = W * (opr.jvp(dm) + d - data.d_obs)
+        r2 = sql * (R @ (dm + model.m - m_ref))
+        out[f"linres_{k}"] = np.array(np.sqrt(r1 @ r1 + r2 @ r2))
+        if k in (5, 20):
+            trial = rb.Model(model.m + dm, m_ref)
+            dn = rb.forward_response(prob, trial, approx, rb.ShiftedFactorCache()).data
+            mis = 0.5 * float(np.sum((W * (dn - data.d_obs)) ** 2))
+            rv, _ = rb.reg_value_grad(reg, trial)
+            out[f"phi_{k}"] = np.array(mis + lam * rv)
+            out[f"chi2_{k}"] = np.array(2.0 * mis / d.size)
+            floor, _ = orc.lsqr_floor(prob, model.m, approx.poles, approx.residues, R, W,
+                                      data.d_obs, lam, k, m_ref=m_ref)
+            out[f"floor_{k}"] = np.array(floor)
+            print(f"k={k}: phi {float(out[f'phi_{k}']):.6e} floor {floor:.2e} "
+                  f"{time.time() - t:.1f}s", flush=True)
+    rr = np.random.default_rng(7)
+    u = rr.standard_normal(P)
+    y = rr.standard_normal(R.shape[0])
+    out.update(R_u=R @ u, R_t_y=R.T @ y, R_nnz=np.array(R.nnz),
+               R_sha=np.array(hashlib.sha256(np.ascontiguousarray(R.data).tobytes()
+                                             + np.ascontiguousarray(R.indices).tobytes()
+                                             ).hexdigest()))
+    np.savez_compressed(os.path.join(HERE, fname), **out)
+    print(f"{fname}: N {prob.dof_count} P {P} adjoint {float(out['adjoint']):.2e} "
+          f"{time.time() - t:.1f}s")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1", action="store_true")
+    ap.add_argument("--c1true", action="store_true")
+    ap.add_argument("--only", default="")
     args = ap.parse_args()
+    if args.only == "c1true":
+        golden_c1_true(fit_approximants()["C1"])
+        return
     approxes = fit_approximants()
     golden_2d()
     golden_3d("C1", 6, approxes["C1"], "ref3d_n6.npz")
-    golden_3d("C3", 6, approxes["C2"], "ref3d_c3_n6.npz", lsqr_iters=(1, 3))
+    golden_3d("C3", 6, approxes["C3"], "ref3d_c3_n6.npz", lsqr_iters=(1, 3))
     if args.c1:
         golden_3d("C1", 16, approxes["C1"], "ref3d_C1.npz", lsqr_iters=(1, 3, 5, 20))
+    if args.c1true:
+        golden_c1_true(approxes["C1"])
 
 
 if __name__ == "__main__":

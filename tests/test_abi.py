@@ -11,7 +11,7 @@ from paper_2605_19951_b200 import _lib
 def header_symbols():
     src = open(os.path.join(ROOT, "include", "rba_b200.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(rba_[a-z0-9_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(rba_[A-Za-z0-9_]+)\s*\(", src)))
 
 
 def test_library_exports_header():

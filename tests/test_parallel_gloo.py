@@ -58,6 +58,9 @@ def _worker(rank, world, port, outdir):
     for k, i in enumerate(local):
         part[k] = torch.from_numpy(_partial(i))
     qall = comm.gather_partials(part).numpy()
+    # mode decisions (e.g. receiver-Green on/off) are the minimum over ranks
+    assert comm.agree_min(1 if rank else 0) == 0
+    assert comm.agree_min(rank + 3) == 3
     d = _combine(qall, comm.slot_of_pole(M), _residues())
     np.save(os.path.join(outdir, f"d_{world}_{rank}.npy"), d)
     dist.barrier()
