@@ -22,6 +22,7 @@ from .inversion import (InversionConfig, InversionState, IterationRecord, LineSe
                         LsqrConfig, chi_squared, default_lambda0, gn_step, line_search,
                         run_inversion)
 from .synthetic import DataSet, NoiseSpec, load_dataset, make_dataset, save_dataset
-from .reporting import TimingModel, fit_timing_model, pole_solution_checksum, scaling_benchmark
+from .reporting import (RunReport, TimingModel, consolidate_report, fit_timing_model, load_state,
+                        pole_solution_checksum, scaling_benchmark, write_run_artifacts)
 
 __version__ = "0.1.0"

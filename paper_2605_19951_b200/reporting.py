@@ -1,25 +1,34 @@
 """Timing/verification helpers of the hot path (rbainv.reporting subset).
 
 Mirrors ``pole_solution_checksum`` (reporting.py:83-84), ``fit_timing_model``
-(:63-80) and ``scaling_benchmark`` (:87-122) -- the C2 harness template.  On
+(:63-80), ``scaling_benchmark`` (:87-122) -- the C2 harness template -- and the
+run-directory format (``write_run_artifacts`` / ``consolidate_report``,
+:125-205: state.json, convergence.csv, timing.csv, residual_heatmap.csv,
+transients.csv), which is also the resume point (``load_state`` ->
+``InversionConfig.m0``, inversion.py:63,218).  On
 the GPU the pole work of one rank is batched into the same launches, so
 "workers" are the ranks of the job (G = world size) rather than host threads;
 the device path is deterministic, so the checksums are bit-identical for any
-worker count exactly as the reference requires.  Rundir/report writers are
-out of scope.
+worker count exactly as the reference requires.  Multi-source data
+([source][channel][receiver]) adds a leading source column to the
+per-receiver CSVs.
 """
 
 from __future__ import annotations
 
+import csv
 import hashlib
+import json
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, field
+from pathlib import Path
 
 import numpy as np
 
 from .shifted import ShiftedFactorCache, resolve_with_cache
 
-__all__ = ["TimingModel", "fit_timing_model", "pole_solution_checksum", "scaling_benchmark"]
+__all__ = ["TimingModel", "fit_timing_model", "pole_solution_checksum", "scaling_benchmark",
+           "RunReport", "write_run_artifacts", "consolidate_report", "load_state"]
 
 
 @dataclass
@@ -128,3 +137,96 @@ def scaling_benchmark(problem, model, approx, worker_counts=(1,), rhs=None,
                      "efficiency": eff, "emulated": emulated,
                      "checksum": pole_solution_checksum(np.array(g_all))})
     return rows
+
+
+# ---------------------------------------------------------------------------
+# run directory (reporting.py:125-205)
+# ---------------------------------------------------------------------------
+CONVERGENCE_FIELDS = ("nu", "phi", "misfit", "reg_value", "chi2", "lam", "eta", "accepted",
+                      "lsqr_iters", "lsqr_istop", "wall_ms", "factorizations", "solves",
+                      "phi_evals", "phi_before", "directional_slope")
+
+
+@dataclass
+class RunReport:
+    iterations: list
+    timing: TimingModel | None
+    counters: dict
+    scaling: list = field(default_factory=list)
+
+
+def _state_json(state) -> dict:
+    return {"model": np.asarray(state.model.m).tolist(),
+            "model_ref": np.asarray(state.model.m_ref).tolist(),
+            "lambda": float(state.lam), "phi": float(state.phi), "chi2": float(state.chi2),
+            "iterations_run": int(state.nu), "diagnostic": state.diagnostic,
+            "counters": dict(state.counters),
+            "history": [h.as_dict() for h in state.history]}
+
+
+def _jsonable(v):
+    if isinstance(v, (np.floating, np.integer, np.bool_)):
+        return v.item()
+    raise TypeError(f"not JSON serialisable: {type(v)}")
+
+
+def write_run_artifacts(rundir, state, data, problem, approx, d_pred) -> None:
+    """Persist one inversion run: state.json (model, lambda, objective,
+    history, counters), convergence.csv and timing.csv (the history), and the
+    per-receiver residual_heatmap.csv (weighted residual per time channel) and
+    transients.csv (long format: receiver, time, observed, predicted)."""
+    out = Path(rundir)
+    out.mkdir(parents=True, exist_ok=True)
+    (out / "state.json").write_text(json.dumps(_state_json(state), indent=1, default=_jsonable))
+    rows = [h.as_dict() for h in state.history]
+    with open(out / "convergence.csv", "w", newline="") as fh:
+        wr = csv.DictWriter(fh, fieldnames=list(CONVERGENCE_FIELDS), extrasaction="ignore")
+        wr.writeheader()
+        wr.writerows(rows)
+    with open(out / "timing.csv", "w", newline="") as fh:
+        wr = csv.writer(fh)
+        wr.writerow(["nu", "lsqr_iters", "wall_ms"])
+        for h in state.history:
+            wr.writerow([h.nu, h.lsqr_iters, h.wall_ms])
+    times = np.asarray(approx.channels.times)
+    Kt, Mr = times.size, int(problem.Q.shape[0])
+    d_pred = np.asarray(d_pred.cpu().numpy() if hasattr(d_pred, "cpu") else d_pred, dtype=float)
+    S = d_pred.size // (Kt * Mr)
+    wres = (np.asarray(data.weights) * (d_pred - np.asarray(data.d_obs))).reshape(S, Kt, Mr)
+    obs = np.asarray(data.d_obs).reshape(S, Kt, Mr)
+    pred = d_pred.reshape(S, Kt, Mr)
+    src = ["source"] if S > 1 else []
+    with open(out / "residual_heatmap.csv", "w", newline="") as fh:
+        wr = csv.writer(fh)
+        wr.writerow(src + ["time_s"] + [f"rx{r}" for r in range(Mr)])
+        for s_ in range(S):
+            for j in range(Kt):
+                wr.writerow(([s_] if S > 1 else []) + [times[j]] + wres[s_, j].tolist())
+    with open(out / "transients.csv", "w", newline="") as fh:
+        wr = csv.writer(fh)
+        wr.writerow(src + ["receiver", "time_s", "observed", "predicted"])
+        for s_ in range(S):
+            for r in range(Mr):
+                for j in range(Kt):
+                    wr.writerow(([s_] if S > 1 else []) +
+                                [r, times[j], obs[s_, j, r], pred[s_, j, r]])
+
+
+def consolidate_report(rundir) -> RunReport:
+    """reporting.py:190-205: the report of a run directory (history, timing
+    model when at least 3 iterations ran, counters, optional scaling.json)."""
+    out = Path(rundir)
+    doc = json.loads((out / "state.json").read_text())
+    hist = doc["history"]
+    timing = fit_timing_model(hist) if len(hist) >= 3 else None
+    scaling = json.loads((out / "scaling.json").read_text()) if (out / "scaling.json").exists() \
+        else []
+    return RunReport(iterations=hist, timing=timing, counters=doc.get("counters", {}),
+                     scaling=scaling)
+
+
+def load_state(rundir):
+    """(m, m_ref, lambda) of a run directory: resume by passing m as
+    InversionConfig.m0 and lambda as lambda0 (inversion.py:63,218)."""
+    doc = json.loads((Path(rundir) / "state.json").read_text())
+    return np.asarray(doc["model"]), np.asarray(doc["model_ref"]), float(doc["lambda"])

@@ -291,12 +291,40 @@ def golden_c1_true(approx, fname="ref3d_C1_true.npz", n=16, lam=1e-2, iters=(1, 
           f"{time.time() - t:.1f}s")
 
 
+def golden_rundir():
+    from rundir_case import rundir_case
+    """The reference's own write_run_artifacts (reporting.py:139-187) on a
+    synthetic state: the committed files pin the rundir format."""
+    import scipy.sparse as sp
+    c = rundir_case()
+    state = rb.InversionState(model=rb.Model(c["m"], c["m_ref"]), lam=c["lam"], nu=c["nu"],
+                              phi=c["phi"], chi2=c["chi2"],
+                              history=[rb.inversion.IterationRecord(**h) for h in c["history"]],
+                              diagnostic=c["diagnostic"], counters=c["counters"])
+    data = rb.DataSet(d_obs=c["d_obs"], sigma_d=c["sigma"], times=c["times"],
+                      receivers=np.zeros((c["M_r"], 2)), eps_r=0.0, eps_a=1.0, seed=0,
+                      provenance={})
+
+    class _P:
+        receiver_count = c["M_r"]
+        Q = sp.csr_matrix((c["M_r"], 1))
+
+    class _A:
+        channels = rb.TimeChannels(c["times"])
+    out = os.path.join(HERE, "rundir_ref")
+    rb.reporting.write_run_artifacts(out, state, data, _P(), _A(), c["d_pred"])
+    print("rundir_ref:", sorted(os.listdir(out)))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--c1", action="store_true")
     ap.add_argument("--c1true", action="store_true")
     ap.add_argument("--only", default="")
     args = ap.parse_args()
+    if args.only == "rundir":
+        golden_rundir()
+        return
     if args.only == "c1true":
         golden_c1_true(fit_approximants()["C1"])
         return
