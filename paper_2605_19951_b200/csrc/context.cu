@@ -42,15 +42,19 @@ int fail(int code, const std::string& msg) {
       return fail(RBA_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
   } while (0)
 
-enum StepKind { ST_EA = 0, ST_DIAG = 1, ST_TRSM = 2, ST_GEMM = 3 };
+enum StepKind { ST_EA = 0, ST_DIAG = 1, ST_TRSM = 2, ST_GEMM = 3, ST_OZ = 4 };
 struct Step {
   int kind;
   int64_t off;
   int n;
   int ntiles;
-  int schur;   // ST_GEMM: 1 = Schur-complement update (K = npiv), 0 = panel update
+  int schur;   // ST_GEMM: 1 = Schur-complement update (K = npiv), 0 = panel update;
+               // ST_OZ: row tiles of the step (digit-split CTAs)
   int level;
+  int64_t oz_split = 0;   // ST_OZ: digit-block bytes per pole
+  int64_t oz_rows = 0;    // ST_OZ: border rows (row exponents) per pole
 };
+constexpr int64_t OZ_BLK_BYTES = 7 * 2 * 192 * 16;  // kernels_ozaki.cu OZ_BLK (A_big + B)
 
 int nr_pad(int s) { return s <= 1 ? 1 : s <= 2 ? 2 : s <= 4 ? 4 : 8; }
 }  // namespace
@@ -84,6 +88,14 @@ struct rba_ctx {
   int2* ea_tasks = nullptr;
   rba::PanelTask* pt_tasks = nullptr;
   rba::GemmTask* gm_tasks = nullptr;
+  // Ozaki-scheme INT8 tensor-core Schur updates (RBA_OZAKI, kernels_ozaki.cu)
+  bool ozaki = true;           // RBA_OZAKI=0: DMMA for every Schur update
+  int oz_min_k = 256;          // fronts with at least this many pivots
+  rba::OzTask* oz_tasks = nullptr;
+  int64_t oz_split_max = 0, oz_rows_max = 0;
+  int oz_sub = 1;              // poles per Ozaki launch (digit-buffer budget)
+  unsigned char* oz_buf = nullptr;
+  int* oz_exp = nullptr;
   std::vector<std::pair<int64_t, int>> fwd_lv, bwd_lv, fwdb_lv, bwdb_lv, small_lv;
   std::vector<int> small_mb;   // per level: pivot blocks of the largest warp-per-front front
   // host copies for the pruned forward sweeps of the receiver-Green build
@@ -276,6 +288,8 @@ void free_slots(rba_ctx* c) {
   c->wa = nullptr;
   c->pole_of_slot = nullptr;
   c->slot_map = nullptr;
+  c->oz_buf = nullptr;
+  c->oz_exp = nullptr;
   c->poles_d = nullptr;
   c->res_d = nullptr;
   c->mem_factor = 0;
@@ -301,7 +315,9 @@ int build_plans(rba_ctx* c) {
   std::vector<int2> ea;
   std::vector<rba::PanelTask> pt;
   std::vector<rba::GemmTask> gm;
+  std::vector<rba::OzTask> oz;
   c->plan.clear();
+  c->oz_split_max = c->oz_rows_max = 0;
   for (int L = 0; L < S.nlevels; ++L) {
     const size_t plan0 = c->plan.size();
     const int q0 = S.level_ptr[L], q1 = S.level_ptr[L + 1];
@@ -374,24 +390,50 @@ int build_plans(rba_ctx* c) {
       }
       if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles});
     }
-    // Schur complement of each front with a border
+    // Schur complement of each front with a border: large fronts on the INT8
+    // tensor cores (Ozaki scheme), the rest with the DMMA GEMM
     int64_t goff = gm.size();
     int tiles = 0;
+    const int64_t ooff = oz.size();
+    int oz_tiles = 0, oz_rt = 0;
+    int64_t oz_bytes = 0, oz_rows = 0;
     for (int q = q0; q < q1; ++q) {
       int s = S.level_fronts[q];
       int p = S.npiv[s], nf = S.nf[s];
       if (nf <= p || p == 0) continue;
       int ntr = (nf - p + rba::GT - 1) / rba::GT;
+      if (c->ozaki && p >= c->oz_min_k && p <= 16384) {
+        const int nks = (p + 15) / 16;
+        rba::OzTask t{};
+        t.s = s; t.p = p; t.nf = nf; t.nrt = ntr; t.nks = nks;
+        t.tile_start = oz_tiles; t.rt_start = oz_rt;
+        t.split_off = oz_bytes; t.exp_off = oz_rows;
+        oz.push_back(t);
+        oz_tiles += ntr * (ntr + 1) / 2;
+        oz_rt += ntr;
+        oz_bytes += (int64_t)ntr * nks * OZ_BLK_BYTES;
+        oz_rows += nf - p;
+        continue;
+      }
       gm.push_back({s, 0, p, p, nf, tiles, ntr, 0});
       tiles += ntr * (ntr + 1) / 2;
     }
     if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles, 1});
+    if ((int64_t)oz.size() > ooff) {
+      Step st{ST_OZ, ooff, (int)(oz.size() - ooff), oz_tiles, oz_rt, 0};
+      st.oz_split = oz_bytes;
+      st.oz_rows = oz_rows;
+      c->plan.push_back(st);
+      c->oz_split_max = std::max(c->oz_split_max, oz_bytes);
+      c->oz_rows_max = std::max(c->oz_rows_max, oz_rows);
+    }
     for (size_t q = plan0; q < c->plan.size(); ++q) c->plan[q].level = L;
   }
   int rc;
   if ((rc = upload(c, c->allocs, &c->ea_tasks, ea.data(), ea.size()))) return rc;
   if ((rc = upload(c, c->allocs, &c->pt_tasks, pt.data(), pt.size()))) return rc;
   if ((rc = upload(c, c->allocs, &c->gm_tasks, gm.data(), gm.size()))) return rc;
+  if (!oz.empty() && (rc = upload(c, c->allocs, &c->oz_tasks, oz.data(), oz.size()))) return rc;
 
   // solve plans
   std::vector<rba::SolveTask> ft, bt, ftb, btb;
@@ -541,6 +583,24 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
           rba::launch_trsm(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
         else
           rba::launch_trsm3(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->gemm_var);
+        break;
+      }
+      case ST_OZ: {
+        Timed t(c, KC_GEMM);
+        Timed tg(c, 112 + std::min(s.level, 15), 0);
+        for (int g0 = 0; g0 < pb.count; g0 += c->oz_sub) {
+          rba::PoleBatch sub{};
+          sub.count = std::min(c->oz_sub, pb.count - g0);
+          for (int i = 0; i < sub.count; ++i) {
+            sub.factor[i] = pb.factor[g0 + i];
+            sub.upd[i] = pb.upd[g0 + i];
+            sub.tmap[i] = pb.tmap[g0 + i];
+            sub.xi[i] = pb.xi[g0 + i];
+          }
+          c->launches += 1;
+          rba::launch_oz_schur(c->st, c->oz_tasks + s.off, s.n, s.schur, s.ntiles, c->F, sub,
+                               c->oz_buf, s.oz_split, c->oz_exp, s.oz_rows);
+        }
         break;
       }
       case ST_GEMM: {
@@ -733,6 +793,19 @@ int ensure_slots(rba_ctx* c) {
     }
   }
   if ((rc = dalloc(c, c->pole_allocs, &c->wa, (size_t)nl * std::max(c->S, 1) * std::max<int64_t>(c->Mr, 1), &c->mem_work))) return rc;
+  if (c->ozaki && c->oz_split_max > 0) {
+    // digit blocks of one Ozaki Schur step for oz_sub poles at a time, sized
+    // to the memory left after the factors, arenas and work vectors
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t margin = (size_t)3 << 29;        // 1.5 GB
+    const size_t per = (size_t)c->oz_split_max;
+    int sub = fr > margin + per ? (int)((fr - margin) / per) : 1;
+    c->oz_sub = std::max(1, std::min(sub, c->fbatch));
+    if (const char* e = getenv("RBA_OZ_SUB")) c->oz_sub = std::max(1, std::min(atoi(e), c->fbatch));
+    if ((rc = dalloc(c, c->pole_allocs, &c->oz_buf, per * c->oz_sub, &c->mem_work))) return rc;
+    if ((rc = dalloc(c, c->pole_allocs, &c->oz_exp, (size_t)c->oz_rows_max * c->oz_sub, &c->mem_work))) return rc;
+  }
   std::vector<int32_t> pos(c->local.begin(), c->local.end());
   if ((rc = dalloc(c, c->pole_allocs, &c->pole_of_slot, nl, &c->mem_other))) return rc;
   CK(cudaMemcpyAsync(c->pole_of_slot, pos.data(), nl * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
@@ -981,6 +1054,8 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) == "fused";
   if (const char* e = getenv("RBA_SMALLP")) c->small_p = std::string(e) == "64" ? rba::PB : 2 * rba::PB;
   if (const char* e = getenv("RBA_DIAG")) c->diag_v1 = std::string(e) == "v1";
+  if (const char* e = getenv("RBA_OZAKI")) c->ozaki = std::string(e) != "0";
+  if (const char* e = getenv("RBA_OZ_MINK")) c->oz_min_k = std::max(16, atoi(e));
   int rc;
   if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||
       (rc = dalloc(c, c->allocs, &c->red_part, 1024, &c->mem_other)) ||

@@ -64,5 +64,12 @@ __device__ __forceinline__ cplx* faddr(cplx* panel, cplx* upd, int p, int nf, in
 struct PanelTask { int32_t s, k0, r0, pad; };
 struct GemmTask { int32_t s, t0, t1, c_lo, c_hi, tile_start, ntr, pad; };
 struct SolveTask { int32_t s, blk; };
+// Ozaki-scheme Schur update of one front (kernels_ozaki.cu): nrt row tiles of
+// 64 border rows, nks k steps of 16 pivots; its digit blocks start at
+// split_off (bytes, per pole), its row exponents at exp_off (rows, per pole)
+struct OzTask {
+  int32_t s, p, nf, nrt, nks, tile_start, rt_start, pad;
+  int64_t split_off, exp_off;
+};
 
 }  // namespace rba

@@ -1,0 +1,329 @@
+// Schur-complement update of the large fronts on the INT8 tensor cores
+// (tcgen05.mma kind::i8, TMEM accumulators): an Ozaki-scheme FP64 GEMM.
+//
+// The Schur update of a front with p pivots and b = nf - p border rows is
+//     C (b x b, complex symmetric, packed lower)  -=  L' L'^T,   L' = L'[p:nf, 0:p]
+// (L' = L D^{1/2}, fronts.cuh).  Each complex row r of L' is scaled by its own
+// power of two 2^-e_r (max_k max(|Re|, |Im|) < 2^e_r) and written as 7 balanced
+// base-256 digits d_1..d_7 in [-128, 127] of Y = rint(L'_rk 2^(54 - e_r)):
+//     L'_rk = 2^(e_r - 54) sum_t d_t 256^(7 - t)   (exact up to the rint, 2^-55
+// relative to the row maximum).  Then
+//     (L' L'^T)_ij = 2^(e_i + e_j - 108) sum_{t,u} 256^(14 - t - u) sum_k d_t(ik) d_u(jk)
+// and the 28 most significant digit pairs (t + u <= 8) are kept; every inner
+// sum is an exact int8 x int8 -> int32 tensor-core product (K <= 18,000 cannot
+// overflow).  Complex arithmetic rides a real embedding (4 real products): the
+// 128 accumulator lanes of a tile hold the real parts of 64 complex rows
+// (A row = (Re, -Im) interleaved along k) and their imaginary parts
+// (A row = (Im, Re)); the B rows are (Re, Im).  k_oz_split writes all three
+// digit layouts once per factorisation step, so the GEMM only streams them.
+//
+// The GEMM CTA (one 64 x 64 complex tile of one front of one pole) keeps the 7
+// digit levels d = t + u = 2..8 in 7 TMEM accumulators of 64 columns (448 of
+// 512), streams 16 complex k per stage (A_big 28 KB + B 14 KB digit blocks, bulk
+// copies by a producer thread into a 4-stage ring), issues 28 MMAs (M=128,
+// N=64, K=32) per stage from one thread, and combines the levels in FP64 in
+// the epilogue:  C_ij -= 2^(e_i + e_j - 108) sum_{d=8..2} 256^(14 - d) acc_d(ij)
+// (all scalings exact powers of two).
+// Deterministic: fixed k order, fixed level order, one CTA per C tile.
+// Accuracy: normwise like an FP64 GEMM (2^-54 of row max x column max per
+// term); the device factor is checked against the reference's SuperLU
+// backward error and the parity goldens (tests/test_gpu_verify.py).
+#include "fronts.cuh"
+#include "kernels.h"
+
+namespace rba {
+
+namespace {
+constexpr int OZ_S = 7;                    // digits per value
+constexpr int OZ_KS = 16;                  // complex k per stage (= one MMA-K32)
+constexpr int OZ_ABYTES = OZ_S * 2 * 128 * 16;  // A_big digits of one (row tile, k step)
+constexpr int OZ_BBYTES = OZ_S * 2 * 64 * 16;   // B digits
+constexpr int OZ_BLK = OZ_ABYTES + OZ_BBYTES;   // one (row tile, k step) block
+constexpr int OZ_NLD = 4;                  // stages of the load ring
+constexpr int OZ_LEV = 7;                  // accumulator levels d = 2..8
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;                  // sm_100 descriptor version; no swizzle
+  return d;
+}
+// s32 accumulator, s8 x s8, both K-major, M = 128, N = 64
+constexpr uint32_t OZ_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) |
+                              ((uint32_t)(128 >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t dtmem, uint64_t da, uint64_t db, int acc) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+               " tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+               :: "r"(dtmem), "l"(da), "l"(db), "r"(OZ_IDESC), "r"(acc));
+}
+__device__ __forceinline__ void mbar_init_(uint64_t* bar, int n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" :: "r"(su32(bar)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0, tries = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done) : "r"(su32(bar)), "r"(parity) : "memory");
+    if (++tries > (1u << 28)) __trap();
+  } while (!done);
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// digit split: one CTA per (front task, row tile of 64 border rows, pole).
+// Balanced base-256 digits without carries: U = Y + 0x80808080808080 is
+// non-negative for |Y| < 2^54 and byte j of U, XOR 0x80, is the signed digit
+// of weight 256^j.  -Im gets its own digits (a negated -128 would overflow).
+// Per (row tile, k step) block: A_big [slice][chunk][128 rows][16 B] with rows
+// 0..63 = (Re, -Im) and 64..127 = (Im, Re), then B [slice][chunk][64][16 B]
+// = (Re, Im); k interleaved with the real/imaginary part inside each 16 B.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long oz_u(double v, int e) {
+  return (unsigned long long)(__double2ll_rn(ldexp(v, 54 - e)) + 0x80808080808080LL);
+}
+// digit byte (signed, as raw bits) of slice t (t = 0: most significant, 256^6)
+__device__ __forceinline__ uint32_t oz_dig(unsigned long long u, int t) {
+  return (uint32_t)((u >> (8 * (OZ_S - 1 - t))) & 0xFFu) ^ 0x80u;
+}
+
+__global__ void __launch_bounds__(128) k_oz_split(const OzTask* __restrict__ tasks, int ntasks,
+                                                  FrontsDev F, PoleBatch pb,
+                                                  unsigned char* __restrict__ split,
+                                                  int64_t split_pole, int* __restrict__ expo,
+                                                  int64_t exp_pole) {
+  __shared__ int s_e[64];
+  __shared__ double s_m[2][64];
+  const int slot = blockIdx.y;
+  int ti = 0;
+  {
+    int lo = 0, hi = ntasks - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tasks[mid].rt_start <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+    }
+    ti = lo;
+  }
+  const OzTask tk = tasks[ti];
+  const int rt = blockIdx.x - tk.rt_start;
+  const int s = tk.s, p = tk.p, nf = tk.nf;
+  const int b = nf - p;
+  const cplx* __restrict__ panel = pb.factor[slot] + F.panel_off[s];
+  const int tid = threadIdx.x, r = tid & 63, h = tid >> 6;
+  const int row = rt * 64 + r;                 // border row (0-based)
+  const bool on = row < b;
+  // pass 1: row maximum over the p pivot columns
+  double m = 0.0;
+  if (on)
+    for (int k = h; k < p; k += 2) {
+      const cplx v = __ldg(panel + (int64_t)k * nf + p + row);
+      m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
+    }
+  s_m[h][r] = m;
+  __syncthreads();
+  if (h == 0) {
+    const double mm = fmax(s_m[0][r], s_m[1][r]);
+    s_e[r] = mm > 0.0 ? ilogb(mm) + 1 : 0;     // mm < 2^e
+    if (on) expo[(int64_t)slot * exp_pole + tk.exp_off + row] = s_e[r];
+  }
+  __syncthreads();
+  const int e = s_e[r];
+  // pass 2: digits, thread = (row r, chunk h of 8 complex k) per k step
+  unsigned char* out = split + (int64_t)slot * split_pole + tk.split_off + (int64_t)rt * tk.nks * OZ_BLK;
+  for (int ks = 0; ks < tk.nks; ++ks) {
+    unsigned long long ure[8], uim[8], unim[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int k = ks * OZ_KS + h * 8 + j;
+      cplx v = cmk(0.0, 0.0);
+      if (on && k < p) v = __ldg(panel + (int64_t)k * nf + p + row);
+      ure[j] = oz_u(v.x, e);
+      uim[j] = oz_u(v.y, e);
+      unim[j] = oz_u(-v.y, e);
+    }
+    unsigned char* blk = out + (int64_t)ks * OZ_BLK;
+#pragma unroll
+    for (int t = 0; t < OZ_S; ++t) {
+      uint4 wre, wim, wb;
+      uint32_t* pre = &wre.x;
+      uint32_t* pim = &wim.x;
+      uint32_t* pb_ = &wb.x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t r0 = oz_dig(ure[2 * q], t), r1 = oz_dig(ure[2 * q + 1], t);
+        const uint32_t i0 = oz_dig(uim[2 * q], t), i1 = oz_dig(uim[2 * q + 1], t);
+        const uint32_t n0 = oz_dig(unim[2 * q], t), n1 = oz_dig(unim[2 * q + 1], t);
+        pre[q] = r0 | (n0 << 8) | (r1 << 16) | (n1 << 24);   // (Re, -Im)
+        pim[q] = i0 | (r0 << 8) | (i1 << 16) | (r1 << 24);   // (Im, Re)
+        pb_[q] = r0 | (i0 << 8) | (r1 << 16) | (i1 << 24);   // (Re, Im)
+      }
+      *reinterpret_cast<uint4*>(blk + ((t * 2 + h) * 128 + r) * 16) = wre;
+      *reinterpret_cast<uint4*>(blk + ((t * 2 + h) * 128 + 64 + r) * 16) = wim;
+      *reinterpret_cast<uint4*>(blk + OZ_ABYTES + ((t * 2 + h) * 64 + r) * 16) = wb;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// INT8 tensor-core Schur GEMM, warp-specialised: warp 0 loads (bulk copies
+// into a ring of OZ_NLD stages), warp 1 issues the MMAs (one thread), all
+// four warps run the epilogue (TMEM lanes 32w..32w+31).
+// ---------------------------------------------------------------------------
+struct OzSmem {
+  unsigned char st[OZ_NLD][OZ_BLK];          // [stage][A_big | B] digit blocks
+  uint64_t full[OZ_NLD], empty[OZ_NLD], done;
+  uint32_t tbase;
+};
+
+__global__ void __launch_bounds__(128, 1) k_oz_gemm(const OzTask* __restrict__ tasks, int ntasks,
+                                                    FrontsDev F, PoleBatch pb,
+                                                    const unsigned char* __restrict__ split,
+                                                    int64_t split_pole, const int* __restrict__ expo,
+                                                    int64_t exp_pole) {
+  extern __shared__ __align__(1024) unsigned char oz_raw[];
+  OzSmem& S = *reinterpret_cast<OzSmem*>(oz_raw);
+  const int slot = blockIdx.y, tile = blockIdx.x;
+  int ti = 0;
+  {
+    int lo = 0, hi = ntasks - 1;
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (tasks[mid].tile_start <= tile) lo = mid; else hi = mid - 1;
+    }
+    ti = lo;
+  }
+  const OzTask tk = tasks[ti];
+  int local = tile - tk.tile_start, tj = 0;
+  while (local >= tk.nrt - tj) { local -= tk.nrt - tj; ++tj; }
+  const int tr = tj + local;                   // row tile >= column tile
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const unsigned char* sp = split + (int64_t)slot * split_pole + tk.split_off;
+  const unsigned char* srcA = sp + (int64_t)tr * tk.nks * OZ_BLK;
+  const unsigned char* srcB = sp + (int64_t)tj * tk.nks * OZ_BLK + OZ_ABYTES;
+  const int nks = tk.nks;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" :: "r"(su32(&S.tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 32) {
+    for (int q = 0; q < OZ_NLD; ++q) {
+      mbar_init_(&S.full[q], 1);
+      mbar_init_(&S.empty[q], 1);
+    }
+    mbar_init_(&S.done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tb = S.tbase;
+
+  if (tid == 0) {
+    // producer: stage q is refilled once the MMAs that read it committed
+    for (int ks = 0; ks < nks; ++ks) {
+      const int q = ks % OZ_NLD;
+      if (ks >= OZ_NLD) mbar_wait_(&S.empty[q], ((ks / OZ_NLD) - 1) & 1);
+      const uint32_t bar = su32(&S.full[q]);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" :: "r"(bar), "r"(OZ_ABYTES + OZ_BBYTES) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                   :: "r"(su32(S.st[q])), "l"(srcA + (int64_t)ks * OZ_BLK), "r"(OZ_ABYTES), "r"(bar) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                   :: "r"(su32(S.st[q] + OZ_ABYTES)), "l"(srcB + (int64_t)ks * OZ_BLK), "r"(OZ_BBYTES), "r"(bar) : "memory");
+    }
+  } else if (tid == 32) {
+    // MMA issuer: 28 digit-pair products per k step into the 7 level accumulators
+    for (int ks = 0; ks < nks; ++ks) {
+      const int q = ks % OZ_NLD;
+      mbar_wait_(&S.full[q], (ks / OZ_NLD) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      const uint32_t abase = su32(S.st[q]), bbase = abase + OZ_ABYTES;
+#pragma unroll
+      for (int d = 2; d <= 8; ++d)
+#pragma unroll
+        for (int t = 1; t < d; ++t) {
+          const int u = d - t;
+          if (t > OZ_S || u > OZ_S) continue;
+          const uint64_t da = umma_desc(abase + (t - 1) * 2 * 128 * 16, 128 * 16, 128);
+          const uint64_t db = umma_desc(bbase + (u - 1) * 2 * 64 * 16, 64 * 16, 128);
+          mma_i8(tb + (d - 2) * 64, da, db, (ks > 0 || t > 1) ? 1 : 0);
+        }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                   :: "r"(su32(&S.empty[q])) : "memory");
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                 :: "r"(su32(&S.done)) : "memory");
+  }
+  __syncwarp();
+  mbar_wait_(&S.done, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+
+  // epilogue: lane = accumulator row (warp w owns TMEM lanes 32w..32w+31)
+  const int arow = warp * 32 + lane;
+  const bool imag = arow >= 64;
+  const int lr = arow & 63;
+  const int s = tk.s, p = tk.p, nf = tk.nf, b = nf - p;
+  const int grow = tr * 64 + lr;               // border row of this accumulator row
+  const int* ex = expo + (int64_t)slot * exp_pole + tk.exp_off;
+  const int ei = grow < b ? __ldg(ex + grow) : 0;
+  cplx* upd = pb.upd[slot] + (F.upd_off[s] >= 0 ? F.upd_off[s] : 0);
+  for (int c0 = 0; c0 < 64; c0 += 16) {
+    double acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+#pragma unroll
+    for (int d = 8; d >= 2; --d) {             // smallest terms first
+      uint32_t v[16];
+      const uint32_t taddr = tb + (uint32_t)((d - 2) * 64 + c0) + ((uint32_t)(warp * 32) << 16);
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                     "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+                     "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                   : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      const double w = ldexp(1.0, 8 * (14 - d));
+#pragma unroll
+      for (int i = 0; i < 16; ++i) acc[i] = fma((double)(int32_t)v[i], w, acc[i]);
+    }
+    if (grow < b) {
+      double* dst[16];
+      double cur[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int gcol = tj * 64 + c0 + i;     // border column
+        dst[i] = (gcol < b && gcol <= grow)
+                     ? reinterpret_cast<double*>(upd + ucol(gcol, b) + (grow - gcol)) + (imag ? 1 : 0)
+                     : nullptr;
+        cur[i] = dst[i] ? __ldcg(dst[i]) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        if (dst[i]) *dst[i] = cur[i] - ldexp(acc[i], ei + __ldg(ex + tj * 64 + c0 + i) - 108);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" :: "r"(tb));
+}
+
+void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, int nrowtiles, int ntiles, const FrontsDev& F, const PoleBatch& pb,
+                     unsigned char* split, int64_t split_pole, int* expo, int64_t exp_pole) {
+  if (ntasks <= 0 || ntiles <= 0) return;
+  k_oz_split<<<dim3(nrowtiles, pb.count), 128, 0, st>>>(tasks, ntasks, F, pb, split,
+                                                        split_pole, expo, exp_pole);
+  const size_t smem = sizeof(OzSmem) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_oz_gemm<<<dim3(ntiles, pb.count), 128, smem, st>>>(tasks, ntasks, F, pb, split, split_pole,
+                                                       expo, exp_pole);
+}
+
+}  // namespace rba

@@ -275,3 +275,80 @@ def test_eight_rhs_solves_vs_splu(gpu):
         err = max(rel(X[:, k], Xs[:, k]) for k in range(8))
         print(f"pole {i}: 8-RHS solve vs splu {err:.2e}")
         assert err <= 1e-9
+
+
+def _c1_true():
+    z = golden("ref3d_C1_true.npz")
+    prob, _ = rb.build_config("C1", n=int(z["n"]))
+    approx = rb.config_approximant("C1")
+    model = rb.Model(z["m"], z["m_ref"])
+    return z, prob, approx, model
+
+
+def test_c1_true_model_forward_and_jacobian(gpu):
+    """C1 at full size at its TRUE model: 1e-8 S/m air, 1 S/m block
+    (make_golden.py golden_c1_true, unmodified reference)."""
+    z, prob, approx, model = _c1_true()
+    assert np.unique(np.exp(z["m"])).size >= 3           # air, half-space, block
+    cache = rb.ShiftedFactorCache()
+    d = rb.forward_response(prob, model, approx, cache).data
+    opr = rb.JacobianOperator(prob, model, approx, cache)
+    ef, ej, et = rel(d, z["d"]), rel(opr.jvp(z["v"]), z["jv"]), rel(opr.vjp(z["w"]), z["jtw"])
+    adj = rb.adjoint_test(opr, trials=3, seed=4)
+    print(f"C1 true model: forward {ef:.2e}  J v {ej:.2e}  J^T w {et:.2e}  adjoint {adj:.2e} "
+          f"(reference {float(z['adjoint']):.2e})")
+    assert ef <= 1e-9 and ej <= 1e-8 and et <= 1e-8
+    assert adj <= 1e-8
+    # the reference's d_clean of the old start-model golden is this same forward
+    z0 = golden("ref3d_C1.npz")
+    assert rel(d, z0["d_clean"]) <= 1e-9
+
+
+def test_c1_true_model_gn_update(gpu):
+    """GN update dm after 1/3/5/20 LSQR iterations at the true model with the
+    reference's LAPACK R: <= max(1e-8, 10 x the reference's own solver-to-
+    solver floor) (floors measured by make_golden.py), and the
+    iteration-count-robust secondaries after the 20-iteration step."""
+    import hashlib
+    from paper_2605_19951_b200.inversion import _augmented_lsqr
+    z, prob, approx, model = _c1_true()
+    reg = rb.build_reg(prob.grid, root="chol")
+    R = reg.R_factor
+    rr = np.random.default_rng(7)
+    u = rr.standard_normal(R.shape[1])
+    y = rr.standard_normal(R.shape[0])
+    same = hashlib.sha256(np.ascontiguousarray(R.data).tobytes() +
+                          np.ascontiguousarray(R.indices).tobytes()).hexdigest() == str(z["R_sha"])
+    print(f"reference R: bitwise {'identical' if same else 'different'}, R u {rel(R @ u, z['R_u']):.1e},"
+          f" R^T y {rel(R.T @ y, z['R_t_y']):.1e}")
+    assert R.nnz == int(z["R_nnz"])
+    assert rel(R @ u, z["R_u"]) <= 1e-13 and rel(R.T @ y, z["R_t_y"]) <= 1e-13
+    cache = rb.ShiftedFactorCache()
+    opr = rb.JacobianOperator(prob, model, approx, cache)
+    data = _data(z)
+    lam = float(z["lam"])
+    W = data.weights
+    for k in (1, 3, 5, 20):
+        dm, itn, _ = _augmented_lsqr(opr, reg, data, z["d"], model, lam,
+                                     rb.LsqrConfig(tol=0.0, max_iters=k))
+        assert itn == k
+        err = rel(dm, z[f"dm_{k}"])
+        floor = float(z[f"floor_{k}"]) if f"floor_{k}" in z else 0.0
+        r1 = W * (opr.jvp(dm) + z["d"] - z["d_obs"])
+        r2 = np.sqrt(lam) * (R @ (dm + model.m - model.m_ref))
+        lin = float(np.sqrt(r1 @ r1 + r2 @ r2))
+        elin = abs(lin - float(z[f"linres_{k}"])) / float(z[f"linres_{k}"])
+        msg = f"k={k}: dm vs reference {err:.2e} (floor {floor:.2e}), linearised residual {elin:.1e}"
+        if k in (5, 20):
+            trial = rb.Model(model.m + dm, model.m_ref)
+            dn = rb.forward_response(prob, trial, approx, rb.ShiftedFactorCache()).data
+            mis = 0.5 * float(np.sum((W * (dn - z["d_obs"])) ** 2))
+            rv, _ = rb.reg_value_grad(reg, trial)
+            ephi = abs(mis + lam * rv - float(z[f"phi_{k}"])) / float(z[f"phi_{k}"])
+            echi = abs(2 * mis / dn.size - float(z[f"chi2_{k}"])) / float(z[f"chi2_{k}"])
+            msg += f", phi after step {ephi:.1e}, chi2 {echi:.1e}"
+        print(msg)
+        assert err <= max(1e-8, 10 * floor), msg
+        assert elin <= 1e-8, msg
+        if k == 20:
+            assert ephi <= 10 * floor and echi <= 10 * floor, msg

@@ -1,0 +1,37 @@
+"""C4 factorisation time and per-pole backward error, DMMA vs Ozaki (INT8)
+Schur updates: python tools/oz_check.py  (env RBA_OZAKI selects the path)."""
+import os, sys, time
+import numpy as np, torch
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2605_19951_b200 as rb
+from paper_2605_19951_b200.engine import Engine
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench
+
+prob, _ = rb.build_config("C4")
+approx = rb.config_approximant("C4")
+eng = Engine(prob, approx)
+eng.set_model(prob.m_true)
+eng.factor()
+torch.cuda.synchronize()
+ts = []
+for _ in range(3):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); eng.factor(); e1.record(); torch.cuda.synchronize()
+    ts.append(e0.elapsed_time(e1))
+eng.set_timing(2); eng.set_timing(1); eng.factor(); cls = eng.timings(); lev = eng.timings_detail(); eng.set_timing(0)
+print("factor_by_level", [round(x, 1) for x in lev["factor_by_level"][:15]])
+print("gemm_by_level", [round(x, 1) for x in lev["gemm_by_level"][:15]])
+print("classes", {k: round(v, 1) for k, v in cls.items()})
+M = bench.host_mass(prob, prob.m_true).astype(complex)
+K = prob.K.astype(complex).tocsr()
+rng = np.random.default_rng(0)
+b = rng.standard_normal(eng.N) + 1j * rng.standard_normal(eng.N)
+out = []
+for i in (0, 8, 15):
+    A = (K - approx.poles[i] * M).tocsr()
+    x = eng.solve(i, b)
+    nA = abs(A).sum(axis=1).max()
+    out.append(float(np.linalg.norm(A @ x - b) / (nA * np.linalg.norm(x) + np.linalg.norm(b))))
+print(f"RBA_OZAKI={os.environ.get('RBA_OZAKI','0')}: factor 16 poles {min(ts):.1f} ms "
+      f"gemm {cls['gemm']:.1f} ms; backward {out}; mem {eng.info()['mem_work']/1e9:.1f} GB work", flush=True)
