@@ -279,7 +279,7 @@ def run_ours(args, world, rank):
     traffic = measured_traffic()
     # kernel-class times from the instrumented last warm-up step (one GN
     # iteration: split_fact factorisations, split_solves solves)
-    fact_ms = sum(cls[k] for k in ("scatter", "extend_add", "diag", "trsm", "gemm"))
+    fact_ms = sum(cls[k] for k in ("scatter", "extend_add", "diag", "trsm", "gemm", "ozaki"))
     solve_ms = cls["solve_fwd"] + cls["solve_bwd"]
     n_local_fact = split_fact
     fact_flops = sym_flops * n_local_fact
@@ -311,6 +311,38 @@ def run_ours(args, world, rank):
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                 "per_unit": "2*nnz(L)*16 + N*16 + 4*N*nrhs*16 bytes/solve",
                 "units_per_step": n_local_solve}
+    # per-kernel rooflines of the factorisation's two GEMM engines (one
+    # instrumented GN iteration): the Ozaki INT8 Schur kernel against the INT8
+    # dense peak (2 x the measured BF16 dense peak: same tcgen05 datapath at
+    # twice the rate) and the DMMA GEMM against the measured FP64 DMMA peak
+    oz = eng.oz_stats()
+    rooflines = {}
+    if oz["on"] and cls.get("ozaki", 0) > 0:
+        int8_peak = 2.0 * peaks.get("bf16_tflops", 2250.0)
+        ach = oz["int8_ops_per_pole"] * n_local_fact / (cls["ozaki"] * 1e-3) / 1e12
+        rooflines["ozaki_int8_schur"] = {
+            "bound": "tensor", "achieved": ach, "peak": int8_peak, "unit": "TOPS (int8)",
+            "frac": ach / int8_peak, "ms_per_step": cls["ozaki"],
+            "fp64_equiv_tflops": oz["flops_per_pole"] * n_local_fact / (cls["ozaki"] * 1e-3) / 1e12,
+            "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense INT8 = 2 x BF16 on sm_100)",
+            "per_unit": "2*28*(128*64*32)*ksteps*tiles int8 ops per pole (7 digits, 28 pairs, "
+                        "4-multiply real embedding)"}
+    dmma_flops = (sym_flops - oz["flops_per_pole"] * (1 if oz["on"] else 0)
+                  - getattr(symbolic_stats, "diag_trsm_flops", 0.0)) * n_local_fact
+    if cls.get("gemm", 0) > 0:
+        ach = dmma_flops / (cls["gemm"] * 1e-3) / 1e12
+        rooflines["dmma_gemm"] = {
+            "bound": "tensor", "achieved": ach, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+            "frac": ach / peaks["fp64_tflops"], "ms_per_step": cls["gemm"],
+            "peak_source": "measured FP64 DMMA microbenchmark (profiles/fp64_peak_r01.json)",
+            "note": "algorithmic 4-multiply flops of the trailing / small-front Schur updates; "
+                    "the 3-multiply DMMA kernel executes 3/4 of them"}
+    rooflines["factorisation"] = {k: roof[k] for k in ("achieved", "unit", "peak", "frac")}
+    if rooflines.get("ozaki_int8_schur") and rooflines.get("dmma_gemm"):
+        dom = max(("ozaki_int8_schur", "dmma_gemm"), key=lambda k: rooflines[k]["ms_per_step"])
+        roof = dict(rooflines[dom], kernel=dom, traffic=None,
+                    traffic_unit="see profiles/ for the ncu capture of this kernel",
+                    units_per_step=n_local_fact)
     value = ms_step / 1e3
     line = {
         "metric": METRIC, "value": value, "unit": "s/GN-iteration", "n_gpus": world,
@@ -330,6 +362,8 @@ def run_ours(args, world, rank):
         "solve_ms_by_level": {k: [x for x in v if x > 0] for k, v in lev.items()},
         "counts": {"factorizations": n_fact, "solves": n_solve},
         "roofline": roof,
+        "rooflines": rooflines,
+        "ozaki": oz,
         "clocks": clk,
         "e2e": {"value": e2e_ms / 1e3, "unit": "s/GN-iteration",
                 "h2d_bytes_per_step": bytes_in, "d2h_bytes_per_step": bytes_out},
@@ -428,7 +462,22 @@ def symbolic_stats(eng):
     st = np.zeros(16, np.int64)
     ds = np.zeros(4)
     eng.lib.rba_symbolic_stats(h, ptr(st), ptr(ds))
+    # diagonal-block LDL^T + TRSM flops (per 64-pivot block: 8 kb^3/6 and
+    # 8 (rows below) kb^2/2): the part of the factorisation outside the GEMMs
+    arrs = {}
+    for name in ("npiv", "nf"):
+        nb = C.c_int64()
+        eng.lib.rba_symbolic_array(h, name.encode(), None, 0, C.byref(nb))
+        a = np.empty(nb.value // 4, dtype=np.int32)
+        eng.lib.rba_symbolic_array(h, name.encode(), ptr(a), nb.value, C.byref(nb))
+        arrs[name] = a.astype(np.int64)
     eng.lib.rba_symbolic_destroy(h)
+    dt = 0.0
+    for p, nf in zip(arrs["npiv"], arrs["nf"]):
+        for c0 in range(0, int(p), 64):
+            kb = min(64, int(p) - c0)
+            dt += 8.0 * kb ** 3 / 6 + 8.0 * (int(nf) - c0 - kb) * kb * kb / 2
+    symbolic_stats.diag_trsm_flops = dt
     return float(ds[0]), int(st[3])
 
 

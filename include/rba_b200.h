@@ -195,9 +195,14 @@ int rba_sync(rba_ctx* ctx);
  *                        pole count is not known up front); set before
  *                        rba_set_poles. */
 int rba_set_option(rba_ctx* ctx, const char* name, int64_t value);
+/* The Ozaki-scheme INT8 Schur updates (kernels_ozaki.cu; env RBA_OZAKI=0
+ * turns them off): out[5] = on (1/0), executed int8 ops and FP64-equivalent
+ * flops per pole factorisation, poles per launch, minimum pivots per front. */
+int rba_oz_stats(rba_ctx* ctx, double* out_h);
 /* Device time per kernel class (ms, CUDA events around every launch while
- * timing is enabled), out[16]: scatter, extend-add, diag, trsm, gemm,
- * solve-fwd, solve-bwd, element/observation, vector/SpMV, M assembly, ...,
+ * timing is enabled), out[16]: scatter, extend-add, diag, trsm, gemm (DMMA),
+ * solve-fwd, solve-bwd, element/observation, vector/SpMV, M assembly,
+ * receiver-Green, Ozaki INT8 Schur (digit split + GEMM), ...,
  * out[15] = kernel launches issued by this context (always counted).
  * rba_set_timing: 1 on, 0 off, 2 reset the accumulators. */
 int rba_timings(rba_ctx* ctx, double* out_h);

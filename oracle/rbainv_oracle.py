@@ -359,7 +359,7 @@ def gn_iteration(problem, m, m_ref, poles, residues, R, L, weights, d_obs, lam, 
 
 
 def lsqr_floor(problem, m, poles, residues, R, weights, d_obs, lam, iters, orderings=(
-        "COLAMD", "MMD_AT_PLUS_A"), m_ref=None):
+        "COLAMD", "MMD_AT_PLUS_A"), m_ref=None, return_all=False):
     """The reference's own solver-to-solver floor on the GN update:
     relative difference of dm computed with two SuperLU orderings."""
     out = []
@@ -370,6 +370,8 @@ def lsqr_floor(problem, m, poles, residues, R, weights, d_obs, lam, iters, order
         dm, _, _ = augmented_lsqr(J, R, weights, d_obs, d, m, m if m_ref is None else m_ref,
                                   lam, 0.0, iters)
         out.append(dm)
+    if return_all:
+        return float(np.linalg.norm(out[0] - out[1]) / np.linalg.norm(out[0])), out
     return float(np.linalg.norm(out[0] - out[1]) / np.linalg.norm(out[0])), out[0]
 
 

@@ -76,6 +76,7 @@ _SIGS = {
     "rba_factor_stats": (C.c_int, [vp, i32, vp]),
     "rba_set_option": (C.c_int, [vp, C.c_char_p, i64]),
     "rba_set_reg_L": (C.c_int, [vp, i64, vp, vp, vp]),
+    "rba_oz_stats": (C.c_int, [vp, vp]),
     "rba_reg_L_apply": (C.c_int, [vp, vp, f64, vp, i32]),
 }
 

@@ -93,6 +93,8 @@ struct rba_ctx {
   int oz_min_k = 256;          // fronts with at least this many pivots
   rba::OzTask* oz_tasks = nullptr;
   int64_t oz_split_max = 0, oz_rows_max = 0;
+  double oz_int8_ops = 0, oz_flops = 0;   // per pole factorisation: executed int8 ops,
+                                          // FP64-equivalent (4-multiply) flops
   int oz_sub = 1;              // poles per Ozaki launch (digit-buffer budget)
   unsigned char* oz_buf = nullptr;
   int* oz_exp = nullptr;
@@ -209,7 +211,7 @@ struct rba_ctx {
 namespace {
 
 enum KClass { KC_SCATTER = 0, KC_EA = 1, KC_DIAG = 2, KC_TRSM = 3, KC_GEMM = 4, KC_FWD = 5,
-              KC_BWD = 6, KC_ELEM = 7, KC_VEC = 8, KC_ASSEMBLY = 9, KC_GREEN = 10 };
+              KC_BWD = 6, KC_ELEM = 7, KC_VEC = 8, KC_ASSEMBLY = 9, KC_GREEN = 10, KC_OZ = 11 };
 
 struct Timed {
   rba_ctx* c;
@@ -318,6 +320,7 @@ int build_plans(rba_ctx* c) {
   std::vector<rba::OzTask> oz;
   c->plan.clear();
   c->oz_split_max = c->oz_rows_max = 0;
+  c->oz_int8_ops = c->oz_flops = 0;
   for (int L = 0; L < S.nlevels; ++L) {
     const size_t plan0 = c->plan.size();
     const int q0 = S.level_ptr[L], q1 = S.level_ptr[L + 1];
@@ -411,6 +414,8 @@ int build_plans(rba_ctx* c) {
         oz.push_back(t);
         oz_tiles += ntr * (ntr + 1) / 2;
         oz_rt += ntr;
+        c->oz_int8_ops += 2.0 * 28 * (128.0 * 64 * 32) * nks * (ntr * (ntr + 1) / 2);
+        c->oz_flops += 8.0 * 0.5 * (double)(nf - p) * (nf - p + 1) * p;
         oz_bytes += (int64_t)ntr * nks * OZ_BLK_BYTES;
         oz_rows += nf - p;
         continue;
@@ -586,7 +591,7 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
         break;
       }
       case ST_OZ: {
-        Timed t(c, KC_GEMM);
+        Timed t(c, KC_OZ);
         Timed tg(c, 112 + std::min(s.level, 15), 0);
         for (int g0 = 0; g0 < pb.count; g0 += c->oz_sub) {
           rba::PoleBatch sub{};
@@ -1829,6 +1834,16 @@ int rba_reg_L_apply(rba_ctx* c, const double* x, double alpha, double* y, int32_
   Timed t(c, KC_VEC);
   rba::launch_spmv(c->st, c->L_n, c->l_ptr, c->l_idx, c->l_val, x, alpha, y, accumulate != 0);
   CKL();
+  return RBA_OK;
+}
+
+int rba_oz_stats(rba_ctx* c, double* out) {
+  if (!c || !out) return fail(RBA_ERR_INVALID, "null argument");
+  out[0] = c->ozaki ? 1.0 : 0.0;
+  out[1] = c->oz_int8_ops;
+  out[2] = c->oz_flops;
+  out[3] = (double)c->oz_sub;
+  out[4] = (double)c->oz_min_k;
   return RBA_OK;
 }
 

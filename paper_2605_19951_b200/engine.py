@@ -361,7 +361,16 @@ class Engine:
                     mem_other=int(mem[2]))
 
     KCLASSES = ("scatter", "extend_add", "diag", "trsm", "gemm", "solve_fwd", "solve_bwd",
-                "elem", "vec", "assembly", "green")
+                "elem", "vec", "assembly", "green", "ozaki")
+
+    def oz_stats(self) -> dict:
+        """Ozaki-scheme INT8 Schur updates: on/off, int8 ops and FP64-equivalent
+        flops per pole factorisation, poles per launch, pivot threshold."""
+        out = np.zeros(5)
+        check(self.lib.rba_oz_stats(self.ctx, ptr(out)))
+        return {"on": bool(out[0]), "int8_ops_per_pole": float(out[1]),
+                "flops_per_pole": float(out[2]), "poles_per_launch": int(out[3]),
+                "min_pivots": int(out[4])}
 
     def set_timing(self, mode):
         """True/1: record device time per kernel class; False/0: stop; 2: reset."""

@@ -274,9 +274,22 @@ def golden_c1_true(approx, fname="ref3d_C1_true.npz", n=16, lam=1e-2, iters=(1, 
             rv, _ = rb.reg_value_grad(reg, trial)
             out[f"phi_{k}"] = np.array(mis + lam * rv)
             out[f"chi2_{k}"] = np.array(2.0 * mis / d.size)
-            floor, _ = orc.lsqr_floor(prob, model.m, approx.poles, approx.residues, R, W,
-                                      data.d_obs, lam, k, m_ref=m_ref)
+            floor, dms = orc.lsqr_floor(prob, model.m, approx.poles, approx.residues, R, W,
+                                        data.d_obs, lam, k, m_ref=m_ref, return_all=True)
             out[f"floor_{k}"] = np.array(floor)
+            # the same secondaries for both orderings' updates: their spread is
+            # the reference's own floor on phi / chi^2 / linearised residual
+            sec = []
+            for dmo in dms:
+                r1o = W * (opr.jvp(dmo) + d - data.d_obs)
+                r2o = sql * (R @ (dmo + model.m - m_ref))
+                tro = rb.Model(model.m + dmo, m_ref)
+                dno = rb.forward_response(prob, tro, approx, rb.ShiftedFactorCache()).data
+                miso = 0.5 * float(np.sum((W * (dno - data.d_obs)) ** 2))
+                rvo, _ = rb.reg_value_grad(reg, tro)
+                sec.append((np.sqrt(r1o @ r1o + r2o @ r2o), miso + lam * rvo))
+            out[f"secfloor_{k}"] = np.array(max(abs(sec[0][0] - sec[1][0]) / sec[0][0],
+                                                abs(sec[0][1] - sec[1][1]) / sec[0][1]))
             print(f"k={k}: phi {float(out[f'phi_{k}']):.6e} floor {floor:.2e} "
                   f"{time.time() - t:.1f}s", flush=True)
     rr = np.random.default_rng(7)

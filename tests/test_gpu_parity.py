@@ -347,8 +347,12 @@ def test_c1_true_model_gn_update(gpu):
             ephi = abs(mis + lam * rv - float(z[f"phi_{k}"])) / float(z[f"phi_{k}"])
             echi = abs(2 * mis / dn.size - float(z[f"chi2_{k}"])) / float(z[f"chi2_{k}"])
             msg += f", phi after step {ephi:.1e}, chi2 {echi:.1e}"
+        # the reference's own secondaries floor (SuperLU COLAMD vs MMD_AT_PLUS_A,
+        # same inputs) where the golden carries it, else the dm floor
+        sec = float(z[f"secfloor_{k}"]) if f"secfloor_{k}" in z else floor
+        msg += f" (secondaries floor {sec:.1e})"
         print(msg)
         assert err <= max(1e-8, 10 * floor), msg
-        assert elin <= 1e-8, msg
-        if k == 20:
-            assert ephi <= 10 * floor and echi <= 10 * floor, msg
+        assert elin <= max(1e-8, 10 * sec), msg
+        if k in (5, 20):
+            assert ephi <= max(1e-8, 10 * sec) and echi <= max(1e-8, 10 * sec), msg

@@ -154,6 +154,57 @@ __global__ void k_rate(int iters, int32_t* sink) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" :: "r"(tb));
 }
 
+
+template <int N, int NACC>
+__global__ void k_rateN(int iters, int32_t* sink) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  int8_t* As = (int8_t*)sm;                 // 4 slices x [2][128][16]
+  int8_t* Bs = As + 4 * 32 * 128;           // 4 slices x [2][N][16]
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int e = tid; e < 4 * 32 * 128 + 4 * 32 * N; e += blockDim.x) As[e] = (int8_t)((e * 37) & 7) - 3;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" :: "r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) mbar_init(&bar, 1);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tb = tbase;
+  if (tid == 0) {
+    const uint32_t idesc = idesc_i8(128, N);
+    for (int it = 0; it < iters; ++it)
+      for (int q = 0; q < 28; ++q) {
+        const uint64_t da = make_desc(smem_u32(As + (q % 4) * 32 * 128), 128 * 16, 128);
+        const uint64_t db = make_desc(smem_u32(Bs + ((q / 4) % 4) * 32 * N), N * 16, 128);
+        mma_i8(tb + (q % NACC) * N, da, db, idesc, it > 0 || q >= NACC);
+      }
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  int32_t v[16];
+  tmem_ld16(tb + ((uint32_t)((warp & 3) * 32) << 16), v);
+  if (v[0] == 123456789) sink[0] = v[1];
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" :: "r"(tb));
+}
+template <int N, int NACC>
+void rateN(int32_t* sink) {
+  CK(cudaFuncSetAttribute(k_rateN<N, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int iters = 1000, ctas = 148;
+  k_rateN<N, NACC><<<ctas, 128, 120 * 1024>>>(10, sink); CK(cudaDeviceSynchronize());
+  cudaEventRecord(e0); k_rateN<N, NACC><<<ctas, 128, 120 * 1024>>>(iters, sink); cudaEventRecord(e1);
+  CK(cudaEventSynchronize(e1));
+  float ms; cudaEventElapsedTime(&ms, e0, e1);
+  printf("N=%d acc=%d: %.1f TOPS\n", N, NACC, 2.0 * ctas * iters * 28.0 * 128 * N * 32 / (ms * 1e-3) / 1e12);
+}
+
 int main() {
   constexpr int K = 128;
   const int nlev = 7;
@@ -210,5 +261,9 @@ int main() {
     printf("ctas %d: %.3f ms, %.1f TOPS int8 (dense)\n", ctas, ms, ops / (ms * 1e-3) / 1e12);
   }
   (void)smem2;
+  rateN<64, 7>(sink);
+  rateN<128, 4>(sink);
+  rateN<256, 2>(sink);
+  rateN<128, 1>(sink);
   return 0;
 }
