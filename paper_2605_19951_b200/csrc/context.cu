@@ -53,6 +53,7 @@ struct Step {
   int level;
   int64_t oz_split = 0;   // ST_OZ: digit-block bytes per pole
   int64_t oz_rows = 0;    // ST_OZ: border rows (row exponents) per pole
+  int64_t oz_tile_off = 0;  // ST_OZ: offset of the step's tile list
 };
 constexpr int64_t OZ_BLK_BYTES = 7 * 2 * 192 * 16;  // kernels_ozaki.cu OZ_BLK (A_big + B)
 
@@ -92,6 +93,7 @@ struct rba_ctx {
   bool ozaki = true;           // RBA_OZAKI=0: DMMA for every Schur update
   int oz_min_k = 256;          // fronts with at least this many pivots
   rba::OzTask* oz_tasks = nullptr;
+  int2* oz_tiles = nullptr;    // (row tile, column tile) per CTA, L2-friendly order
   int64_t oz_split_max = 0, oz_rows_max = 0;
   double oz_int8_ops = 0, oz_flops = 0;   // per pole factorisation: executed int8 ops,
                                           // FP64-equivalent (4-multiply) flops
@@ -318,6 +320,7 @@ int build_plans(rba_ctx* c) {
   std::vector<rba::PanelTask> pt;
   std::vector<rba::GemmTask> gm;
   std::vector<rba::OzTask> oz;
+  std::vector<int2> ozt;
   c->plan.clear();
   c->oz_split_max = c->oz_rows_max = 0;
   c->oz_int8_ops = c->oz_flops = 0;
@@ -398,6 +401,7 @@ int build_plans(rba_ctx* c) {
     int64_t goff = gm.size();
     int tiles = 0;
     const int64_t ooff = oz.size();
+    const int64_t otoff = ozt.size();
     int oz_tiles = 0, oz_rt = 0;
     int64_t oz_bytes = 0, oz_rows = 0;
     for (int q = q0; q < q1; ++q) {
@@ -412,9 +416,18 @@ int build_plans(rba_ctx* c) {
         t.tile_start = oz_tiles; t.rt_start = oz_rt;
         t.split_off = oz_bytes; t.exp_off = oz_rows;
         oz.push_back(t);
-        oz_tiles += ntr * (ntr + 1) / 2;
+        // lower-triangle 64 x 64 tiles in 12 x 12 super-blocks (column-major
+        // inside): the ~148 CTAs resident at a time reuse each other's digit
+        // blocks in L2
+        constexpr int SB = 12;
+        const int nt = ntr * (ntr + 1) / 2;
+        for (int I = 0; I < ntr; I += SB)
+          for (int J = 0; J <= I + SB - 1 && J < ntr; J += SB)
+            for (int j = J; j < std::min(J + SB, ntr); ++j)
+              for (int i = std::max(I, j); i < std::min(I + SB, ntr); ++i) ozt.push_back(make_int2(i, j));
+        oz_tiles += nt;
         oz_rt += ntr;
-        c->oz_int8_ops += 2.0 * 28 * (128.0 * 64 * 32) * nks * (ntr * (ntr + 1) / 2);
+        c->oz_int8_ops += 2.0 * 28 * (128.0 * 64 * 32) * nks * nt;
         c->oz_flops += 8.0 * 0.5 * (double)(nf - p) * (nf - p + 1) * p;
         oz_bytes += (int64_t)ntr * nks * OZ_BLK_BYTES;
         oz_rows += nf - p;
@@ -428,6 +441,7 @@ int build_plans(rba_ctx* c) {
       Step st{ST_OZ, ooff, (int)(oz.size() - ooff), oz_tiles, oz_rt, 0};
       st.oz_split = oz_bytes;
       st.oz_rows = oz_rows;
+      st.oz_tile_off = otoff;
       c->plan.push_back(st);
       c->oz_split_max = std::max(c->oz_split_max, oz_bytes);
       c->oz_rows_max = std::max(c->oz_rows_max, oz_rows);
@@ -439,6 +453,7 @@ int build_plans(rba_ctx* c) {
   if ((rc = upload(c, c->allocs, &c->pt_tasks, pt.data(), pt.size()))) return rc;
   if ((rc = upload(c, c->allocs, &c->gm_tasks, gm.data(), gm.size()))) return rc;
   if (!oz.empty() && (rc = upload(c, c->allocs, &c->oz_tasks, oz.data(), oz.size()))) return rc;
+  if (!ozt.empty() && (rc = upload(c, c->allocs, &c->oz_tiles, ozt.data(), ozt.size()))) return rc;
 
   // solve plans
   std::vector<rba::SolveTask> ft, bt, ftb, btb;
@@ -603,7 +618,8 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
             sub.xi[i] = pb.xi[g0 + i];
           }
           c->launches += 1;
-          rba::launch_oz_schur(c->st, c->oz_tasks + s.off, s.n, s.schur, s.ntiles, c->F, sub,
+          rba::launch_oz_schur(c->st, c->oz_tasks + s.off, s.n, c->oz_tiles + s.oz_tile_off, s.schur,
+                               s.ntiles, c->F, sub,
                                c->oz_buf, s.oz_split, c->oz_exp, s.oz_rows);
         }
         break;

@@ -65,12 +65,16 @@ __device__ __forceinline__ void mbar_init_(uint64_t* bar, int n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" :: "r"(su32(bar)), "r"(n) : "memory");
 }
 __device__ __forceinline__ void mbar_wait_(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0, tries = 0;
+  uint32_t done = 0;
+  long long t0 = 0;
   do {
     asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
                  " selp.u32 %0, 1, 0, p;\n}\n"
                  : "=r"(done) : "r"(su32(bar)), "r"(parity) : "memory");
-    if (++tries > (1u << 28)) __trap();
+    if (!done) {                       // a lost copy / commit must not hang the device
+      if (t0 == 0) t0 = clock64();
+      else if (clock64() - t0 > 40000000000LL) __trap();
+    }
   } while (!done);
 }
 }  // namespace
@@ -181,6 +185,7 @@ struct OzSmem {
 };
 
 __global__ void __launch_bounds__(128, 1) k_oz_gemm(const OzTask* __restrict__ tasks, int ntasks,
+                                                    const int2* __restrict__ tiles,
                                                     FrontsDev F, PoleBatch pb,
                                                     const unsigned char* __restrict__ split,
                                                     int64_t split_pole, const int* __restrict__ expo,
@@ -198,9 +203,10 @@ __global__ void __launch_bounds__(128, 1) k_oz_gemm(const OzTask* __restrict__ t
     ti = lo;
   }
   const OzTask tk = tasks[ti];
-  int local = tile - tk.tile_start, tj = 0;
-  while (local >= tk.nrt - tj) { local -= tk.nrt - tj; ++tj; }
-  const int tr = tj + local;                   // row tile >= column tile
+  // tiles in L2-friendly order (host: 12 x 12 super-blocks of the lower
+  // triangle, so the CTAs resident together share row and column digit blocks)
+  const int2 tt = __ldg(tiles + tile);
+  const int tr = tt.x, tj = tt.y;              // row tile >= column tile
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const unsigned char* sp = split + (int64_t)slot * split_pole + tk.split_off;
   const unsigned char* srcA = sp + (int64_t)tr * tk.nks * OZ_BLK;
@@ -311,7 +317,8 @@ __global__ void __launch_bounds__(128, 1) k_oz_gemm(const OzTask* __restrict__ t
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" :: "r"(tb));
 }
 
-void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, int nrowtiles, int ntiles, const FrontsDev& F, const PoleBatch& pb,
+void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int2* tiles,
+                     int nrowtiles, int ntiles, const FrontsDev& F, const PoleBatch& pb,
                      unsigned char* split, int64_t split_pole, int* expo, int64_t exp_pole) {
   if (ntasks <= 0 || ntiles <= 0) return;
   k_oz_split<<<dim3(nrowtiles, pb.count), 128, 0, st>>>(tasks, ntasks, F, pb, split,
@@ -322,7 +329,7 @@ void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, int nrowt
     cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_oz_gemm<<<dim3(ntiles, pb.count), 128, smem, st>>>(tasks, ntasks, F, pb, split, split_pole,
+  k_oz_gemm<<<dim3(ntiles, pb.count), 128, smem, st>>>(tasks, ntasks, tiles, F, pb, split, split_pole,
                                                        expo, exp_pole);
 }
 
