@@ -318,13 +318,18 @@ def run_ours(args, world, rank):
     oz = eng.oz_stats()
     rooflines = {}
     if oz["on"] and cls.get("ozaki", 0) > 0:
-        int8_peak = 2.0 * peaks.get("bf16_tflops", 2250.0)
+        try:
+            int8_peak = json.load(open(os.path.join(ROOT, "profiles", "int8_peak_r02.json")))["peak_tops"]
+            int8_src = "measured tcgen05 kind::i8 microbenchmark (profiles/int8_peak_r02.json)"
+        except OSError:
+            int8_peak = 2.0 * peaks.get("bf16_tflops", 2250.0)
+            int8_src = "2 x MEASURED_PEAKS.json bf16_tflops (dense INT8 = 2 x BF16 on sm_100)"
         ach = oz["int8_ops_per_pole"] * n_local_fact / (cls["ozaki"] * 1e-3) / 1e12
         rooflines["ozaki_int8_schur"] = {
             "bound": "tensor", "achieved": ach, "peak": int8_peak, "unit": "TOPS (int8)",
             "frac": ach / int8_peak, "ms_per_step": cls["ozaki"],
             "fp64_equiv_tflops": oz["flops_per_pole"] * n_local_fact / (cls["ozaki"] * 1e-3) / 1e12,
-            "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (dense INT8 = 2 x BF16 on sm_100)",
+            "peak_source": int8_src,
             "per_unit": "2*28*(128*64*32)*ksteps*tiles int8 ops per pole (7 digits, 28 pairs, "
                         "4-multiply real embedding)"}
     dmma_flops = (sym_flops - oz["flops_per_pole"] * (1 if oz["on"] else 0)
