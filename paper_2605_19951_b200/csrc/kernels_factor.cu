@@ -69,8 +69,6 @@ void launch_scatter_A(cudaStream_t st, int64_t nnz, const int64_t* tgt, const do
 // columns of the tile, then add every child's update block restricted to the
 // tile, children in ascending order (deterministic, no atomics).
 // ---------------------------------------------------------------------------
-constexpr int EA_RM_CAP = 6144;               // staged relmap entries (24 KB)
-
 __device__ __forceinline__ int lower_bound_i32(const int32_t* a, int n, int v) {
   int lo = 0, hi = n;
   while (lo < hi) {
@@ -118,41 +116,18 @@ __global__ void __launch_bounds__(256) k_extend_add(const int2* __restrict__ tas
     for (int r = c + threadIdx.x; r < nf; r += blockDim.x)
       upd[ucol(c - p, nf - p) + (r - c)] = cmk(0.0, 0.0);
   __syncthreads();
-  extern __shared__ int32_t rms[];           // the child's relmap rows j0.. (when they fit)
   for (int ci = F.child_ptr[s]; ci < F.child_ptr[s + 1]; ++ci) {
     const int ch = F.child_list[ci];
     const int rc = F.nf[ch] - F.npiv[ch];
     const int32_t* rm = F.relmap + F.rel_off[ch];
     const int j0 = lower_bound_i32(rm, rc, c0), j1 = lower_bound_i32(rm, rc, c1);
-    if (j0 >= j1) continue;
     const cplx* U = pb.upd[slot] + F.upd_off[ch];
-    // relmap rows j0..rc-1 staged in shared memory: the row index no longer
-    // heads a dependent global-load chain
-    const bool st = rc - j0 <= EA_RM_CAP;
-    if (st)
-      for (int i = j0 + threadIdx.x; i < rc; i += blockDim.x) rms[i - j0] = __ldg(rm + i);
-    __syncthreads();
     for (int j = j0; j < j1; ++j) {
-      const int tc = st ? rms[j - j0] : rm[j];
+      const int tc = rm[j];
       const cplx* Uc = U + ucol(j, rc);
-      // 4 rows per thread in flight: loads first, then the adds and stores
-      for (int i = j + threadIdx.x; i < rc; i += 4 * blockDim.x) {
-        cplx* dst[4];
-        cplx a[4], u[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int ii = i + q * blockDim.x;
-          dst[q] = nullptr;
-          if (ii < rc) {
-            const int r = st ? rms[ii - j0] : __ldg(rm + ii);
-            dst[q] = faddr(panel, upd, p, nf, r, tc);
-            u[q] = __ldg(Uc + (ii - j));
-            a[q] = *dst[q];
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q)
-          if (dst[q]) *dst[q] = cadd(a[q], u[q]);
+      for (int i = j + threadIdx.x; i < rc; i += blockDim.x) {
+        cplx* dst = faddr(panel, upd, p, nf, rm[i], tc);
+        *dst = cadd(*dst, Uc[i - j]);
       }
     }
     __syncthreads();
@@ -163,13 +138,7 @@ void launch_extend_add(cudaStream_t st, const int2* tasks, int ntasks, const Fro
                        const PoleBatch& pb) {
   if (ntasks <= 0) return;
   dim3 grid(ntasks, pb.count);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_extend_add, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         EA_RM_CAP * (int)sizeof(int32_t));
-    attr = true;
-  }
-  k_extend_add<<<grid, 256, EA_RM_CAP * sizeof(int32_t), st>>>(tasks, F, pb);
+  k_extend_add<<<grid, 256, 0, st>>>(tasks, F, pb);
 }
 
 // ---------------------------------------------------------------------------
