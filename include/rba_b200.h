@@ -42,6 +42,7 @@ enum {
 
 typedef struct rba_ctx rba_ctx;
 typedef struct rba_symbolic rba_symbolic;
+typedef struct rba_box rba_box;
 
 const char* rba_last_error(void);
 int rba_version(void);
@@ -67,6 +68,29 @@ int rba_mesh_prepare(int64_t N, int64_t P, int32_t k, const int32_t* cell_dofs_h
                      const double* mass_local_h, const int64_t* K_indptr_h,
                      const int32_t* K_indices_h, const double* K_data_h, const double* coords_h,
                      int32_t leaf, int64_t* out_h);
+
+/* ---- 3-D operator generation on the GPU (mesh_gen.cu) ----------------------
+ * The lowest-order Nedelec problem on a Kuhn-split n^3 hex box with PEC
+ * boundary, the 3-D counterpart of the reference's build_problem
+ * (/root/reference/pkg/src/rbainv/mesh.py:294-345): edge dofs in (low, high)
+ * vertex order, per-tet dofs and vertices, the curl-curl K (CSR, duplicates
+ * summed in element order; stiff6 = the 6 Kuhn-tet local matrices, 6x36),
+ * edge midpoints, interior-face adjacency and measures (RT0 regulariser).
+ * info[6]: N, P, nnz(K), faces, edges, vertices.  Arrays by name: "cell_dofs"
+ * (i32 P*6), "cells" (i64 P*4), "indptr" (i64 N+1), "indices" (i32), "data"
+ * (f64), "face_cells" (i32 F*2), "face_measure" (f64 F), "dof_of_edge" (i64 E),
+ * "dof_coords" (f64 N*3), "dof_offset" (i64 vertices+1: first dof of the edges
+ * leaving each vertex). */
+int rba_box_generate(int32_t n, double h, const double* stiff6_h, rba_box** out);
+int rba_box_info(const rba_box* box, int64_t* info_h);
+int rba_box_get(const rba_box* box, const char* name, void* out_h, int64_t capacity_bytes);
+void rba_box_destroy(rba_box* box);
+const char* rba_box_last_error(void);
+/* Largest generalised eigenvalue over the element pencils (K_c, e^{m_c} M_c),
+ * P cells of 6x6 matrices (mesh.py:406-421 spectral_bound): one Cholesky +
+ * power iteration per cell on the device, max over cells. */
+int rba_spectral_bound(int64_t P, const double* mass_local_h, const double* stiff_local_h,
+                       const double* m_h, double* out_h);
 
 /* ---- context ------------------------------------------------------------ */
 int rba_ctx_create(int device, void* cuda_stream, rba_ctx** out);

@@ -77,6 +77,12 @@ _SIGS = {
     "rba_set_option": (C.c_int, [vp, C.c_char_p, i64]),
     "rba_set_reg_L": (C.c_int, [vp, i64, vp, vp, vp]),
     "rba_oz_stats": (C.c_int, [vp, vp]),
+    "rba_box_generate": (C.c_int, [i32, f64, vp, C.POINTER(vp)]),
+    "rba_box_info": (C.c_int, [vp, vp]),
+    "rba_box_get": (C.c_int, [vp, C.c_char_p, vp, i64]),
+    "rba_box_destroy": (None, [vp]),
+    "rba_box_last_error": (C.c_char_p, []),
+    "rba_spectral_bound": (C.c_int, [i64, vp, vp, vp, vp]),
     "rba_reg_L_apply": (C.c_int, [vp, vp, f64, vp, i32]),
 }
 

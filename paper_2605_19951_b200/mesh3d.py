@@ -97,16 +97,18 @@ def _local_matrices(h, mu):
     return mass, stiff, curls, vol
 
 
-def build_box_problem(spec: BoxSpec, m_true=None) -> Problem:
+def _box_topology_host(spec, nodes, tet_type, mass6, stiff6):
+    """Host NumPy path of build_box_problem's topology (the reference layout):
+    tets, edge numbering (np.unique of (low, high) vertex keys), PEC edges,
+    dofs, K (COO -> CSR), edge midpoints, interior faces."""
     n, h = spec.n, spec.h
     NV1 = n + 1
-    # --- tets -----------------------------------------------------------
+    NVt = nodes.shape[0]
     hx, hy, hz = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
     hx, hy, hz = hx.ravel(order="F"), hy.ravel(order="F"), hz.ravel(order="F")
     # hex id = x + n*(y + n*z) ordering (x fastest)
     H = n ** 3
     cells = np.empty((H, 6, 4), dtype=np.int64)
-    tet_type = np.tile(np.arange(6), H)
     for t, perm in enumerate(_PERMS):
         cx, cy, cz = hx.copy(), hy.copy(), hz.copy()
         cells[:, t, 0] = _vid(n, cx, cy, cz)
@@ -120,12 +122,6 @@ def build_box_problem(spec: BoxSpec, m_true=None) -> Problem:
             cells[:, t, s + 1] = _vid(n, cx, cy, cz)
     cells = cells.reshape(H * 6, 4)
     P = cells.shape[0]
-    gx, gy, gz = np.meshgrid(np.arange(NV1), np.arange(NV1), np.arange(NV1), indexing="ij")
-    nodes = np.column_stack([gx.ravel(order="F"), gy.ravel(order="F"),
-                             gz.ravel(order="F")]).astype(float) * h
-
-    # --- edges / dofs ---------------------------------------------------
-    NVt = nodes.shape[0]
     la = np.array([e[0] for e in LOCAL_EDGES])
     lb = np.array([e[1] for e in LOCAL_EDGES])
     va, vb = cells[:, la], cells[:, lb]                     # (P, 6)
@@ -145,24 +141,131 @@ def build_box_problem(spec: BoxSpec, m_true=None) -> Problem:
     dof_of_edge[~on_bnd] = np.arange(N)
     cell_dofs = dof_of_edge[cell_edges]
     dof_coords = (0.5 * (nodes[e_lo] + nodes[e_hi]))[~on_bnd]
-
-    # --- local matrices (edge signs folded in) ----------------------------
-    mass6, stiff6, curl6, vol = _local_matrices(h, spec.mu)
     S = sign[:, :, None] * sign[:, None, :]
     mass_local = mass6[tet_type] * S
     stiff_local = stiff6[tet_type] * S
-
     k = 6
     rows = np.repeat(cell_dofs, k, axis=1).ravel()
     cols = np.tile(cell_dofs, (1, k)).ravel()
     keep = (rows >= 0) & (cols >= 0)
     K = sp.coo_matrix((stiff_local.ravel()[keep], (rows[keep], cols[keep])),
                       shape=(N, N)).tocsr()
+    # interior faces (RT0 regulariser adjacency)
+    fl = np.array([(0, 1, 2), (0, 1, 3), (0, 2, 3), (1, 2, 3)])
+    tri = np.sort(cells[:, fl], axis=2).reshape(-1, 3)                   # (4P, 3)
+    fkeys = (tri[:, 0] * NVt + tri[:, 1]) * NVt + tri[:, 2]
+    order = np.argsort(fkeys, kind="stable")
+    sk = fkeys[order]
+    dup = np.flatnonzero(sk[1:] == sk[:-1])
+    owner = np.repeat(np.arange(P), 4)
+    face_cells = np.column_stack([owner[order[dup]], owner[order[dup + 1]]])
+    t0 = tri[order[dup]]
+    p0, p1, p2 = nodes[t0[:, 0]], nodes[t0[:, 1]], nodes[t0[:, 2]]
+    face_measure = 0.5 * np.linalg.norm(np.cross(p1 - p0, p2 - p0), axis=1)
+    edge_index = {int(kk): i for i, kk in enumerate(ukeys)} if len(spec.loops) else {}
+
+    def dof_of(a, b):
+        return int(dof_of_edge[edge_index[int(min(a, b) * NVt + max(a, b))]])
+    return (P, N, cells, cell_dofs, K, dof_of_edge, dof_coords, face_cells, face_measure, sign,
+            mass_local, stiff_local, dof_of)
+
+
+_DIRS = ((1, 0, 0), (0, 1, 0), (1, 1, 0), (0, 0, 1), (1, 0, 1), (0, 1, 1), (1, 1, 1))
+
+
+def _interior_mask(n, x, y, z):
+    """Edge directions (bit d: _DIRS[d]) leaving vertex (x, y, z) that exist in
+    the box and are not PEC edges (both ends on one boundary plane)."""
+    mask = 0
+    for d, (dx, dy, dz) in enumerate(_DIRS):
+        if x + dx > n or y + dy > n or z + dz > n:
+            continue
+        bnd = (dx == 0 and x in (0, n)) or (dy == 0 and y in (0, n)) or (dz == 0 and z in (0, n))
+        if not bnd:
+            mask |= 1 << d
+    return mask
+
+
+def _box_topology_gpu(n, h, stiff6):
+    """Edge numbering, tet vertices / dofs, curl-curl K, edge midpoints and the
+    interior-face adjacency generated on the GPU (csrc/mesh_gen.cu,
+    rba_box_generate) -- the same numbering as the host path below."""
+    import ctypes as C
+    from . import _lib
+    lib = _lib.load()
+    h_ = _lib.vp()
+    st6 = np.ascontiguousarray(stiff6.reshape(6, 36), dtype=np.float64)
+    rc = lib.rba_box_generate(int(n), float(h), st6.ctypes.data, C.byref(h_))
+    if rc != 0:
+        raise RuntimeError("GPU mesh generation failed: " + lib.rba_box_last_error().decode())
+    info = np.zeros(6, np.int64)
+    lib.rba_box_info(h_, info.ctypes.data)
+    N, P, nnz, F, E, NVt = (int(v) for v in info)
+
+    def get(name, shape, dtype):
+        a = np.empty(shape, dtype=dtype)
+        rc2 = lib.rba_box_get(h_, name.encode(), a.ctypes.data, a.nbytes)
+        if rc2 != 0:
+            raise RuntimeError(lib.rba_box_last_error().decode())
+        return a
+    try:
+        out = dict(N=N, P=P,
+                   cells=get("cells", (P, 4), np.int64),
+                   cell_dofs=get("cell_dofs", (P, 6), np.int32).astype(np.int64),
+                   K=sp.csr_matrix((get("data", nnz, np.float64), get("indices", nnz, np.int32),
+                                    get("indptr", N + 1, np.int64)), shape=(N, N)),
+                   face_cells=get("face_cells", (F, 2), np.int32).astype(np.int64),
+                   face_measure=get("face_measure", F, np.float64),
+                   dof_of_edge=get("dof_of_edge", E, np.int64),
+                   dof_coords=get("dof_coords", (N, 3), np.float64),
+                   dof_offset=get("dof_offset", NVt + 1, np.int64))
+    finally:
+        lib.rba_box_destroy(h_)
+    return out
+
+
+def build_box_problem(spec: BoxSpec, m_true=None, device: bool = False) -> Problem:
+    """The 3-D Nedelec `Problem` of a BoxSpec.  device=True generates the
+    topology and K on the GPU (rba_box_generate: the same numbering and the
+    same element-order duplicate sums); the default is the host NumPy path."""
+    n, h = spec.n, spec.h
+    NV1 = n + 1
+    H = n ** 3
+    tet_type = np.tile(np.arange(6), H)
+    gx, gy, gz = np.meshgrid(np.arange(NV1), np.arange(NV1), np.arange(NV1), indexing="ij")
+    nodes = np.column_stack([gx.ravel(order="F"), gy.ravel(order="F"),
+                             gz.ravel(order="F")]).astype(float) * h
+    NVt = nodes.shape[0]
+    mass6, stiff6, curl6, vol = _local_matrices(h, spec.mu)
+    if device:
+        g = _box_topology_gpu(n, h, stiff6)
+        P, N = g["P"], g["N"]
+        cells, cell_dofs, K = g["cells"], g["cell_dofs"], g["K"]
+        dof_of_edge, dof_coords = g["dof_of_edge"], g["dof_coords"]
+        face_cells, face_measure = g["face_cells"], g["face_measure"]
+        sign = np.ones((P, 6))                    # vertex ids increase along every tet edge
+        mass_local = mass6[tet_type]
+        stiff_local = stiff6[tet_type]
+        doff = g["dof_offset"]
+
+        def dof_of(a, b):
+            lo, hi = min(a, b), max(a, b)
+            x, y, z = lo % NV1, (lo // NV1) % NV1, lo // (NV1 * NV1)
+            dx, dy, dz = hi % NV1 - x, (hi // NV1) % NV1 - y, hi // (NV1 * NV1) - z
+            d = _DIRS.index((dx, dy, dz))
+            mask = _interior_mask(n, x, y, z)
+            if not mask >> d & 1:
+                return -1
+            return int(doff[lo]) + bin(mask & ((1 << d) - 1)).count("1")
+    else:
+        (P, N, cells, cell_dofs, K, dof_of_edge, dof_coords, face_cells, face_measure, sign,
+         mass_local, stiff_local, dof_of) = _box_topology_host(spec, nodes, tet_type, mass6,
+                                                              stiff6)
+    cell_measure = np.full(P, vol)
 
     # --- sources: square loops at the air/ground interface ----------------
     z_if = n - spec.n_air
     srcs = []
-    edge_index = {int(kk): i for i, kk in enumerate(ukeys)} if len(spec.loops) else {}
     for (x0, y0, size) in spec.loops:
         f = np.zeros(N)
         path = [(x0 + i, y0, 0, +1) for i in range(size)]                 # +x along y=y0
@@ -172,8 +275,7 @@ def build_box_problem(spec: BoxSpec, m_true=None) -> Problem:
         for (x, y, ax, direction) in path:
             a = _vid(n, x, y, z_if)
             b = _vid(n, x + (ax == 0), y + (ax == 1), z_if)
-            e = edge_index[int(min(a, b) * NVt + max(a, b))]
-            d = dof_of_edge[e]
+            d = dof_of(a, b)
             if d < 0:
                 raise ValueError("source loop touches the PEC boundary")
             f[d] += spec.current * direction * (1.0 if b > a else -1.0)
@@ -198,20 +300,6 @@ def build_box_problem(spec: BoxSpec, m_true=None) -> Problem:
                 q_cols.append(d)
                 q_vals.append(val)
     Q = sp.coo_matrix((q_vals, (q_rows, q_cols)), shape=(recv.shape[0], N)).tocsr()
-
-    # --- faces (RT0 regulariser adjacency) --------------------------------
-    fl = np.array([(0, 1, 2), (0, 1, 3), (0, 2, 3), (1, 2, 3)])
-    tri = np.sort(cells[:, fl], axis=2).reshape(-1, 3)                   # (4P, 3)
-    fkeys = (tri[:, 0] * NVt + tri[:, 1]) * NVt + tri[:, 2]
-    order = np.argsort(fkeys, kind="stable")
-    sk = fkeys[order]
-    dup = np.flatnonzero(sk[1:] == sk[:-1])
-    owner = np.repeat(np.arange(P), 4)
-    face_cells = np.column_stack([owner[order[dup]], owner[order[dup + 1]]])
-    t0 = tri[order[dup]]
-    p0, p1, p2 = nodes[t0[:, 0]], nodes[t0[:, 1]], nodes[t0[:, 2]]
-    face_measure = 0.5 * np.linalg.norm(np.cross(p1 - p0, p2 - p0), axis=1)
-    cell_measure = np.full(P, vol)
 
     grid = Grid(dimension=3, nodes=nodes, cells=cells, cell_measure=cell_measure,
                 face_cells=face_cells, face_measure=face_measure,
@@ -243,11 +331,24 @@ def cell_centroids_box(n, h=1.0):
     return ((base[:, None, :] + offs[None, :, :]).reshape(-1, 3)) * h
 
 
-def spectral_bound(problem: Problem, m: np.ndarray) -> float:
+def spectral_bound(problem: Problem, m: np.ndarray, device: bool = False) -> float:
     """Largest generalized eigenvalue over the element pencils
     (stiff_c, e^{m_c} mass_c) -- vectorised form of the reference's
     `spectral_bound` (mesh.py:406-421).  The curl-curl pencil is singular in K
-    but M_c is SPD, so Cholesky of M_c is safe."""
+    but M_c is SPD, so Cholesky of M_c is safe.  device=True: one Cholesky +
+    power iteration per cell on the GPU (rba_spectral_bound), any mesh."""
+    if device:
+        from . import _lib
+        lib = _lib.load()
+        ml = np.ascontiguousarray(problem.mass_local, dtype=np.float64)
+        sl = np.ascontiguousarray(problem.stiff_local, dtype=np.float64)
+        mm = np.ascontiguousarray(m, dtype=np.float64)
+        out = np.zeros(1)
+        rc = lib.rba_spectral_bound(ml.shape[0], ml.ctypes.data, sl.ctypes.data, mm.ctypes.data,
+                                    out.ctypes.data)
+        if rc != 0:
+            raise RuntimeError("rba_spectral_bound failed: " + lib.rba_box_last_error().decode())
+        return float(out[0])
     tt = problem.extra.get("tet_type")
     if tt is not None:
         best = 0.0
@@ -401,8 +502,10 @@ def config_true_model(name: str, spec: BoxSpec) -> np.ndarray:
     return np.log(sig)
 
 
-def build_config(name: str, n: int | None = None):
+def build_config(name: str, n: int | None = None, device: bool = False):
+    """BASELINE config `name` (n overrides the mesh size); device=True builds
+    the topology and K on the GPU (rba_box_generate)."""
     spec, meta = config_spec(name, n)
     m_true = config_true_model(name, spec)
-    prob = build_box_problem(spec, m_true=m_true)
+    prob = build_box_problem(spec, m_true=m_true, device=device)
     return prob, meta

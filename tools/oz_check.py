@@ -35,3 +35,12 @@ for i in (0, 8, 15):
     out.append(float(np.linalg.norm(A @ x - b) / (nA * np.linalg.norm(x) + np.linalg.norm(b))))
 print(f"RBA_OZAKI={os.environ.get('RBA_OZAKI','0')}: factor 16 poles {min(ts):.1f} ms "
       f"gemm {cls['gemm']:.1f} ms; backward {out}; mem {eng.info()['mem_work']/1e9:.1f} GB work", flush=True)
+# forward solves of all 16 poles (4 RHS): per-level split of one instrumented call
+eng.forward(); torch.cuda.synchronize()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+e0.record(); eng.forward(); e1.record(); torch.cuda.synchronize()
+tsol = e0.elapsed_time(e1)
+eng.set_timing(2); eng.set_timing(1); eng.forward(); lev = eng.timings_detail(); cls = eng.timings(); eng.set_timing(0)
+print(f"forward (16 poles, 4 RHS): {tsol:.2f} ms; fwd {cls['solve_fwd']:.2f} bwd {cls['solve_bwd']:.2f} elem {cls['elem']:.2f}")
+print("solve_fwd_by_level", [round(x, 2) for x in lev["solve_fwd_by_level"][:15]])
+print("solve_bwd_by_level", [round(x, 2) for x in lev["solve_bwd_by_level"][:15]])
