@@ -91,7 +91,10 @@ struct rba_ctx {
   rba::GemmTask* gm_tasks = nullptr;
   // Ozaki-scheme INT8 tensor-core Schur updates (RBA_OZAKI, kernels_ozaki.cu)
   bool ozaki = true;           // RBA_OZAKI=0: DMMA for every Schur update
-  int oz_min_k = 256;          // fronts with at least this many pivots
+  int oz_min_k = 256;          // Schur updates of fronts with at least this many pivots
+  bool oz_trail = false;       // RBA_OZ_TRAIL=1: aggregated panel updates on INT8 too (+2% at
+                               // RBA_PANEL=16, slightly larger backward error): off
+  int oz_min_rows = 512;       // aggregated panel updates with at least this many rows
   rba::OzTask* oz_tasks = nullptr;
   int2* oz_tiles = nullptr;    // (row tile, column tile) per CTA, L2-friendly order
   int64_t oz_split_max = 0, oz_rows_max = 0;
@@ -324,6 +327,47 @@ int build_plans(rba_ctx* c) {
   c->plan.clear();
   c->oz_split_max = c->oz_rows_max = 0;
   c->oz_int8_ops = c->oz_flops = 0;
+  // one plan step of Ozaki (INT8 tensor-core) updates: C[r, c] -= L'[r, t0:t1]
+  // L'[c, t0:t1]^T for clo <= c < chi, c <= r < nf, per front
+  struct OzStep { int64_t ooff = 0, otoff = 0, bytes = 0, rows = 0; int tiles = 0, rt = 0; };
+  auto oz_begin = [&]() { OzStep o; o.ooff = (int64_t)oz.size(); o.otoff = (int64_t)ozt.size(); return o; };
+  auto oz_add = [&](OzStep& o, int s, int nf, int clo, int chi, int t0, int t1) {
+    const int nrt = (nf - clo + 63) / 64, ntc = (chi - clo + 63) / 64, nks = (t1 - t0 + 15) / 16;
+    rba::OzTask t{};
+    t.s = s; t.nf = nf; t.c_lo = clo; t.c_hi = chi; t.t0 = t0; t.t1 = t1;
+    t.nrt = nrt; t.nks = nks; t.tile_start = o.tiles; t.rt_start = o.rt;
+    t.split_off = o.bytes; t.exp_off = o.rows;
+    oz.push_back(t);
+    // lower-triangle 64 x 64 tiles in 12 x 12 super-blocks (column-major
+    // inside): the ~148 CTAs resident at a time reuse each other's digit
+    // blocks in L2
+    constexpr int SB = 12;
+    int nt = 0;
+    for (int I = 0; I < nrt; I += SB)
+      for (int J = 0; J < ntc && J <= I + SB - 1; J += SB)
+        for (int j = J; j < std::min(J + SB, ntc); ++j)
+          for (int i = std::max(I, j); i < std::min(I + SB, nrt); ++i) {
+            ozt.push_back(make_int2(i, j));
+            ++nt;
+          }
+    o.tiles += nt;
+    o.rt += nrt;
+    o.bytes += (int64_t)nrt * nks * OZ_BLK_BYTES;
+    o.rows += nf - clo;
+    const double w = chi - clo;
+    c->oz_int8_ops += 2.0 * 28 * (128.0 * 64 * 32) * nks * nt;
+    c->oz_flops += 8.0 * (w * (nf - clo) - 0.5 * w * (w - 1)) * (t1 - t0);
+  };
+  auto oz_end = [&](OzStep& o, int level) {
+    if ((int64_t)oz.size() == o.ooff) return;
+    Step st{ST_OZ, o.ooff, (int)((int64_t)oz.size() - o.ooff), o.tiles, o.rt, level};
+    st.oz_split = o.bytes;
+    st.oz_rows = o.rows;
+    st.oz_tile_off = o.otoff;
+    c->plan.push_back(st);
+    c->oz_split_max = std::max(c->oz_split_max, o.bytes);
+    c->oz_rows_max = std::max(c->oz_rows_max, o.rows);
+  };
   for (int L = 0; L < S.nlevels; ++L) {
     const size_t plan0 = c->plan.size();
     const int q0 = S.level_ptr[L], q1 = S.level_ptr[L + 1];
@@ -373,6 +417,7 @@ int build_plans(rba_ctx* c) {
       // K = the whole panel (fewer, fatter tensor-core GEMM passes).
       int64_t goff = gm.size();
       int tiles = 0;
+      OzStep otr = oz_begin();
       for (int q = q0; q < q1; ++q) {
         int s = S.level_fronts[q];
         const int p = S.npiv[s];
@@ -387,6 +432,12 @@ int build_plans(rba_ctx* c) {
           t0 = pstart; t1 = pend; clo = pend; chi = p;
         }
         if (chi <= clo) continue;
+        // aggregated panel updates of tall fronts on the INT8 tensor cores
+        if (c->ozaki && c->oz_trail && t1 - t0 >= std::min(256, c->oz_min_k) &&
+            S.nf[s] - clo >= c->oz_min_rows) {
+          oz_add(otr, s, S.nf[s], clo, chi, t0, t1);
+          continue;
+        }
         int ntr = (S.nf[s] - clo + rba::GT - 1) / rba::GT;
         int ntc = (chi - clo + rba::GT - 1) / rba::GT;
         int nt = 0;
@@ -395,57 +446,27 @@ int build_plans(rba_ctx* c) {
         tiles += nt;
       }
       if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles});
+      oz_end(otr, L);
     }
     // Schur complement of each front with a border: large fronts on the INT8
     // tensor cores (Ozaki scheme), the rest with the DMMA GEMM
     int64_t goff = gm.size();
     int tiles = 0;
-    const int64_t ooff = oz.size();
-    const int64_t otoff = ozt.size();
-    int oz_tiles = 0, oz_rt = 0;
-    int64_t oz_bytes = 0, oz_rows = 0;
+    OzStep osc = oz_begin();
     for (int q = q0; q < q1; ++q) {
       int s = S.level_fronts[q];
       int p = S.npiv[s], nf = S.nf[s];
       if (nf <= p || p == 0) continue;
-      int ntr = (nf - p + rba::GT - 1) / rba::GT;
       if (c->ozaki && p >= c->oz_min_k && p <= 16384) {
-        const int nks = (p + 15) / 16;
-        rba::OzTask t{};
-        t.s = s; t.p = p; t.nf = nf; t.nrt = ntr; t.nks = nks;
-        t.tile_start = oz_tiles; t.rt_start = oz_rt;
-        t.split_off = oz_bytes; t.exp_off = oz_rows;
-        oz.push_back(t);
-        // lower-triangle 64 x 64 tiles in 12 x 12 super-blocks (column-major
-        // inside): the ~148 CTAs resident at a time reuse each other's digit
-        // blocks in L2
-        constexpr int SB = 12;
-        const int nt = ntr * (ntr + 1) / 2;
-        for (int I = 0; I < ntr; I += SB)
-          for (int J = 0; J <= I + SB - 1 && J < ntr; J += SB)
-            for (int j = J; j < std::min(J + SB, ntr); ++j)
-              for (int i = std::max(I, j); i < std::min(I + SB, ntr); ++i) ozt.push_back(make_int2(i, j));
-        oz_tiles += nt;
-        oz_rt += ntr;
-        c->oz_int8_ops += 2.0 * 28 * (128.0 * 64 * 32) * nks * nt;
-        c->oz_flops += 8.0 * 0.5 * (double)(nf - p) * (nf - p + 1) * p;
-        oz_bytes += (int64_t)ntr * nks * OZ_BLK_BYTES;
-        oz_rows += nf - p;
+        oz_add(osc, s, nf, p, nf, 0, p);
         continue;
       }
+      int ntr = (nf - p + rba::GT - 1) / rba::GT;
       gm.push_back({s, 0, p, p, nf, tiles, ntr, 0});
       tiles += ntr * (ntr + 1) / 2;
     }
     if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles, 1});
-    if ((int64_t)oz.size() > ooff) {
-      Step st{ST_OZ, ooff, (int)(oz.size() - ooff), oz_tiles, oz_rt, 0};
-      st.oz_split = oz_bytes;
-      st.oz_rows = oz_rows;
-      st.oz_tile_off = otoff;
-      c->plan.push_back(st);
-      c->oz_split_max = std::max(c->oz_split_max, oz_bytes);
-      c->oz_rows_max = std::max(c->oz_rows_max, oz_rows);
-    }
+    oz_end(osc, L);
     for (size_t q = plan0; q < c->plan.size(); ++q) c->plan[q].level = L;
   }
   int rc;
@@ -1077,6 +1098,8 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   if (const char* e = getenv("RBA_DIAG")) c->diag_v1 = std::string(e) == "v1";
   if (const char* e = getenv("RBA_OZAKI")) c->ozaki = std::string(e) != "0";
   if (const char* e = getenv("RBA_OZ_MINK")) c->oz_min_k = std::max(16, atoi(e));
+  if (const char* e = getenv("RBA_OZ_TRAIL")) c->oz_trail = std::string(e) == "1";
+  if (const char* e = getenv("RBA_OZ_MINROWS")) c->oz_min_rows = std::max(64, atoi(e));
   int rc;
   if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||
       (rc = dalloc(c, c->allocs, &c->red_part, 1024, &c->mem_other)) ||

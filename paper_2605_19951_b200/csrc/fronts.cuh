@@ -64,11 +64,15 @@ __device__ __forceinline__ cplx* faddr(cplx* panel, cplx* upd, int p, int nf, in
 struct PanelTask { int32_t s, k0, r0, pad; };
 struct GemmTask { int32_t s, t0, t1, c_lo, c_hi, tile_start, ntr, pad; };
 struct SolveTask { int32_t s, blk; };
-// Ozaki-scheme Schur update of one front (kernels_ozaki.cu): nrt row tiles of
-// 64 border rows, nks k steps of 16 pivots; its digit blocks start at
-// split_off (bytes, per pole), its row exponents at exp_off (rows, per pole)
+// One INT8-tensor-core (Ozaki scheme) update of front s (kernels_ozaki.cu):
+//   C[r, c] -= sum_{t0 <= k < t1} L'[r, k] L'[c, k],  c_lo <= c < c_hi, c <= r < nf
+// (front coordinates; columns >= npiv live in the update block).  The Schur
+// update is c_lo = npiv, c_hi = nf, [t0, t1) = [0, npiv); an aggregated panel
+// update is c_lo = panel end, c_hi = npiv, [t0, t1) = the panel.  nrt row
+// tiles of 64 rows from c_lo, nks k steps of 16; digit blocks at split_off
+// (bytes, per pole), row exponents at exp_off (rows, per pole).
 struct OzTask {
-  int32_t s, p, nf, nrt, nks, tile_start, rt_start, pad;
+  int32_t s, nf, c_lo, c_hi, t0, t1, nrt, nks, tile_start, rt_start;
   int64_t split_off, exp_off;
 };
 

@@ -115,17 +115,17 @@ __global__ void __launch_bounds__(128) k_oz_split(const OzTask* __restrict__ tas
   }
   const OzTask tk = tasks[ti];
   const int rt = blockIdx.x - tk.rt_start;
-  const int s = tk.s, p = tk.p, nf = tk.nf;
-  const int b = nf - p;
+  const int s = tk.s, nf = tk.nf, c_lo = tk.c_lo, t0 = tk.t0, t1 = tk.t1;
+  const int b = nf - c_lo;                     // rows of the region
   const cplx* __restrict__ panel = pb.factor[slot] + F.panel_off[s];
   const int tid = threadIdx.x, r = tid & 63, h = tid >> 6;
-  const int row = rt * 64 + r;                 // border row (0-based)
+  const int row = rt * 64 + r;                 // region row (0-based)
   const bool on = row < b;
-  // pass 1: row maximum over the p pivot columns
+  // pass 1: row maximum over the k range
   double m = 0.0;
   if (on)
-    for (int k = h; k < p; k += 2) {
-      const cplx v = __ldg(panel + (int64_t)k * nf + p + row);
+    for (int k = t0 + h; k < t1; k += 2) {
+      const cplx v = __ldg(panel + (int64_t)k * nf + c_lo + row);
       m = fmax(m, fmax(fabs(v.x), fabs(v.y)));
     }
   s_m[h][r] = m;
@@ -143,9 +143,9 @@ __global__ void __launch_bounds__(128) k_oz_split(const OzTask* __restrict__ tas
     unsigned long long ure[8], uim[8], unim[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const int k = ks * OZ_KS + h * 8 + j;
+      const int k = t0 + ks * OZ_KS + h * 8 + j;
       cplx v = cmk(0.0, 0.0);
-      if (on && k < p) v = __ldg(panel + (int64_t)k * nf + p + row);
+      if (on && k < t1) v = __ldg(panel + (int64_t)k * nf + c_lo + row);
       ure[j] = oz_u(v.x, e);
       uim[j] = oz_u(v.y, e);
       unim[j] = oz_u(-v.y, e);
@@ -174,44 +174,49 @@ __global__ void __launch_bounds__(128) k_oz_split(const OzTask* __restrict__ tas
 }
 
 // ---------------------------------------------------------------------------
-// INT8 tensor-core Schur GEMM, warp-specialised: warp 0 loads (bulk copies
-// into a ring of OZ_NLD stages), warp 1 issues the MMAs (one thread), all
-// four warps run the epilogue (TMEM lanes 32w..32w+31).
+// INT8 tensor-core GEMM, persistent and warp-specialised (192 threads):
+// warp 0 / lane 0 streams the digit blocks (bulk copies into a 4-stage
+// mbarrier ring, straight across tile boundaries), warp 1 / lane 0 issues the
+// 28 digit-pair MMAs per k step into the 7 TMEM level accumulators, warps 2..5
+// (TMEM lanes 32 (w mod 4) ...) read the accumulators, hand TMEM back to the
+// MMA warp and only then do the read-modify-write of C -- so the global
+// epilogue of one tile overlaps the MMAs of the next.  CTA b takes the items
+// (pole, tile) b, b + G, b + 2G, ...: each tile is still computed by exactly
+// one CTA in a fixed k and level order (deterministic).
 // ---------------------------------------------------------------------------
 struct OzSmem {
   unsigned char st[OZ_NLD][OZ_BLK];          // [stage][A_big | B] digit blocks
-  uint64_t full[OZ_NLD], empty[OZ_NLD], done;
+  uint64_t full[OZ_NLD], empty[OZ_NLD];
+  uint64_t tfull, tempty;                    // accumulators: MMA -> epilogue -> MMA
   uint32_t tbase;
 };
 
-__global__ void __launch_bounds__(128, 1) k_oz_gemm(const OzTask* __restrict__ tasks, int ntasks,
-                                                    const int2* __restrict__ tiles,
+__device__ __forceinline__ void oz_item(const OzTask* __restrict__ tasks, int ntasks,
+                                        const int2* __restrict__ tiles, int ntiles, int item,
+                                        int& slot, OzTask& tk, int& tr, int& tj) {
+  slot = item / ntiles;
+  const int tile = item - slot * ntiles;
+  int lo = 0, hi = ntasks - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (tasks[mid].tile_start <= tile) lo = mid; else hi = mid - 1;
+  }
+  tk = tasks[lo];
+  const int2 tt = __ldg(tiles + tile);
+  tr = tt.x;
+  tj = tt.y;
+}
+
+__global__ void __launch_bounds__(192, 1) k_oz_gemm(const OzTask* __restrict__ tasks, int ntasks,
+                                                    const int2* __restrict__ tiles, int ntiles,
                                                     FrontsDev F, PoleBatch pb,
                                                     const unsigned char* __restrict__ split,
                                                     int64_t split_pole, const int* __restrict__ expo,
                                                     int64_t exp_pole) {
   extern __shared__ __align__(1024) unsigned char oz_raw[];
   OzSmem& S = *reinterpret_cast<OzSmem*>(oz_raw);
-  const int slot = blockIdx.y, tile = blockIdx.x;
-  int ti = 0;
-  {
-    int lo = 0, hi = ntasks - 1;
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (tasks[mid].tile_start <= tile) lo = mid; else hi = mid - 1;
-    }
-    ti = lo;
-  }
-  const OzTask tk = tasks[ti];
-  // tiles in L2-friendly order (host: 12 x 12 super-blocks of the lower
-  // triangle, so the CTAs resident together share row and column digit blocks)
-  const int2 tt = __ldg(tiles + tile);
-  const int tr = tt.x, tj = tt.y;              // row tile >= column tile
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const unsigned char* sp = split + (int64_t)slot * split_pole + tk.split_off;
-  const unsigned char* srcA = sp + (int64_t)tr * tk.nks * OZ_BLK;
-  const unsigned char* srcB = sp + (int64_t)tj * tk.nks * OZ_BLK + OZ_ABYTES;
-  const int nks = tk.nks;
+  const int nitems = ntiles * pb.count;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" :: "r"(su32(&S.tbase)));
@@ -222,7 +227,8 @@ __global__ void __launch_bounds__(128, 1) k_oz_gemm(const OzTask* __restrict__ t
       mbar_init_(&S.full[q], 1);
       mbar_init_(&S.empty[q], 1);
     }
-    mbar_init_(&S.done, 1);
+    mbar_init_(&S.tfull, 1);
+    mbar_init_(&S.tempty, 128);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -231,85 +237,120 @@ __global__ void __launch_bounds__(128, 1) k_oz_gemm(const OzTask* __restrict__ t
   const uint32_t tb = S.tbase;
 
   if (tid == 0) {
-    // producer: stage q is refilled once the MMAs that read it committed
-    for (int ks = 0; ks < nks; ++ks) {
-      const int q = ks % OZ_NLD;
-      if (ks >= OZ_NLD) mbar_wait_(&S.empty[q], ((ks / OZ_NLD) - 1) & 1);
-      const uint32_t bar = su32(&S.full[q]);
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" :: "r"(bar), "r"(OZ_ABYTES + OZ_BBYTES) : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-                   :: "r"(su32(S.st[q])), "l"(srcA + (int64_t)ks * OZ_BLK), "r"(OZ_ABYTES), "r"(bar) : "memory");
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-                   :: "r"(su32(S.st[q] + OZ_ABYTES)), "l"(srcB + (int64_t)ks * OZ_BLK), "r"(OZ_BBYTES), "r"(bar) : "memory");
+    // ---- producer ----
+    int g = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+      int slot, tr, tj;
+      OzTask tk;
+      oz_item(tasks, ntasks, tiles, ntiles, item, slot, tk, tr, tj);
+      const unsigned char* sp = split + (int64_t)slot * split_pole + tk.split_off;
+      const unsigned char* srcA = sp + (int64_t)tr * tk.nks * OZ_BLK;
+      const unsigned char* srcB = sp + (int64_t)tj * tk.nks * OZ_BLK + OZ_ABYTES;
+      for (int ks = 0; ks < tk.nks; ++ks, ++g) {
+        const int q = g % OZ_NLD;
+        if (g >= OZ_NLD) mbar_wait_(&S.empty[q], ((g / OZ_NLD) - 1) & 1);
+        const uint32_t bar = su32(&S.full[q]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" :: "r"(bar), "r"(OZ_ABYTES + OZ_BBYTES) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                     :: "r"(su32(S.st[q])), "l"(srcA + (int64_t)ks * OZ_BLK), "r"(OZ_ABYTES), "r"(bar) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                     :: "r"(su32(S.st[q] + OZ_ABYTES)), "l"(srcB + (int64_t)ks * OZ_BLK), "r"(OZ_BBYTES), "r"(bar) : "memory");
+      }
     }
   } else if (tid == 32) {
-    // MMA issuer: 28 digit-pair products per k step into the 7 level accumulators
-    for (int ks = 0; ks < nks; ++ks) {
-      const int q = ks % OZ_NLD;
-      mbar_wait_(&S.full[q], (ks / OZ_NLD) & 1);
+    // ---- MMA issuer ----
+    int g = 0, it = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
+      int slot, tr, tj;
+      OzTask tk;
+      oz_item(tasks, ntasks, tiles, ntiles, item, slot, tk, tr, tj);
+      if (it > 0) mbar_wait_(&S.tempty, (it - 1) & 1);     // epilogue drained TMEM
       asm volatile("tcgen05.fence::after_thread_sync;\n");
-      const uint32_t abase = su32(S.st[q]), bbase = abase + OZ_ABYTES;
+      for (int ks = 0; ks < tk.nks; ++ks, ++g) {
+        const int q = g % OZ_NLD;
+        mbar_wait_(&S.full[q], (g / OZ_NLD) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const uint32_t abase = su32(S.st[q]), bbase = abase + OZ_ABYTES;
 #pragma unroll
-      for (int d = 2; d <= 8; ++d)
+        for (int d = 2; d <= 8; ++d)
 #pragma unroll
-        for (int t = 1; t < d; ++t) {
-          const int u = d - t;
-          if (t > OZ_S || u > OZ_S) continue;
-          const uint64_t da = umma_desc(abase + (t - 1) * 2 * 128 * 16, 128 * 16, 128);
-          const uint64_t db = umma_desc(bbase + (u - 1) * 2 * 64 * 16, 64 * 16, 128);
-          mma_i8(tb + (d - 2) * 64, da, db, (ks > 0 || t > 1) ? 1 : 0);
-        }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
-                   :: "r"(su32(&S.empty[q])) : "memory");
-    }
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
-                 :: "r"(su32(&S.done)) : "memory");
-  }
-  __syncwarp();
-  mbar_wait_(&S.done, 0);
-  asm volatile("tcgen05.fence::after_thread_sync;\n");
-
-  // epilogue: lane = accumulator row (warp w owns TMEM lanes 32w..32w+31)
-  const int arow = warp * 32 + lane;
-  const bool imag = arow >= 64;
-  const int lr = arow & 63;
-  const int s = tk.s, p = tk.p, nf = tk.nf, b = nf - p;
-  const int grow = tr * 64 + lr;               // border row of this accumulator row
-  const int* ex = expo + (int64_t)slot * exp_pole + tk.exp_off;
-  const int ei = grow < b ? __ldg(ex + grow) : 0;
-  cplx* upd = pb.upd[slot] + (F.upd_off[s] >= 0 ? F.upd_off[s] : 0);
-  for (int c0 = 0; c0 < 64; c0 += 16) {
-    double acc[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
-#pragma unroll
-    for (int d = 8; d >= 2; --d) {             // smallest terms first
-      uint32_t v[16];
-      const uint32_t taddr = tb + (uint32_t)((d - 2) * 64 + c0) + ((uint32_t)(warp * 32) << 16);
-      asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-                   : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-                     "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
-                     "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                   : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-      const double w = ldexp(1.0, 8 * (14 - d));
-#pragma unroll
-      for (int i = 0; i < 16; ++i) acc[i] = fma((double)(int32_t)v[i], w, acc[i]);
-    }
-    if (grow < b) {
-      double* dst[16];
-      double cur[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int gcol = tj * 64 + c0 + i;     // border column
-        dst[i] = (gcol < b && gcol <= grow)
-                     ? reinterpret_cast<double*>(upd + ucol(gcol, b) + (grow - gcol)) + (imag ? 1 : 0)
-                     : nullptr;
-        cur[i] = dst[i] ? __ldcg(dst[i]) : 0.0;
+          for (int t = 1; t < d; ++t) {
+            const int u = d - t;
+            if (t > OZ_S || u > OZ_S) continue;
+            const uint64_t da = umma_desc(abase + (t - 1) * 2 * 128 * 16, 128 * 16, 128);
+            const uint64_t db = umma_desc(bbase + (u - 1) * 2 * 64 * 16, 64 * 16, 128);
+            mma_i8(tb + (d - 2) * 64, da, db, (ks > 0 || t > 1) ? 1 : 0);
+          }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                     :: "r"(su32(&S.empty[q])) : "memory");
       }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                   :: "r"(su32(&S.tfull)) : "memory");
+    }
+  } else if (warp >= 2) {
+    // ---- epilogue: warp w reads TMEM lanes 32 (w mod 4) .. +31 ----
+    const int wq = warp & 3;
+    const int arow = wq * 32 + lane;
+    const bool imag = arow >= 64;
+    const int lr = arow & 63;
+    int it = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x, ++it) {
+      int slot, tr, tj;
+      OzTask tk;
+      oz_item(tasks, ntasks, tiles, ntiles, item, slot, tk, tr, tj);
+      mbar_wait_(&S.tfull, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      double acc[64];
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        if (dst[i]) *dst[i] = cur[i] - ldexp(acc[i], ei + __ldg(ex + tj * 64 + c0 + i) - 108);
+      for (int i = 0; i < 64; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+#pragma unroll
+        for (int d = 8; d >= 2; --d) {            // smallest terms first
+          uint32_t v[16];
+          const uint32_t taddr = tb + (uint32_t)((d - 2) * 64 + c0) + ((uint32_t)(wq * 32) << 16);
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                         "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+                         "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                       : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          const double w = ldexp(1.0, 8 * (14 - d));
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[c0 + i] = fma((double)(int32_t)v[i], w, acc[c0 + i]);
+        }
+      }
+      // TMEM is free for the next tile's MMAs
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" :: "r"(su32(&S.tempty)) : "memory");
+      const int s = tk.s, nf = tk.nf, c_lo = tk.c_lo, c_hi = tk.c_hi;
+      const int p = F.npiv[s];
+      const int b = nf - c_lo;
+      const int grow = tr * 64 + lr;                // region row of this accumulator row
+      if (grow < b) {
+        const int* ex = expo + (int64_t)slot * exp_pole + tk.exp_off;
+        const int ei = __ldg(ex + grow);
+        cplx* panel = pb.factor[slot] + F.panel_off[s];
+        cplx* upd = pb.upd[slot] + (F.upd_off[s] >= 0 ? F.upd_off[s] : 0);
+        const int r = c_lo + grow;                   // front row
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          double* dst[16];
+          double cur[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int gcol = tj * 64 + c0 + i;
+            const int c = c_lo + gcol;               // front column
+            dst[i] = (c < c_hi && gcol <= grow)
+                         ? reinterpret_cast<double*>(faddr(panel, upd, p, nf, r, c)) + (imag ? 1 : 0)
+                         : nullptr;
+            cur[i] = dst[i] ? __ldcg(dst[i]) : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (dst[i]) *dst[i] = cur[i] - ldexp(acc[c0 + i], ei + __ldg(ex + tj * 64 + c0 + i) - 108);
+        }
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -329,8 +370,15 @@ void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int
     cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_oz_gemm<<<dim3(ntiles, pb.count), 128, smem, st>>>(tasks, ntasks, tiles, F, pb, split, split_pole,
-                                                       expo, exp_pole);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int items = ntiles * pb.count;
+  k_oz_gemm<<<std::min(items, nsm), 192, smem, st>>>(tasks, ntasks, tiles, ntiles, F, pb, split,
+                                                     split_pole, expo, exp_pole);
 }
 
 }  // namespace rba
