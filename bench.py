@@ -136,9 +136,11 @@ def measured_peaks():
     return peaks
 
 
-def build_workload(name, n_override, lsqr_override):
+def build_workload(name, n_override, lsqr_override, device=False):
     import paper_2605_19951_b200 as rb
-    prob, meta = rb.build_config(name, n=n_override)
+    # device=True: topology and K generated on the GPU (mesh_gen.cu), same
+    # problem as the host builder (tests/test_gpu_meshgen.py)
+    prob, meta = rb.build_config(name, n=n_override, device=device)
     approx = rb.config_approximant(name)
     lsqr_iters = lsqr_override or meta.get("lsqr_iters", 30)
     return prob, meta, approx, lsqr_iters
@@ -151,7 +153,7 @@ def run_ours(args, world, rank):
     from paper_2605_19951_b200.inversion import GNDriver, InversionConfig, LsqrConfig
 
     t_setup = time.perf_counter()
-    prob, meta, approx, lsqr_iters = build_workload(args.config, args.n, args.lsqr)
+    prob, meta, approx, lsqr_iters = build_workload(args.config, args.n, args.lsqr, device=True)
     m_true = rb.Model(prob.m_true, np.full(prob.grid.cell_count, np.log(0.01)))
     cache = rb.ShiftedFactorCache()
     eps_r, seed = meta.get("noise", (0.02, 2))
@@ -917,12 +919,12 @@ def run_shard(args, world, rank):
     import torch
     import paper_2605_19951_b200 as rb
     from paper_2605_19951_b200.engine import Engine
-    from paper_2605_19951_b200.parallel import PoleComm
+    from paper_2605_19951_b200.parallel import ShardComm
     from paper_2605_19951_b200 import _lib
     from paper_2605_19951_b200._lib import ptr
     G = args.shard
-    prob, meta, approx, lsqr_iters = build_workload(args.config, args.n, args.lsqr)
-    eng = Engine(prob, approx, comm=PoleComm(G, 0))
+    prob, meta, approx, lsqr_iters = build_workload(args.config, args.n, args.lsqr, device=True)
+    eng = Engine(prob, approx, comm=ShardComm(G, 0))   # rank 0's poles, no collective
     eng.set_model(prob.m_true)
     flops, nnzL = symbolic_stats(eng)
     stream = torch.cuda.current_stream()

@@ -122,6 +122,8 @@ struct rba_ctx {
   int epoch_limit = 1 << 20;  // flags/counters are monotonic in the epoch; reset before overflow
   bool fused_sweep = false;   // RBA_SWEEP=fused: one launch per sweep (cross-front counters)
   bool diag_v1 = false;       // RBA_DIAG=v1: unblocked diagonal-block kernel
+  int bwd_gemm = -1;          // RBA_BWD_GEMM: 1 / 0 force the DMMA-GEMM / GEMV backward
+                              // tasks; default: GEMM for 8 right-hand sides
   int* tickets = nullptr;
   int64_t nblocks = 0;
   // observation / sources
@@ -924,13 +926,23 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR, int prune_b =
       }
     }
     if (c->timing) cudaEventRecord(c->ev[1], c->st);
+    // backward sweeps of the large fronts: with 8 right-hand sides as FP64
+    // tensor-core GEMM tasks (k_zbwd on x: the block's rows-beyond product
+    // L'^T x is a DMMA GEMM with N = 8), else the GEMV tasks of k_bwd
+    const bool bgemm = c->bwd_gemm > 0 ? true : c->bwd_gemm == 0 ? false : NR >= 8;
+    rba::SlotPtrs xz{};
+    for (int i = 0; i < ns; ++i) xz.p[i] = b.x[i];
     for (int L = S.nlevels - 1; L >= 0 && !fwd_only; --L) {
       Timed tl(c, 48 + std::min(L, 31), 0);
       if (c->bwdb_lv[L].second > 0) {
         Timed tm(c, KC_BWD);
-        rba::launch_solve_level(c->st, false, NR, c->bwdb_tasks + c->bwdb_lv[L].first,
-                                c->bwdb_lv[L].second, ns, c->F, b, c->tickets + S.nlevels + L,
-                                c->epoch, c->parent_d, c->need_u_d, false);
+        if (bgemm)
+          rba::launch_zbwd(c->st, c->bwdb_tasks + c->bwdb_lv[L].first, c->bwdb_lv[L].second, ns, c->F, b,
+                           c->tickets + S.nlevels + L, NR, xz);
+        else
+          rba::launch_solve_level(c->st, false, NR, c->bwdb_tasks + c->bwdb_lv[L].first,
+                                  c->bwdb_lv[L].second, ns, c->F, b, c->tickets + S.nlevels + L,
+                                  c->epoch, c->parent_d, c->need_u_d, false);
         CKL();
       }
       if (c->small_lv[L].second > 0) {
@@ -1096,6 +1108,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   if (const char* e = getenv("RBA_SWEEP")) c->fused_sweep = std::string(e) == "fused";
   if (const char* e = getenv("RBA_SMALLP")) c->small_p = std::string(e) == "64" ? rba::PB : 2 * rba::PB;
   if (const char* e = getenv("RBA_DIAG")) c->diag_v1 = std::string(e) == "v1";
+  if (const char* e = getenv("RBA_BWD_GEMM")) c->bwd_gemm = atoi(e) ? 1 : 0;
   if (const char* e = getenv("RBA_OZAKI")) c->ozaki = std::string(e) != "0";
   if (const char* e = getenv("RBA_OZ_MINK")) c->oz_min_k = std::max(16, atoi(e));
   if (const char* e = getenv("RBA_OZ_TRAIL")) c->oz_trail = std::string(e) == "1";

@@ -79,7 +79,7 @@ __global__ void k_ts(const int8_t* A, const int8_t* B, int32_t* D) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" :: "r"(tb));
 }
 // rate: per stage 7 tcgen05.cp (A slices into TMEM) + 28 TS MMAs
-__global__ void k_rate(int iters, int32_t* sink) {
+__global__ void k_rate(int iters, int32_t* sink, int with_cp) {
   extern __shared__ __align__(1024) unsigned char sm[];
   int8_t* As = (int8_t*)sm;          // 7 x [2][128][16]
   int8_t* Bs = As + 7 * 4096;        // 7 x [2][64][16]
@@ -98,8 +98,9 @@ __global__ void k_rate(int iters, int32_t* sink) {
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tb = tbase;
   if (tid == 0) {
+    for (int t = 0; t < 7; ++t) cp_a(tb + 448 + t * 8, mdesc(su(As + t * 4096), 2048, 128));
     for (int it = 0; it < iters; ++it) {
-      for (int t = 0; t < 7; ++t) cp_a(tb + 448 + t * 8, mdesc(su(As + t * 4096), 2048, 128));
+      if (with_cp) for (int t = 0; t < 7; ++t) cp_a(tb + 448 + t * 8, mdesc(su(As + t * 4096), 2048, 128));
       for (int d = 2; d <= 8; ++d)
         for (int t = 1; t < d; ++t)
           mma_ts(tb + (d - 2) * 64, tb + 448 + (t - 1) * 8, mdesc(su(Bs + (d - t - 1) * 2048), 1024, 128),
@@ -140,14 +141,15 @@ int main() {
   CK(cudaFuncSetAttribute(k_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
   int32_t* sink; CK(cudaMalloc(&sink, 4));
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (int ctas : {148, 296}) {
+  for (int wc : {1, 0}) {
+    const int ctas = 148;
     const int iters = 2000;
-    k_rate<<<ctas, 128, 120 * 1024>>>(10, sink); CK(cudaDeviceSynchronize());
-    cudaEventRecord(e0); k_rate<<<ctas, 128, 120 * 1024>>>(iters, sink); cudaEventRecord(e1);
+    k_rate<<<ctas, 128, 120 * 1024>>>(10, sink, wc); CK(cudaDeviceSynchronize());
+    cudaEventRecord(e0); k_rate<<<ctas, 128, 120 * 1024>>>(iters, sink, wc); cudaEventRecord(e1);
     CK(cudaEventSynchronize(e1));
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     const double ops = 2.0 * ctas * (double)iters * 28 * 128 * 64 * 32;
-    printf("TS rate ctas %d: %.3f ms, %.1f TOPS int8\n", ctas, ms, ops / (ms * 1e-3) / 1e12);
+    printf("TS rate with_cp=%d: %.3f ms, %.1f TOPS int8\n", wc, ms, ops / (ms * 1e-3) / 1e12);
   }
   return 0;
 }
