@@ -122,6 +122,7 @@ struct rba_ctx {
   int epoch_limit = 1 << 20;  // flags/counters are monotonic in the epoch; reset before overflow
   bool fused_sweep = false;   // RBA_SWEEP=fused: one launch per sweep (cross-front counters)
   bool diag_v1 = false;       // RBA_DIAG=v1: unblocked diagonal-block kernel
+  int fwd_gemm = -1;          // RBA_FWD_GEMM: as RBA_BWD_GEMM for the forward tasks
   int bwd_gemm = -1;          // RBA_BWD_GEMM: 1 / 0 force the DMMA-GEMM / GEMV backward
                               // tasks; default: GEMM for 8 right-hand sides
   int* tickets = nullptr;
@@ -905,6 +906,9 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR, int prune_b =
     }
     CKL();
   } else {
+    // forward sweeps of the large fronts: GEMV tasks of k_fwd, or DMMA GEMM
+    // tasks (k_zfwd) with RBA_FWD_GEMM=1
+    const bool fgemm = c->fwd_gemm > 0;      // measured neutral at NR = 8 (C5): off by default
     for (int L = 0; L < S.nlevels; ++L) {
       Timed tl(c, 16 + std::min(L, 31), 0);
       const bool pr = prune_b >= 0;
@@ -919,9 +923,13 @@ int solve_slots(rba_ctx* c, const std::vector<int>& slots, int NR, int prune_b =
       if (fl.second > 0) {
         Timed tm(c, KC_FWD);
         const int nfr_lv = S.level_ptr[L + 1] - S.level_ptr[L];
-        rba::launch_solve_level(c->st, true, NR, (pr ? c->pr_fwdb : c->fwdb_tasks) + fl.first,
-                                fl.second, ns, c->F, b, c->tickets + L, c->epoch,
-                                c->parent_d, c->need_u_d, false, nfr_lv <= 2);
+        if (fgemm)
+          rba::launch_zfwd(c->st, (pr ? c->pr_fwdb : c->fwdb_tasks) + fl.first, fl.second, ns, c->F, b,
+                           c->tickets + L, NR);
+        else
+          rba::launch_solve_level(c->st, true, NR, (pr ? c->pr_fwdb : c->fwdb_tasks) + fl.first,
+                                  fl.second, ns, c->F, b, c->tickets + L, c->epoch,
+                                  c->parent_d, c->need_u_d, false, nfr_lv <= 2);
         CKL();
       }
     }
@@ -1109,6 +1117,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   if (const char* e = getenv("RBA_SMALLP")) c->small_p = std::string(e) == "64" ? rba::PB : 2 * rba::PB;
   if (const char* e = getenv("RBA_DIAG")) c->diag_v1 = std::string(e) == "v1";
   if (const char* e = getenv("RBA_BWD_GEMM")) c->bwd_gemm = atoi(e) ? 1 : 0;
+  if (const char* e = getenv("RBA_FWD_GEMM")) c->fwd_gemm = atoi(e) ? 1 : 0;
   if (const char* e = getenv("RBA_OZAKI")) c->ozaki = std::string(e) != "0";
   if (const char* e = getenv("RBA_OZ_MINK")) c->oz_min_k = std::max(16, atoi(e));
   if (const char* e = getenv("RBA_OZ_TRAIL")) c->oz_trail = std::string(e) == "1";

@@ -65,6 +65,9 @@ void launch_solve_small(cudaStream_t st, bool forward, int nr, const int32_t* fr
 // receiver-Green build: backward sweep over Z (N x Mr) as DMMA GEMMs
 void launch_zbwd(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
                  const FrontsDev& F, const SolveBatch& b, int* ticket, int Mr, const SlotPtrs& Z);
+// forward sweep of the large fronts as DMMA GEMM tasks (NR right-hand sides)
+void launch_zfwd(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
+                 const FrontsDev& F, const SolveBatch& b, int* ticket, int NR);
 void launch_perm_in(cudaStream_t st, int64_t n, int nrhs, int NR, const int32_t* perm,
                     const cplx* b, int64_t ldb, cplx* x);
 void launch_perm_out(cudaStream_t st, int64_t n, int nrhs, int NR, const int32_t* perm,

@@ -1002,6 +1002,191 @@ void launch_zbwd(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots
   else zbwd_go<8, 3>(st, tasks, ntasks, nslots, F, sb, ticket, Mr, Z);
 }
 
+// ---------------------------------------------------------------------------
+// Forward sweep of the large fronts with NR (8) right-hand sides as FP64
+// tensor-core GEMM tasks -- the k_fwd recurrence (task = front s, 64-row block
+// blk; see k_fwd) with the row reduction done by DMMA:
+//   T = L'[rows of blk, pivot columns < jmax] Y[pivot columns < jmax]   (GEMM,
+//       K = the previous pivot columns, NR columns of y)
+//   pivot block : y_blk = S^{-1} X_blk (v_blk - T)    (v = rhs + child u-vectors)
+//   border block: u     = (child u-vectors) - T       -> parent
+// CTA tile 64 rows x ZMC columns (the NR used ones), 4 warps of 32 x 16, 4 real
+// DMMAs per complex product, cp.async 2-stage pipeline over k; the flag of
+// pivot block j is awaited at the first k chunk of block j (earlier tickets).
+// ---------------------------------------------------------------------------
+template <int ZK, int ZNS>
+__global__ void __launch_bounds__(128) k_zfwd(const SolveTask* __restrict__ tasks, int nslots,
+                                              FrontsDev F, SolveBatchDev sb, int* ticket, int NR) {
+  using ZStage = ::rba::ZStage<ZK>;
+  constexpr int ZLK = ZStage::ZLK;
+  extern __shared__ __align__(16) unsigned char zsm[];
+  ZStage* st = reinterpret_cast<ZStage*>(zsm);
+  cplx(*Vs)[ZMC + 1] = reinterpret_cast<cplx(*)[ZMC + 1]>(zsm);   // overlays the stages
+  __shared__ int s_t;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_t = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int t = s_t;
+  const int slot = t % nslots;
+  const int epoch = sb.epoch[slot];
+  const SolveTask tk = tasks[t / nslots];
+  const int s = tk.s, blk = tk.blk;
+  const int p = F.npiv[s], nf = F.nf[s], first = F.first[s];
+  const int npb = (p + PB - 1) / PB;
+  const cplx* panel = sb.factor[slot] + F.panel_off[s];
+  cplx* x = sb.x[slot];
+  const cplx* uvec = sb.uvec[slot];
+  int* flags = sb.flags[slot] + F.blk_off[s];
+  const bool pivot = blk < npb;
+  const int r0 = pivot ? blk * PB : p + (blk - npb) * PB;
+  const int nr = pivot ? min(PB, p - r0) : min(PB, nf - r0);
+  const int jmax = pivot ? blk : npb;                 // pivot blocks entering the product
+  const int kend = min(jmax * PB, p);
+  const int nchunk = (kend + ZK - 1) / ZK;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+  const int g = lane >> 2, t4 = lane & 3;
+  auto issue = [&](int ch) {
+    if (ch >= nchunk) {
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+      return;
+    }
+    ZStage& S = st[ch % ZNS];
+    const int k0 = ch * ZK;
+    const int nval = min(ZK, kend - k0);
+    if (k0 % PB == 0) {
+      // first chunk of pivot block k0 / PB: its y rows must be final
+      if (tid == 0) spin_wait_geq(flags + k0 / PB, epoch);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < (PB * ZK) / 128; ++q) {
+      const int e = tid + q * 128;
+      const int i = e % PB, kk = e / PB;              // A[i][k] = L'[r0 + i, k0 + kk]
+      const bool ok = kk < nval && i < nr;
+      cp_async16(&S.a[i * ZLK + kk], panel + (ok ? (int64_t)(k0 + kk) * nf + r0 + i : 0), ok);
+    }
+#pragma unroll
+    for (int q = 0; q < (ZMC * ZK) / 128; ++q) {
+      const int e = tid + q * 128;
+      const int n = e % ZMC, kk = e / ZMC;            // B[n][k] = y[first + k0 + kk][n]
+      const bool ok = kk < nval && n < NR;
+      cp_async16(&S.b[n * ZLK + kk], x + (ok ? (int64_t)(first + k0 + kk) * NR + n : 0), ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  double cre[4][2][2], cim[4][2][2];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb) {
+      cre[a][bb][0] = cre[a][bb][1] = 0.0;
+      cim[a][bb][0] = cim[a][bb][1] = 0.0;
+    }
+  for (int c = 0; c < ZNS - 1; ++c) issue(c);
+  for (int ch = 0; ch < nchunk; ++ch) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(ZNS - 2) : "memory");
+    __syncthreads();
+    issue(ch + ZNS - 1);
+    const ZStage& S = st[ch % ZNS];
+    if (wm >= nr || wn >= NR) continue;               // warp tile outside the rows / columns
+#pragma unroll
+    for (int k4 = 0; k4 < ZK; k4 += 4) {
+      double ar[4], ai[4], an[4], br[2], bi[2];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const cplx v = S.a[(wm + a * 8 + g) * ZLK + k4 + t4];
+        ar[a] = v.x;
+        ai[a] = v.y;
+        an[a] = -v.y;
+      }
+#pragma unroll
+      for (int bb = 0; bb < 2; ++bb) {
+        const cplx v = S.b[(wn + bb * 8 + g) * ZLK + k4 + t4];
+        br[bb] = v.x;
+        bi[bb] = v.y;
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb) dmma_f64(cre[a][bb][0], cre[a][bb][1], ar[a], br[bb]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb) dmma_f64(cim[a][bb][0], cim[a][bb][1], ar[a], bi[bb]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb) dmma_f64(cre[a][bb][0], cre[a][bb][1], an[a], bi[bb]);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb) dmma_f64(cim[a][bb][0], cim[a][bb][1], ai[a], br[bb]);
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  // v = (rhs for pivot rows) + child u-vectors, in shared memory
+  for (int e = tid; e < nr * NR; e += 128) {
+    const int i = e / NR, r = e % NR;
+    const int rho = r0 + i;
+    cplx val = pivot ? x[(int64_t)(first + rho) * NR + r] : cmk(0.0, 0.0);
+    const int64_t fr = F.rows_off[s] + rho;
+    for (int64_t q = F.ucon_ptr[fr]; q < F.ucon_ptr[fr + 1]; ++q)
+      val = cadd(val, uvec[F.ucon_idx[q] * NR + r]);
+    Vs[i][r] = val;
+  }
+  __syncthreads();
+  // v - T
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = wm + a * 8 + g, n = wn + bb * 8 + t4 * 2 + h;
+        if (i < nr && n < NR) Vs[i][n] = cmk(Vs[i][n].x - cre[a][bb][h], Vs[i][n].y - cim[a][bb][h]);
+      }
+  __syncthreads();
+  if (!pivot) {
+    cplx* u = sb.uvec[slot] + (F.uvec_off[s] + (r0 - p)) * NR;
+    for (int e = tid; e < nr * NR; e += 128) u[e] = Vs[e / NR][e % NR];
+    return;
+  }
+  // y_i = s_i^{-1} (v_i + sum_{c < i} X[i][c] v_c); X[i][c] sits at (row r0+c, col r0+i)
+  for (int e = tid; e < nr * NR; e += 128) {
+    const int i = e / NR, r = e % NR;
+    const cplx* xcol = panel + (int64_t)(r0 + i) * nf + r0;
+    cplx acc = Vs[i][r];
+    for (int c = 0; c < i; ++c) acc = cfma(__ldg(xcol + c), Vs[c][r], acc);
+    x[(int64_t)(first + r0 + i) * NR + r] = cmul(acc, cinv(__ldg(xcol + i)));
+  }
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) st_release(flags + blk, epoch);
+}
+
+void launch_zfwd(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
+                 const FrontsDev& F, const SolveBatch& b, int* ticket, int NR) {
+  if (ntasks <= 0) return;
+  SolveBatchDev sb;
+  for (int i = 0; i < nslots; ++i) {
+    sb.factor[i] = b.factor[i];
+    sb.x[i] = b.x[i];
+    sb.uvec[i] = b.uvec[i];
+    sb.flags[i] = b.flags_f[i];
+    sb.done[i] = b.done_f[i];
+    sb.epoch[i] = b.epoch[i];
+  }
+  constexpr int ZK = 16, ZNS = 2;
+  const size_t smem = std::max(ZNS * sizeof(ZStage<ZK>), PB * (ZMC + 1) * sizeof(cplx));
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_zfwd<ZK, ZNS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_zfwd<ZK, ZNS><<<ntasks * nslots, 128, smem, st>>>(tasks, nslots, F, sb, ticket, NR);
+}
+
 // original-order (column-major N x nrhs complex) <-> permuted padded layout
 __global__ void k_perm_in(int64_t n, int nrhs, int NR, const int32_t* __restrict__ perm,
                           const cplx* __restrict__ b, int64_t ldb, cplx* __restrict__ x) {
