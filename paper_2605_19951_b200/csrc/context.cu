@@ -101,6 +101,7 @@ struct rba_ctx {
   double oz_int8_ops = 0, oz_flops = 0;   // per pole factorisation: executed int8 ops,
                                           // FP64-equivalent (4-multiply) flops
   int oz_sub = 1;              // poles per Ozaki launch (digit-buffer budget)
+  int oz_pair = 0;             // RBA_OZ_2CTA=1: cluster-pair (cta_group::2, M = 256) GEMM
   unsigned char* oz_buf = nullptr;
   int* oz_exp = nullptr;
   std::vector<std::pair<int64_t, int>> fwd_lv, bwd_lv, fwdb_lv, bwdb_lv, small_lv;
@@ -346,6 +347,17 @@ int build_plans(rba_ctx* c) {
     // blocks in L2
     constexpr int SB = 12;
     int nt = 0;
+    if (c->oz_pair) {
+      // cluster pairs own two row tiles (2 tr2, 2 tr2 + 1) x one column tile
+      const int np = (nrt + 1) / 2;
+      for (int I = 0; I < np; I += SB / 2)
+        for (int J = 0; J < ntc && J <= 2 * (I + SB / 2) - 1; J += SB)
+          for (int j = J; j < std::min(J + SB, ntc); ++j)
+            for (int i = std::max(I, j / 2); i < std::min(I + SB / 2, np); ++i) {
+              ozt.push_back(make_int2(i, j));
+              ++nt;
+            }
+    } else
     for (int I = 0; I < nrt; I += SB)
       for (int J = 0; J < ntc && J <= I + SB - 1; J += SB)
         for (int j = J; j < std::min(J + SB, ntc); ++j)
@@ -355,10 +367,10 @@ int build_plans(rba_ctx* c) {
           }
     o.tiles += nt;
     o.rt += nrt;
-    o.bytes += (int64_t)nrt * nks * OZ_BLK_BYTES;
+    o.bytes += (int64_t)(c->oz_pair ? (nrt + 1) / 2 * 2 : nrt) * nks * OZ_BLK_BYTES;
     o.rows += nf - clo;
     const double w = chi - clo;
-    c->oz_int8_ops += 2.0 * 28 * (128.0 * 64 * 32) * nks * nt;
+    c->oz_int8_ops += 2.0 * 28 * ((c->oz_pair ? 256.0 : 128.0) * 64 * 32) * nks * nt;
     c->oz_flops += 8.0 * (w * (nf - clo) - 0.5 * w * (w - 1)) * (t1 - t0);
   };
   auto oz_end = [&](OzStep& o, int level) {
@@ -644,7 +656,7 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
           c->launches += 1;
           rba::launch_oz_schur(c->st, c->oz_tasks + s.off, s.n, c->oz_tiles + s.oz_tile_off, s.schur,
                                s.ntiles, c->F, sub,
-                               c->oz_buf, s.oz_split, c->oz_exp, s.oz_rows);
+                               c->oz_buf, s.oz_split, c->oz_exp, s.oz_rows, c->oz_pair);
         }
         break;
       }
@@ -1121,6 +1133,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   if (const char* e = getenv("RBA_OZAKI")) c->ozaki = std::string(e) != "0";
   if (const char* e = getenv("RBA_OZ_MINK")) c->oz_min_k = std::max(16, atoi(e));
   if (const char* e = getenv("RBA_OZ_TRAIL")) c->oz_trail = std::string(e) == "1";
+  if (const char* e = getenv("RBA_OZ_2CTA")) c->oz_pair = std::string(e) == "1";
   if (const char* e = getenv("RBA_OZ_MINROWS")) c->oz_min_rows = std::max(64, atoi(e));
   int rc;
   if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||

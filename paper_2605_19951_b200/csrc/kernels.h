@@ -51,7 +51,7 @@ void launch_gemm6(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
 void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int2* tiles,
                      int nrowtiles, int ntiles,
                      const FrontsDev& F, const PoleBatch& pb, unsigned char* split,
-                     int64_t split_pole, int* expo, int64_t exp_pole);
+                     int64_t split_pole, int* expo, int64_t exp_pole, int pair);
 void launch_trsm3(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
                   const PoleBatch& pb, int variant);
 

@@ -161,8 +161,12 @@ __global__ void __launch_bounds__(NT3, 2) k_gemm3(const GemmTask* __restrict__ t
     const int kt = t0 + ch * T3K;
     // warp's 16 columns all past the block / tile edge, or 32 rows past the front
     if (cc0 + wn >= cmax || r0 + wm >= nf) continue;
+    // TRSM: X is unit lower triangular (X[c][t] = 0 for t > c), so the k
+    // range past the warp's last column contributes nothing
+    if (MODE == 1 && kt > wn + 15) continue;
 #pragma unroll
     for (int k4 = 0; k4 < T3K; k4 += 4) {
+      if (MODE == 1 && kt + k4 > wn + 15) break;
       double ar[4], ai[4], an[4], br[2], bi[2];
 #pragma unroll
       for (int a = 0; a < 4; ++a) {

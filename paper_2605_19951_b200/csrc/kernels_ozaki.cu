@@ -77,6 +77,20 @@ __device__ __forceinline__ void mbar_wait_(uint64_t* bar, uint32_t parity) {
     }
   } while (!done);
 }
+// the same with cluster-scope acquire: arrivals released by the peer CTA
+__device__ __forceinline__ void mbar_wait_cl_(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  long long t0 = 0;
+  do {
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+                 " selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done) : "r"(su32(bar)), "r"(parity) : "memory");
+    if (!done) {
+      if (t0 == 0) t0 = clock64();
+      else if (clock64() - t0 > 40000000000LL) __trap();
+    }
+  } while (!done);
+}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -100,7 +114,7 @@ __global__ void __launch_bounds__(128) k_oz_split(const OzTask* __restrict__ tas
                                                   FrontsDev F, PoleBatch pb,
                                                   unsigned char* __restrict__ split,
                                                   int64_t split_pole, int* __restrict__ expo,
-                                                  int64_t exp_pole) {
+                                                  int64_t exp_pole, int bhalf) {
   __shared__ int s_e[64];
   __shared__ double s_m[2][64];
   const int slot = blockIdx.y;
@@ -168,7 +182,11 @@ __global__ void __launch_bounds__(128) k_oz_split(const OzTask* __restrict__ tas
       }
       *reinterpret_cast<uint4*>(blk + ((t * 2 + h) * 128 + r) * 16) = wre;
       *reinterpret_cast<uint4*>(blk + ((t * 2 + h) * 128 + 64 + r) * 16) = wim;
-      *reinterpret_cast<uint4*>(blk + OZ_ABYTES + ((t * 2 + h) * 64 + r) * 16) = wb;
+      // B rows: [slice][chunk][64 rows] (one CTA per tile) or, for the
+      // cluster-pair kernel, [row half][slice][chunk][32 rows] (each CTA of
+      // the pair streams its half of the columns contiguously)
+      const int boff = bhalf ? (((r >> 5) * OZ_S + t) * 2 + h) * 32 + (r & 31) : (t * 2 + h) * 64 + r;
+      *reinterpret_cast<uint4*>(blk + OZ_ABYTES + boff * 16) = wb;
     }
   }
 }
@@ -358,18 +376,223 @@ __global__ void __launch_bounds__(192, 1) k_oz_gemm(const OzTask* __restrict__ t
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" :: "r"(tb));
 }
 
+// ---------------------------------------------------------------------------
+// Cluster-pair variant (RBA_OZ_2CTA=1): two CTAs on the two SMs of a TPC run
+// one tcgen05.mma.cta_group::2 (M = 256: 128 complex rows, N = 64): each CTA
+// streams its own 64-row A block and HALF of the 64 B columns, so per SM the
+// MMAs read 5 KB instead of 6 KB of shared memory per 262k MACs and the L2
+// traffic drops by a sixth.  The leader issues the MMAs; both CTAs' bulk
+// copies complete on the leader's stage barrier; the commits are multicast to
+// both CTAs; each CTA drains its own TMEM lanes and arrives on the leader's
+// "TMEM empty" barrier.  A non-tensor bulk copy completes only on a barrier of
+// its own CTA, so the peer's copies land on the peer's stage barrier and a
+// relay thread there forwards each completed stage to the leader's (count 2).
+// Same digits, same order, same results as k_oz_gemm.
+// ---------------------------------------------------------------------------
+constexpr int OZ_BH = OZ_S * 2 * 32 * 16;        // half of a B block (32 rows)
+constexpr uint32_t OZ_IDESC2 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(64 >> 3) << 17) |
+                               ((uint32_t)(256 >> 4) << 24);
+constexpr int OZ_NLD2 = 6;                         // deeper ring: hides the relay hop
+struct OzSmem2 {
+  unsigned char st[OZ_NLD2][OZ_ABYTES + OZ_BH];
+  uint64_t full[OZ_NLD2], empty[OZ_NLD2];
+  uint64_t tfull, tempty;
+  uint32_t tbase;
+};
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_leader(uint32_t saddr) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;\n" : "=r"(r) : "r"(saddr));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
+k_oz_gemm2(const OzTask* __restrict__ tasks, int ntasks, const int2* __restrict__ tiles, int ntiles,
+           FrontsDev F, PoleBatch pb, const unsigned char* __restrict__ split, int64_t split_pole,
+           const int* __restrict__ expo, int64_t exp_pole) {
+  extern __shared__ __align__(1024) unsigned char oz_raw2[];
+  OzSmem2& S = *reinterpret_cast<OzSmem2*>(oz_raw2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cta_rank();
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int nitems = ntiles * pb.count;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" :: "r"(su32(&S.tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  if (tid == 32) {
+    for (int q = 0; q < OZ_NLD2; ++q) {
+      mbar_init_(&S.full[q], rank == 0 ? 2 : 1);
+      mbar_init_(&S.empty[q], 1);
+    }
+    mbar_init_(&S.tfull, 1);
+    mbar_init_(&S.tempty, 256);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  cluster_sync_();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tb = S.tbase;
+
+  if (tid == 0) {
+    // ---- producer (both CTAs): own A block + own half of B ----
+    int g = 0;
+    for (int item = pair; item < nitems; item += npairs) {
+      int slot, tr2, tj;
+      OzTask tk;
+      oz_item(tasks, ntasks, tiles, ntiles, item, slot, tk, tr2, tj);
+      const int tr = 2 * tr2 + (int)rank;
+      const unsigned char* sp = split + (int64_t)slot * split_pole + tk.split_off;
+      const unsigned char* srcA = sp + (int64_t)tr * tk.nks * OZ_BLK;
+      const unsigned char* srcB = sp + (int64_t)tj * tk.nks * OZ_BLK + OZ_ABYTES + rank * OZ_BH;
+      for (int ks = 0; ks < tk.nks; ++ks, ++g) {
+        const int q = g % OZ_NLD2;
+        if (g >= OZ_NLD2) mbar_wait_(&S.empty[q], ((g / OZ_NLD2) - 1) & 1);
+        const uint32_t bar = su32(&S.full[q]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n"
+                     :: "r"(bar), "r"(OZ_ABYTES + OZ_BH) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                     :: "r"(su32(S.st[q])), "l"(srcA + (int64_t)ks * OZ_BLK), "r"(OZ_ABYTES), "r"(bar) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                     :: "r"(su32(S.st[q] + OZ_ABYTES)), "l"(srcB + (int64_t)ks * OZ_BLK), "r"(OZ_BH), "r"(bar) : "memory");
+      }
+    }
+  } else if (tid == 32 && rank == 1) {
+    // ---- relay (peer): forward each landed stage to the leader's barrier ----
+    int g = 0;
+    for (int item = pair; item < nitems; item += npairs) {
+      int slot, tr2, tj;
+      OzTask tk;
+      oz_item(tasks, ntasks, tiles, ntiles, item, slot, tk, tr2, tj);
+      for (int ks = 0; ks < tk.nks; ++ks, ++g) {
+        const int q = g % OZ_NLD2;
+        mbar_wait_(&S.full[q], (g / OZ_NLD2) & 1);
+        asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n"
+                     :: "r"(map_to_leader(su32(&S.full[q]))) : "memory");
+      }
+    }
+  } else if (tid == 32 && rank == 0) {
+    // ---- MMA issuer (leader) ----
+    int g = 0, it = 0;
+    for (int item = pair; item < nitems; item += npairs, ++it) {
+      int slot, tr2, tj;
+      OzTask tk;
+      oz_item(tasks, ntasks, tiles, ntiles, item, slot, tk, tr2, tj);
+      if (it > 0) mbar_wait_cl_(&S.tempty, (it - 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      for (int ks = 0; ks < tk.nks; ++ks, ++g) {
+        const int q = g % OZ_NLD2;
+        mbar_wait_cl_(&S.full[q], (g / OZ_NLD2) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const uint32_t abase = su32(S.st[q]), bbase = abase + OZ_ABYTES;
+#pragma unroll
+        for (int d = 2; d <= 8; ++d)
+#pragma unroll
+          for (int t = 1; t < d; ++t) {
+            const int u = d - t;
+            if (t > OZ_S || u > OZ_S) continue;
+            const uint64_t da = umma_desc(abase + (t - 1) * 2 * 128 * 16, 128 * 16, 128);
+            const uint64_t db = umma_desc(bbase + (u - 1) * 2 * 32 * 16, 32 * 16, 128);
+            asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                         " tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n}\n"
+                         :: "r"(tb + (uint32_t)((d - 2) * 64)), "l"(da), "l"(db), "r"(OZ_IDESC2),
+                            "r"((ks > 0 || t > 1) ? 1 : 0));
+          }
+        asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                     :: "r"(su32(&S.empty[q])), "h"((unsigned short)3) : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n"
+                   :: "r"(su32(&S.tfull)), "h"((unsigned short)3) : "memory");
+    }
+  } else if (warp >= 2) {
+    // ---- epilogue (both CTAs): own 128 TMEM lanes = own 64 complex rows ----
+    const int wq = warp & 3;
+    const int arow = wq * 32 + lane;
+    const bool imag = arow >= 64;
+    const int lr = arow & 63;
+    const uint32_t tempty_leader = map_to_leader(su32(&S.tempty));
+    int it = 0;
+    for (int item = pair; item < nitems; item += npairs, ++it) {
+      int slot, tr2, tj;
+      OzTask tk;
+      oz_item(tasks, ntasks, tiles, ntiles, item, slot, tk, tr2, tj);
+      const int tr = 2 * tr2 + (int)rank;
+      mbar_wait_(&S.tfull, it & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      double acc[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) acc[i] = 0.0;
+#pragma unroll
+      for (int c0 = 0; c0 < 64; c0 += 16) {
+#pragma unroll
+        for (int d = 8; d >= 2; --d) {
+          uint32_t v[16];
+          const uint32_t taddr = tb + (uint32_t)((d - 2) * 64 + c0) + ((uint32_t)(wq * 32) << 16);
+          asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                       : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+                         "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+                         "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                       : "r"(taddr));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+          const double w = ldexp(1.0, 8 * (14 - d));
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[c0 + i] = fma((double)(int32_t)v[i], w, acc[c0 + i]);
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+      asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" :: "r"(tempty_leader) : "memory");
+      const int s = tk.s, nf = tk.nf, c_lo = tk.c_lo, c_hi = tk.c_hi;
+      const int p = F.npiv[s];
+      const int b = nf - c_lo;
+      const int grow = tr * 64 + lr;
+      if (tr < tk.nrt && grow < b) {
+        const int* ex = expo + (int64_t)slot * exp_pole + tk.exp_off;
+        const int ei = __ldg(ex + grow);
+        cplx* panel = pb.factor[slot] + F.panel_off[s];
+        cplx* upd = pb.upd[slot] + (F.upd_off[s] >= 0 ? F.upd_off[s] : 0);
+        const int r = c_lo + grow;
+#pragma unroll
+        for (int c0 = 0; c0 < 64; c0 += 16) {
+          double* dst[16];
+          double cur[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const int gcol = tj * 64 + c0 + i;
+            const int c = c_lo + gcol;
+            dst[i] = (c < c_hi && gcol <= grow)
+                         ? reinterpret_cast<double*>(faddr(panel, upd, p, nf, r, c)) + (imag ? 1 : 0)
+                         : nullptr;
+            cur[i] = dst[i] ? __ldcg(dst[i]) : 0.0;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i)
+            if (dst[i]) *dst[i] = cur[i] - ldexp(acc[c0 + i], ei + __ldg(ex + tj * 64 + c0 + i) - 108);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  cluster_sync_();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" :: "r"(tb));
+}
+
 void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int2* tiles,
                      int nrowtiles, int ntiles, const FrontsDev& F, const PoleBatch& pb,
-                     unsigned char* split, int64_t split_pole, int* expo, int64_t exp_pole) {
+                     unsigned char* split, int64_t split_pole, int* expo, int64_t exp_pole,
+                     int pair) {
   if (ntasks <= 0 || ntiles <= 0) return;
   k_oz_split<<<dim3(nrowtiles, pb.count), 128, 0, st>>>(tasks, ntasks, F, pb, split,
-                                                        split_pole, expo, exp_pole);
-  const size_t smem = sizeof(OzSmem) + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
-  }
+                                                        split_pole, expo, exp_pole, pair);
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
@@ -377,6 +600,24 @@ void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   const int items = ntiles * pb.count;
+  if (pair) {
+    const size_t smem = sizeof(OzSmem2) + 1024;
+    static bool attr2 = false;
+    if (!attr2) {
+      cudaFuncSetAttribute(k_oz_gemm2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr2 = true;
+    }
+    const int npairs = std::min(items, nsm / 2);
+    k_oz_gemm2<<<2 * npairs, 192, smem, st>>>(tasks, ntasks, tiles, ntiles, F, pb, split, split_pole,
+                                               expo, exp_pole);
+    return;
+  }
+  const size_t smem = sizeof(OzSmem) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
   k_oz_gemm<<<std::min(items, nsm), 192, smem, st>>>(tasks, ntasks, tiles, ntiles, F, pb, split,
                                                      split_pole, expo, exp_pole);
 }

@@ -85,3 +85,33 @@ def test_ozaki_c1_parity(gpu, ozaki):
     ef, ej, et = rel(d, z["d"]), rel(opr.jvp(z["v"]), z["jv"]), rel(opr.vjp(z["w"]), z["jtw"])
     print(f"Ozaki C1: forward {ef:.2e} J v {ej:.2e} J^T w {et:.2e}")
     assert ef <= 1e-9 and ej <= 1e-8 and et <= 1e-8
+
+
+def _factor_bytes(monkeypatch, n, pair):
+    monkeypatch.setenv("RBA_OZ_2CTA", "1" if pair else "0")
+    prob, _ = rb.build_config("C4", n=n)
+    approx = rb.config_approximant("C4")
+    eng = Engine(prob, None)
+    eng.set_poles(approx)
+    eng.set_model(prob.m_true)
+    eng.factor()
+    S = mf.analyze(prob.K, prob.dof_coords, 64)
+    tot = int(S["panel_off"][-1])
+    out = []
+    for pole in (0, 9):
+        buf = np.empty(tot, dtype=np.complex128)
+        _lib.check(eng.lib.rba_get_factor(eng.ctx, pole, ptr(buf.view(np.float64)), tot))
+        out.append(buf)
+    eng.close()
+    return out
+
+
+def test_ozaki_cluster_pair_bitwise(gpu, ozaki, monkeypatch):
+    """The cta_group::2 GEMM (RBA_OZ_2CTA=1) accumulates the same digit
+    products in the same order as the one-SM kernel: factors bitwise equal
+    (odd and even row-tile counts, fronts wider than one 12-tile super-block)."""
+    for n in (10, 20):
+        a = _factor_bytes(monkeypatch, n, False)
+        b = _factor_bytes(monkeypatch, n, True)
+        for x, y in zip(a, b):
+            assert np.array_equal(x.view(np.uint64), y.view(np.uint64))

@@ -14,6 +14,7 @@ import scipy.sparse.linalg as spla
 
 from conftest import golden, rel
 import paper_2605_19951_b200 as rb
+from paper_2605_19951_b200.engine import Engine
 from oracle import rbainv_oracle as orc
 
 pytestmark = pytest.mark.gpu
@@ -356,3 +357,24 @@ def test_c1_true_model_gn_update(gpu):
         assert elin <= max(1e-8, 10 * sec), msg
         if k in (5, 20):
             assert ephi <= max(1e-8, 10 * sec) and echi <= max(1e-8, 10 * sec), msg
+
+
+@pytest.mark.parametrize("air", [False, True])
+def test_device_mass_assembly_vs_assemble_M(gpu, air):
+    """K1 (k_exp + k_assemble_M, the device gather of sum_c e^{m_c} M_c) against
+    the oracle's COO->CSR assemble_M (mesh.py:348-355), entry by entry on the
+    lower-triangle pattern, at the true model with 1e-8 S/m air and at the
+    homogeneous start model; K against problem.K."""
+    prob, _ = rb.build_config("C1", n=10)
+    m = prob.m_true if air else np.full(prob.m_true.shape, np.log(0.01))
+    eng = Engine(prob, None)
+    eng.set_model(m)
+    rows, cols, Kv, Mv = eng.pattern(with_M=True)
+    M = orc.assemble_M(prob, m).tocsr()
+    Mref = np.asarray(M[rows, cols]).ravel()
+    Kref = np.asarray(prob.K.tocsr()[rows, cols]).ravel()
+    assert np.all(rows >= cols) and np.count_nonzero(Mref) == sp.tril(M).count_nonzero()
+    scale = np.abs(Mref).max()
+    assert np.abs(Mv - Mref).max() <= 1e-14 * scale
+    np.testing.assert_allclose(Kv, Kref, rtol=0, atol=1e-14 * np.abs(Kref).max())
+    eng.close()
