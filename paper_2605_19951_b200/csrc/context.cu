@@ -102,6 +102,7 @@ struct rba_ctx {
                                           // FP64-equivalent (4-multiply) flops
   int oz_sub = 1;              // poles per Ozaki launch (digit-buffer budget)
   int oz_pair = 0;             // RBA_OZ_2CTA=1: cluster-pair (cta_group::2, M = 256) GEMM
+  int oz_ts = 0;               // RBA_OZ_TS=1: A digits staged in TMEM (tcgen05.cp), B from smem
   unsigned char* oz_buf = nullptr;
   int* oz_exp = nullptr;
   std::vector<std::pair<int64_t, int>> fwd_lv, bwd_lv, fwdb_lv, bwdb_lv, small_lv;
@@ -656,7 +657,8 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
           c->launches += 1;
           rba::launch_oz_schur(c->st, c->oz_tasks + s.off, s.n, c->oz_tiles + s.oz_tile_off, s.schur,
                                s.ntiles, c->F, sub,
-                               c->oz_buf, s.oz_split, c->oz_exp, s.oz_rows, c->oz_pair);
+                               c->oz_buf, s.oz_split, c->oz_exp, s.oz_rows,
+                               c->oz_pair ? 1 : (c->oz_ts ? 2 : 0));
         }
         break;
       }
@@ -1134,6 +1136,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   if (const char* e = getenv("RBA_OZ_MINK")) c->oz_min_k = std::max(16, atoi(e));
   if (const char* e = getenv("RBA_OZ_TRAIL")) c->oz_trail = std::string(e) == "1";
   if (const char* e = getenv("RBA_OZ_2CTA")) c->oz_pair = std::string(e) == "1";
+  if (const char* e = getenv("RBA_OZ_TS")) c->oz_ts = std::string(e) == "1";
   if (const char* e = getenv("RBA_OZ_MINROWS")) c->oz_min_rows = std::max(64, atoi(e));
   int rc;
   if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||

@@ -206,8 +206,19 @@ struct OzSmem {
   unsigned char st[OZ_NLD][OZ_BLK];          // [stage][A_big | B] digit blocks
   uint64_t full[OZ_NLD], empty[OZ_NLD];
   uint64_t tfull, tempty;                    // accumulators: MMA -> epilogue -> MMA
+  uint64_t aslot[8];                         // TS: A digit slot in TMEM free again
   uint32_t tbase;
 };
+// TS variant: the A digit of each (k step, t) is copied once into one of 8
+// TMEM slots of 8 columns (448..511, next to the 7 level accumulators) by
+// tcgen05.cp and the 8 - t MMAs that use it read A from TMEM, so the MMAs
+// read only B (2 KB) from shared memory instead of A + B (6 KB).  A slot is
+// rewritten 8 digits later, after the commit of the MMAs that read it.
+__device__ __forceinline__ void mma_i8_ts(uint32_t dtmem, uint32_t atmem, uint64_t db, int acc) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+               " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n"
+               :: "r"(dtmem), "r"(atmem), "l"(db), "r"(OZ_IDESC), "r"(acc));
+}
 
 __device__ __forceinline__ void oz_item(const OzTask* __restrict__ tasks, int ntasks,
                                         const int2* __restrict__ tiles, int ntiles, int item,
@@ -225,6 +236,7 @@ __device__ __forceinline__ void oz_item(const OzTask* __restrict__ tasks, int nt
   tj = tt.y;
 }
 
+template <bool TS>
 __global__ void __launch_bounds__(192, 1) k_oz_gemm(const OzTask* __restrict__ tasks, int ntasks,
                                                     const int2* __restrict__ tiles, int ntiles,
                                                     FrontsDev F, PoleBatch pb,
@@ -247,6 +259,7 @@ __global__ void __launch_bounds__(192, 1) k_oz_gemm(const OzTask* __restrict__ t
     }
     mbar_init_(&S.tfull, 1);
     mbar_init_(&S.tempty, 128);
+    for (int q = 0; q < 8; ++q) mbar_init_(&S.aslot[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -289,6 +302,28 @@ __global__ void __launch_bounds__(192, 1) k_oz_gemm(const OzTask* __restrict__ t
         mbar_wait_(&S.full[q], (g / OZ_NLD) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         const uint32_t abase = su32(S.st[q]), bbase = abase + OZ_ABYTES;
+        if constexpr (TS) {
+          // digit-major order (integer sums: the order does not change the result)
+#pragma unroll
+          for (int t = 1; t <= OZ_S; ++t) {
+            const int n = g * OZ_S + (t - 1);          // global A digit counter
+            const int sl = n & 7;
+            if (n >= 8) {
+              mbar_wait_(&S.aslot[sl], ((n >> 3) - 1) & 1);
+              asm volatile("tcgen05.fence::after_thread_sync;\n");
+            }
+            const uint32_t ta = tb + 448 + sl * 8;
+            asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;\n"
+                         :: "r"(ta), "l"(umma_desc(abase + (t - 1) * 2 * 128 * 16, 128 * 16, 128)));
+#pragma unroll
+            for (int u = 1; u <= 8 - t; ++u) {
+              const uint64_t db = umma_desc(bbase + (u - 1) * 2 * 64 * 16, 64 * 16, 128);
+              mma_i8_ts(tb + (t + u - 2) * 64, ta, db, (ks > 0 || t > 1) ? 1 : 0);
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+                         :: "r"(su32(&S.aslot[sl])) : "memory");
+          }
+        } else {
 #pragma unroll
         for (int d = 2; d <= 8; ++d)
 #pragma unroll
@@ -299,6 +334,7 @@ __global__ void __launch_bounds__(192, 1) k_oz_gemm(const OzTask* __restrict__ t
             const uint64_t db = umma_desc(bbase + (u - 1) * 2 * 64 * 16, 64 * 16, 128);
             mma_i8(tb + (d - 2) * 64, da, db, (ks > 0 || t > 1) ? 1 : 0);
           }
+        }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
                      :: "r"(su32(&S.empty[q])) : "memory");
       }
@@ -592,7 +628,7 @@ void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int
                      int pair) {
   if (ntasks <= 0 || ntiles <= 0) return;
   k_oz_split<<<dim3(nrowtiles, pb.count), 128, 0, st>>>(tasks, ntasks, F, pb, split,
-                                                        split_pole, expo, exp_pole, pair);
+                                                        split_pole, expo, exp_pole, pair == 1);
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
@@ -600,7 +636,7 @@ void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   const int items = ntiles * pb.count;
-  if (pair) {
+  if (pair == 1) {
     const size_t smem = sizeof(OzSmem2) + 1024;
     static bool attr2 = false;
     if (!attr2) {
@@ -615,11 +651,16 @@ void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int
   const size_t smem = sizeof(OzSmem) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_oz_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_oz_gemm<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_oz_gemm<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_oz_gemm<<<std::min(items, nsm), 192, smem, st>>>(tasks, ntasks, tiles, ntiles, F, pb, split,
-                                                     split_pole, expo, exp_pole);
+  if (pair == 2)
+    k_oz_gemm<true><<<std::min(items, nsm), 192, smem, st>>>(tasks, ntasks, tiles, ntiles, F, pb, split,
+                                                             split_pole, expo, exp_pole);
+  else
+    k_oz_gemm<false><<<std::min(items, nsm), 192, smem, st>>>(tasks, ntasks, tiles, ntiles, F, pb, split,
+                                                              split_pole, expo, exp_pole);
 }
 
 }  // namespace rba

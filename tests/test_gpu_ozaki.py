@@ -87,8 +87,9 @@ def test_ozaki_c1_parity(gpu, ozaki):
     assert ef <= 1e-9 and ej <= 1e-8 and et <= 1e-8
 
 
-def _factor_bytes(monkeypatch, n, pair):
+def _factor_bytes(monkeypatch, n, pair, ts=False):
     monkeypatch.setenv("RBA_OZ_2CTA", "1" if pair else "0")
+    monkeypatch.setenv("RBA_OZ_TS", "1" if ts else "0")
     prob, _ = rb.build_config("C4", n=n)
     approx = rb.config_approximant("C4")
     eng = Engine(prob, None)
@@ -113,5 +114,16 @@ def test_ozaki_cluster_pair_bitwise(gpu, ozaki, monkeypatch):
     for n in (10, 20):
         a = _factor_bytes(monkeypatch, n, False)
         b = _factor_bytes(monkeypatch, n, True)
+        for x, y in zip(a, b):
+            assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
+
+
+def test_ozaki_tmem_a_bitwise(gpu, ozaki, monkeypatch):
+    """The TS GEMM (RBA_OZ_TS=1: A digits copied into TMEM by tcgen05.cp,
+    digit-major MMA order) sums the same exact int32 products: factors
+    bitwise equal to the shared-memory-operand kernel."""
+    for n in (10, 20):
+        a = _factor_bytes(monkeypatch, n, False, False)
+        b = _factor_bytes(monkeypatch, n, False, True)
         for x, y in zip(a, b):
             assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
