@@ -223,6 +223,11 @@ int rba_set_option(rba_ctx* ctx, const char* name, int64_t value);
  * turns them off): out[5] = on (1/0), executed int8 ops and FP64-equivalent
  * flops per pole factorisation, poles per launch, minimum pivots per front. */
 int rba_oz_stats(rba_ctx* ctx, double* out_h);
+/* Cycle counters of the Ozaki GEMM's roles summed over CTAs since the last
+   reset (profiling aid): out_h[10] = MMA-issuer loop, its waits for data, its
+   waits for TMEM, producer waits for a free stage, epilogue waits for the
+   accumulators, TMEM drain, global read-modify-write, k steps, tiles, issuer loop in ns. */
+int rba_oz_prof(rba_ctx* ctx, double* out_h, int reset);
 /* Device time per kernel class (ms, CUDA events around every launch while
  * timing is enabled), out[16]: scatter, extend-add, diag, trsm, gemm (DMMA),
  * solve-fwd, solve-bwd, element/observation, vector/SpMV, M assembly,

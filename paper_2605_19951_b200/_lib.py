@@ -77,6 +77,7 @@ _SIGS = {
     "rba_set_option": (C.c_int, [vp, C.c_char_p, i64]),
     "rba_set_reg_L": (C.c_int, [vp, i64, vp, vp, vp]),
     "rba_oz_stats": (C.c_int, [vp, vp]),
+    "rba_oz_prof": (C.c_int, [vp, vp, C.c_int]),
     "rba_box_generate": (C.c_int, [i32, f64, vp, C.POINTER(vp)]),
     "rba_box_info": (C.c_int, [vp, vp]),
     "rba_box_get": (C.c_int, [vp, C.c_char_p, vp, i64]),

@@ -91,20 +91,23 @@ struct rba_ctx {
   rba::GemmTask* gm_tasks = nullptr;
   // Ozaki-scheme INT8 tensor-core Schur updates (RBA_OZAKI, kernels_ozaki.cu)
   bool ozaki = true;           // RBA_OZAKI=0: DMMA for every Schur update
-  int oz_min_k = 256;          // Schur updates of fronts with at least this many pivots
-  bool oz_trail = false;       // RBA_OZ_TRAIL=1: aggregated panel updates on INT8 too (+2% at
-                               // RBA_PANEL=16, slightly larger backward error): off
-  int oz_min_rows = 512;       // aggregated panel updates with at least this many rows
+  int oz_stages = 4;           // RBA_OZ_STAGES: load-ring depth of the wide GEMM (4 or 5; 5 measured
+                               // the same: the feed is L2-bandwidth, not latency bound)
+  int oz_kmax = 1 << 20;       // RBA_OZ_KMAX: pivots per pass of a Schur update (passes of 1024
+                               // measured 4 % slower: one more epilogue per tile)
+  int oz_min_k = 128;          // Schur updates of fronts with at least this many pivots (RBA_OZ_MINK)
+  bool oz_trail = true;        // RBA_OZ_TRAIL=0: aggregated panel updates stay on the DMMA GEMM
+  int oz_min_rows = 256;       // aggregated panel updates with at least this many rows (RBA_OZ_MINROWS)
   rba::OzTask* oz_tasks = nullptr;
   int2* oz_tiles = nullptr;    // (row tile, column tile) per CTA, L2-friendly order
   int64_t oz_split_max = 0, oz_rows_max = 0;
   double oz_int8_ops = 0, oz_flops = 0;   // per pole factorisation: executed int8 ops,
                                           // FP64-equivalent (4-multiply) flops
   int oz_sub = 1;              // poles per Ozaki launch (digit-buffer budget)
-  int oz_pair = 0;             // RBA_OZ_2CTA=1: cluster-pair (cta_group::2, M = 256) GEMM
-  int oz_ts = 0;               // RBA_OZ_TS=1: A digits staged in TMEM (tcgen05.cp), B from smem
+  int oz_wide = 1;             // RBA_OZ_WIDE=0: one N = 64 MMA per digit pair (28 per k step)
+                               // instead of 10 wide ones (same integer sums, bitwise equal)
   unsigned char* oz_buf = nullptr;
-  int* oz_exp = nullptr;
+  double* oz_exp = nullptr;   // row scales 2^(e_r - 54) of the Ozaki digit blocks
   std::vector<std::pair<int64_t, int>> fwd_lv, bwd_lv, fwdb_lv, bwdb_lv, small_lv;
   std::vector<int> small_mb;   // per level: pivot blocks of the largest warp-per-front front
   // host copies for the pruned forward sweeps of the receiver-Green build
@@ -348,17 +351,6 @@ int build_plans(rba_ctx* c) {
     // blocks in L2
     constexpr int SB = 12;
     int nt = 0;
-    if (c->oz_pair) {
-      // cluster pairs own two row tiles (2 tr2, 2 tr2 + 1) x one column tile
-      const int np = (nrt + 1) / 2;
-      for (int I = 0; I < np; I += SB / 2)
-        for (int J = 0; J < ntc && J <= 2 * (I + SB / 2) - 1; J += SB)
-          for (int j = J; j < std::min(J + SB, ntc); ++j)
-            for (int i = std::max(I, j / 2); i < std::min(I + SB / 2, np); ++i) {
-              ozt.push_back(make_int2(i, j));
-              ++nt;
-            }
-    } else
     for (int I = 0; I < nrt; I += SB)
       for (int J = 0; J < ntc && J <= I + SB - 1; J += SB)
         for (int j = J; j < std::min(J + SB, ntc); ++j)
@@ -368,10 +360,10 @@ int build_plans(rba_ctx* c) {
           }
     o.tiles += nt;
     o.rt += nrt;
-    o.bytes += (int64_t)(c->oz_pair ? (nrt + 1) / 2 * 2 : nrt) * nks * OZ_BLK_BYTES;
+    o.bytes += (int64_t)nrt * nks * OZ_BLK_BYTES;
     o.rows += nf - clo;
     const double w = chi - clo;
-    c->oz_int8_ops += 2.0 * 28 * ((c->oz_pair ? 256.0 : 128.0) * 64 * 32) * nks * nt;
+    c->oz_int8_ops += 2.0 * 28 * (128.0 * 64 * 32) * nks * nt;
     c->oz_flops += 8.0 * (w * (nf - clo) - 0.5 * w * (w - 1)) * (t1 - t0);
   };
   auto oz_end = [&](OzStep& o, int level) {
@@ -468,13 +460,25 @@ int build_plans(rba_ctx* c) {
     // tensor cores (Ozaki scheme), the rest with the DMMA GEMM
     int64_t goff = gm.size();
     int tiles = 0;
-    OzStep osc = oz_begin();
+    // the pivots of a wide front are taken in passes of at most oz_kmax (one
+    // plan step per pass): the digit streams of the ~148 tiles in flight
+    // (12 x 12 super-block: 18 row-tile streams of K / 16 x 28 KB) then stay
+    // L2-resident while the tiles that share them catch up
+    int opass = 1;
+    for (int q = q0; q < q1; ++q) {
+      int s = S.level_fronts[q];
+      int p = S.npiv[s], nf = S.nf[s];
+      if (nf > p && c->ozaki && p >= c->oz_min_k && p <= 16384)
+        opass = std::max(opass, (p + c->oz_kmax - 1) / c->oz_kmax);
+    }
+    std::vector<OzStep> osc(opass);
+    for (auto& o : osc) o = oz_begin();
     for (int q = q0; q < q1; ++q) {
       int s = S.level_fronts[q];
       int p = S.npiv[s], nf = S.nf[s];
       if (nf <= p || p == 0) continue;
       if (c->ozaki && p >= c->oz_min_k && p <= 16384) {
-        oz_add(osc, s, nf, p, nf, 0, p);
+        if (opass == 1) oz_add(osc[0], s, nf, p, nf, 0, p);
         continue;
       }
       int ntr = (nf - p + rba::GT - 1) / rba::GT;
@@ -482,7 +486,22 @@ int build_plans(rba_ctx* c) {
       tiles += ntr * (ntr + 1) / 2;
     }
     if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles, 1});
-    oz_end(osc, L);
+    oz_end(osc[0], L);
+    // tasks of one plan step are contiguous in `oz`, so the passes of a
+    // multi-pass level are built one after the other
+    for (int j = 0; opass > 1 && j < opass; ++j) {
+      OzStep o = oz_begin();
+      for (int q = q0; q < q1; ++q) {
+        int s = S.level_fronts[q];
+        int p = S.npiv[s], nf = S.nf[s];
+        if (nf <= p || !(c->ozaki && p >= c->oz_min_k && p <= 16384)) continue;
+        const int np = (p + c->oz_kmax - 1) / c->oz_kmax;           // this front's passes
+        const int len = ((p + np - 1) / np + 15) / 16 * 16;
+        const int t0 = j * len, t1 = std::min(p, (j + 1) * len);
+        if (t0 < t1) oz_add(o, s, nf, p, nf, t0, t1);
+      }
+      oz_end(o, L);
+    }
     for (size_t q = plan0; q < c->plan.size(); ++q) c->plan[q].level = L;
   }
   int rc;
@@ -658,7 +677,7 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
           rba::launch_oz_schur(c->st, c->oz_tasks + s.off, s.n, c->oz_tiles + s.oz_tile_off, s.schur,
                                s.ntiles, c->F, sub,
                                c->oz_buf, s.oz_split, c->oz_exp, s.oz_rows,
-                               c->oz_pair ? 1 : (c->oz_ts ? 2 : 0));
+                               c->oz_wide ? (c->oz_stages == 5 ? 2 : 1) : 0);
         }
         break;
       }
@@ -1134,9 +1153,10 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   if (const char* e = getenv("RBA_FWD_GEMM")) c->fwd_gemm = atoi(e) ? 1 : 0;
   if (const char* e = getenv("RBA_OZAKI")) c->ozaki = std::string(e) != "0";
   if (const char* e = getenv("RBA_OZ_MINK")) c->oz_min_k = std::max(16, atoi(e));
-  if (const char* e = getenv("RBA_OZ_TRAIL")) c->oz_trail = std::string(e) == "1";
-  if (const char* e = getenv("RBA_OZ_2CTA")) c->oz_pair = std::string(e) == "1";
-  if (const char* e = getenv("RBA_OZ_TS")) c->oz_ts = std::string(e) == "1";
+  if (const char* e = getenv("RBA_OZ_TRAIL")) c->oz_trail = std::string(e) != "0";
+  if (const char* e = getenv("RBA_OZ_KMAX")) c->oz_kmax = std::max(64, atoi(e) / 16 * 16);
+  if (const char* e = getenv("RBA_OZ_WIDE")) c->oz_wide = std::string(e) != "0";
+  if (const char* e = getenv("RBA_OZ_STAGES")) c->oz_stages = atoi(e) == 4 ? 4 : 5;
   if (const char* e = getenv("RBA_OZ_MINROWS")) c->oz_min_rows = std::max(64, atoi(e));
   int rc;
   if ((rc = dalloc(c, c->allocs, &c->err_d, 1, &c->mem_other)) ||
@@ -1921,6 +1941,15 @@ int rba_oz_stats(rba_ctx* c, double* out) {
   out[2] = c->oz_flops;
   out[3] = (double)c->oz_sub;
   out[4] = (double)c->oz_min_k;
+  return RBA_OK;
+}
+
+int rba_oz_prof(rba_ctx* c, double* out, int reset) {
+  if (!c || !out) return fail(RBA_ERR_INVALID, "null argument");
+  CK(cudaStreamSynchronize(c->st));
+  unsigned long long v[10];
+  rba::oz_prof_read(v, reset != 0);
+  for (int i = 0; i < 10; ++i) out[i] = (double)v[i];
   return RBA_OK;
 }
 

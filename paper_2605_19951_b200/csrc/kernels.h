@@ -48,10 +48,11 @@ void launch_gemm5(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
 void launch_gemm6(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
                   const FrontsDev& F, const PoleBatch& pb, const cplx* zeros, int variant);
 // Schur update of large fronts on the INT8 tensor cores (Ozaki scheme)
+void oz_prof_read(unsigned long long* out, bool reset);
 void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int2* tiles,
                      int nrowtiles, int ntiles,
                      const FrontsDev& F, const PoleBatch& pb, unsigned char* split,
-                     int64_t split_pole, int* expo, int64_t exp_pole, int pair);
+                     int64_t split_pole, double* scl, int64_t exp_pole, int wide);
 void launch_trsm3(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
                   const PoleBatch& pb, int variant);
 

@@ -372,6 +372,15 @@ class Engine:
                 "flops_per_pole": float(out[2]), "poles_per_launch": int(out[3]),
                 "min_pivots": int(out[4])}
 
+    def oz_prof(self, reset: bool = True) -> dict:
+        """Cycle counters of the Ozaki GEMM roles, summed over CTAs since the
+        last reset (profiling aid, rba_oz_prof)."""
+        out = np.zeros(10)
+        check(self.lib.rba_oz_prof(self.ctx, ptr(out), 1 if reset else 0))
+        keys = ("mma_loop", "mma_wait_data", "mma_wait_tmem", "producer_wait_stage",
+                "epi_wait_acc", "epi_drain", "epi_rmw", "ksteps", "tiles", "mma_loop_ns")
+        return dict(zip(keys, out.tolist()))
+
     def set_timing(self, mode):
         """True/1: record device time per kernel class; False/0: stop; 2: reset."""
         check(self.lib.rba_set_timing(self.ctx, int(mode)))

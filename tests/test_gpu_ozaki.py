@@ -87,9 +87,8 @@ def test_ozaki_c1_parity(gpu, ozaki):
     assert ef <= 1e-9 and ej <= 1e-8 and et <= 1e-8
 
 
-def _factor_bytes(monkeypatch, n, pair, ts=False):
-    monkeypatch.setenv("RBA_OZ_2CTA", "1" if pair else "0")
-    monkeypatch.setenv("RBA_OZ_TS", "1" if ts else "0")
+def _factor_bytes(monkeypatch, n, wide):
+    monkeypatch.setenv("RBA_OZ_WIDE", "1" if wide else "0")
     prob, _ = rb.build_config("C4", n=n)
     approx = rb.config_approximant("C4")
     eng = Engine(prob, None)
@@ -107,23 +106,14 @@ def _factor_bytes(monkeypatch, n, pair, ts=False):
     return out
 
 
-def test_ozaki_cluster_pair_bitwise(gpu, ozaki, monkeypatch):
-    """The cta_group::2 GEMM (RBA_OZ_2CTA=1) accumulates the same digit
-    products in the same order as the one-SM kernel: factors bitwise equal
-    (odd and even row-tile counts, fronts wider than one 12-tile super-block)."""
+def test_ozaki_wide_mma_bitwise(gpu, ozaki, monkeypatch):
+    """The default GEMM issues each A digit against runs of up to 4 consecutive
+    B digits as ONE MMA of N = 64..256 (10 MMAs per k step); RBA_OZ_WIDE=0
+    issues the 28 digit pairs one by one (N = 64).  Same exact int32 sums:
+    factors bitwise equal (odd and even row-tile counts, fronts wider than
+    one 12-tile super-block)."""
     for n in (10, 20):
         a = _factor_bytes(monkeypatch, n, False)
         b = _factor_bytes(monkeypatch, n, True)
-        for x, y in zip(a, b):
-            assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
-
-
-def test_ozaki_tmem_a_bitwise(gpu, ozaki, monkeypatch):
-    """The TS GEMM (RBA_OZ_TS=1: A digits copied into TMEM by tcgen05.cp,
-    digit-major MMA order) sums the same exact int32 products: factors
-    bitwise equal to the shared-memory-operand kernel."""
-    for n in (10, 20):
-        a = _factor_bytes(monkeypatch, n, False, False)
-        b = _factor_bytes(monkeypatch, n, False, True)
         for x, y in zip(a, b):
             assert np.array_equal(x.view(np.uint64), y.view(np.uint64))

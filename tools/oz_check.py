@@ -20,6 +20,15 @@ for _ in range(3):
     e0.record(); eng.factor(); e1.record(); torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
 eng.set_timing(2); eng.set_timing(1); eng.factor(); cls = eng.timings(); lev = eng.timings_detail(); eng.set_timing(0)
+eng.oz_prof(True); eng.factor(); pr = eng.oz_prof(True)
+if pr["mma_loop"] > 0:
+    print("oz_prof (fractions of the MMA-issuer loop):",
+          {k: round(v / pr["mma_loop"], 3) for k, v in pr.items() if k not in ("ksteps", "tiles", "mma_loop_ns")},
+          "SM MHz", round(1e3 * pr["mma_loop"] / max(pr["mma_loop_ns"], 1)),
+          "clk per k step", round(pr["mma_loop"] / max(pr["ksteps"], 1), 1),
+          "k steps per tile", round(pr["ksteps"] / max(pr["tiles"], 1), 1),
+          "clk per tile: drain", round(pr["epi_drain"] / max(pr["tiles"], 1)),
+          "rmw", round(pr["epi_rmw"] / max(pr["tiles"], 1)))
 print("factor_by_level", [round(x, 1) for x in lev["factor_by_level"][:15]])
 print("gemm_by_level", [round(x, 1) for x in lev["gemm_by_level"][:15]])
 print("classes", {k: round(v, 1) for k, v in cls.items()})
