@@ -29,16 +29,14 @@ def _bwd(A, x, b):
     return float(np.linalg.norm(A @ x - b) / (nA * np.linalg.norm(x) + np.linalg.norm(b)))
 
 
-def test_ozaki_fronts_match_emulation(gpu, ozaki):
-    prob, _ = rb.build_config("C1", n=10)
-    approx = rb.config_approximant("C1")
-    model = prob.true_model()
+def _front_errors(prob, approx, model):
     cache = rb.ShiftedFactorCache()
     rb.factorize_all_poles(prob, model, approx, cache)
     eng = cache.engine
     S = mf.analyze(prob.K, prob.dof_coords, 64)
     tot = int(S["panel_off"][-1])
     buf = np.empty(tot, dtype=np.complex128)
+    out = []
     for pole in (0, 7):
         _lib.check(eng.lib.rba_get_factor(eng.ctx, pole, ptr(buf.view(np.float64)), tot))
         A = (prob.K.astype(complex) - approx.poles[pole] * orc.assemble_M(prob, model.m)).tocsr()
@@ -50,8 +48,30 @@ def test_ozaki_fronts_match_emulation(gpu, ozaki):
                                         .reshape(p, nf).T, p)
             mask = np.tril(np.ones((nf, p), bool))
             worst = max(worst, np.abs(Ld[mask] - Lh[mask]).max() / max(np.abs(Lh[mask]).max(), 1e-300))
-        print(f"Ozaki fronts pole {pole}: worst front error {worst:.2e}")
-        assert worst <= 1e-10
+        out.append(worst)
+    eng.close()
+    return out
+
+
+def test_ozaki_fronts_match_emulation(gpu, monkeypatch):
+    """Front by front against the host emulation at the C1-shape true model
+    (1e-8 S/m air: the entries of the ill-conditioned air fronts differ at the
+    1e-10 level between ANY two FP64 orderings).  The INT8 path (Schur and
+    aggregated panel updates, every front: RBA_OZ_MINK=16) must stay at the
+    level of the all-DMMA factor of the same matrices."""
+    prob, _ = rb.build_config("C1", n=10)
+    approx = rb.config_approximant("C1")
+    model = prob.true_model()
+    monkeypatch.setenv("RBA_OZAKI", "0")
+    dmma = _front_errors(prob, approx, model)
+    monkeypatch.setenv("RBA_OZAKI", "1")
+    monkeypatch.setenv("RBA_OZ_MINK", "16")
+    monkeypatch.setenv("RBA_OZ_MINROWS", "64")
+    oz = _front_errors(prob, approx, model)
+    for pole, a, b in zip((0, 7), dmma, oz):
+        print(f"fronts pole {pole}: worst front error DMMA {a:.2e}  Ozaki {b:.2e}")
+        assert a <= 1e-10
+        assert b <= max(1e-10, 3.0 * a)
 
 
 def test_ozaki_backward_error_c4_shape(gpu, ozaki):
