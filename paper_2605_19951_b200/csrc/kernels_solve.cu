@@ -460,6 +460,268 @@ __global__ void __launch_bounds__(32 * NW) k_bwd(const SolveTask* __restrict__ t
 }
 
 // ---------------------------------------------------------------------------
+// 4 right-hand sides: the row reduction sum_rho L'[rho, c] x_rho of the
+// backward sweep on the FP64 tensor cores (mma.sync m8n8k4).  A = 8 columns x
+// 4 rows of L' (one 16-byte load per lane: lane = (column lane / 4, row
+// lane % 4)), B = the 4 rows x [Re x (4 RHS) | Im x (4 RHS)], two MMAs per
+// 4 rows (Re L' with (Re x | Im x), Im L' with (-Im x | Re x)); the 8 x 8
+// accumulator holds [Re | Im] of the 8 columns x 4 RHS sums, so there is no
+// shuffle reduction, one x load per lane per 4 rows instead of 4 per row, and
+// 2 accumulator registers instead of 32: the sweep stays on the HBM stream.
+// ---------------------------------------------------------------------------
+constexpr int BCH = 512;   // border rows gathered per shared-memory chunk (k_bwd_mma4)
+struct BwdFrag {
+  double c0 = 0.0, c1 = 0.0;
+  __device__ __forceinline__ void mac(cplx l, cplx xv, bool hi) {
+    dmma_f64(c0, c1, l.x, hi ? xv.y : xv.x);
+    dmma_f64(c0, c1, l.y, hi ? xv.x : -xv.y);
+  }
+};
+
+// Backward task (front s, pivot column block cb) for NR = 4: 8 warps x 8 columns.
+__global__ void __launch_bounds__(256, 2) k_bwd_mma4(const SolveTask* __restrict__ tasks, int nslots,
+                                                     FrontsDev F, SolveBatchDev sb, int* ticket,
+                                                     SweepDeps dep) {
+  constexpr int NR = 4;
+  __shared__ int s_t;
+  extern __shared__ cplx dsm[];
+  cplx(*red)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm);
+  cplx(*tv)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + PB * NR);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_t = atomicAdd(ticket, 1);
+  __syncthreads();
+  const int t = s_t;
+  const int slot = t % nslots;
+  const int epoch = sb.epoch[slot];
+  const SolveTask tk = tasks[t / nslots];
+  const int s = tk.s, cb = tk.blk;
+  const int p = F.npiv[s], nf = F.nf[s], first = F.first[s];
+  const int npb = (p + PB - 1) / PB;
+  const cplx* panel = sb.factor[slot] + F.panel_off[s];
+  cplx* x = sb.x[slot];
+  int* flags = sb.flags[slot] + F.blk_off[s];
+  const int c0 = cb * PB, ncol = min(PB, p - c0);
+  const int* rows = F.rows + F.rows_off[s];
+  cplx* Xs = dsm + 2 * PB * NR;       // [PB][PB+1]: Xs[i][c] = panel(row c0+c, col c0+i)
+  for (int e = tid; e < ncol * ncol; e += blockDim.x) {
+    const int i = e / ncol, c = e - i * ncol;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(Xs + i * (PB + 1) + c);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(sa),
+                 "l"(panel + (int64_t)(c0 + i) * nf + c0 + c) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  if (dep.fused && nf > p) {
+    const int par = dep.parent[s];
+    const int need = (F.npiv[par] + PB - 1) / PB;
+    if (tid == 0) spin_wait_geq(sb.done[slot] + par, epoch * need);
+    __syncthreads();
+  }
+  const int kq = lane & 3, cq = lane >> 2;
+  const int col = warp * 8 + cq;                 // this lane's column of the block
+  const bool con = col < ncol;
+  const cplx* colp = panel + (int64_t)(c0 + (con ? col : 0)) * nf;
+  const int rhs = cq & 3;
+  const bool hi = cq >= 4;
+  BwdFrag acc, acc2;
+  // border rows (pivots of ancestors, final before this launch): the x rows
+  // are gathered once per CTA into shared memory in chunks of BCH rows, then
+  // every warp streams its 8 columns of L' against them
+  cplx(*xs)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + 2 * PB * NR + PB * (PB + 1));
+  const bool won = warp * 8 < ncol;
+  for (int ch0 = p; ch0 < nf; ch0 += BCH) {
+    const int nch = min(BCH, nf - ch0);
+    // first L' loads of the chunk go out before the gather and the barrier
+    cplx lv[8];
+#pragma unroll
+    for (int h = 0; h < 8; ++h) {
+      const int rho = ch0 + 4 * h + kq;
+      lv[h] = (won && con && rho < nf) ? __ldg(colp + rho) : cmk(0.0, 0.0);
+    }
+    __syncthreads();                               // previous chunk consumed
+    for (int e = tid; e < nch * NR; e += blockDim.x) {
+      const int rr = e >> 2, r = e & 3;
+      const int g = __ldg(rows + ch0 + rr);
+      xs[rr][r] = __ldg(x + (int64_t)g * NR + r);
+    }
+    for (int e = nch * NR + tid; e < ((nch + 3) & ~3) * NR; e += blockDim.x) xs[e >> 2][e & 3] = cmk(0.0, 0.0);
+    __syncthreads();
+    if (won) {
+      for (int g0 = 0; g0 < nch; g0 += 32) {
+        cplx ln[8];
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {              // next 32 rows in flight
+          const int rho = ch0 + g0 + 32 + 4 * h + kq;
+          ln[h] = (con && g0 + 32 < nch && rho < nf) ? __ldg(colp + rho) : cmk(0.0, 0.0);
+        }
+#pragma unroll
+        for (int h = 0; h < 8; ++h) {
+          const int rr = g0 + 4 * h + kq;
+          const cplx xv = rr < ((nch + 3) & ~3) ? xs[rr][rhs] : cmk(0.0, 0.0);
+          if (h & 1) acc2.mac(lv[h], xv, hi); else acc.mac(lv[h], xv, hi);
+        }
+#pragma unroll
+        for (int h = 0; h < 8; ++h) lv[h] = ln[h];
+      }
+    }
+  }
+  if (won) {
+    // later pivot blocks of this front (earlier tickets of this launch): L'
+    // is loaded before the wait, x with L2 loads after it
+    for (int rb = npb - 1; rb > cb; --rb) {
+      const int q0 = rb * PB, q1 = min(q0 + PB, p);
+      cplx lv[16];
+#pragma unroll
+      for (int h = 0; h < 16; ++h) {
+        const int rho = q0 + 4 * h + kq;
+        lv[h] = (con && rho < q1) ? __ldg(colp + rho) : cmk(0.0, 0.0);
+      }
+      if (lane == 0) spin_wait_geq(flags + rb, epoch);
+      __syncwarp();
+      cplx xv[16];
+#pragma unroll
+      for (int h = 0; h < 16; ++h) {
+        const int rho = q0 + 4 * h + kq;
+        xv[h] = rho < q1 ? ldcg_c(x + (int64_t)(first + rho) * NR + rhs) : cmk(0.0, 0.0);
+      }
+#pragma unroll
+      for (int h = 0; h < 16; ++h) { if (h & 1) acc2.mac(lv[h], xv[h], hi); else acc.mac(lv[h], xv[h], hi); }
+    }
+    // accumulator (column cq, n = 2 kq, 2 kq + 1): n < 4 real part of RHS n, else imaginary of n - 4
+    if (con) {
+      double* rd = reinterpret_cast<double*>(&red[col][0]);
+      const int n0 = 2 * kq;
+      rd[2 * (n0 & 3) + (n0 >> 2)] = acc.c0 + acc2.c0;
+      rd[2 * ((n0 + 1) & 3) + ((n0 + 1) >> 2)] = acc.c1 + acc2.c1;
+    }
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  if (tid < ncol) {
+    const cplx sc = Xs[tid * (PB + 1) + tid];   // s_c = sqrt(d_c)
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      const cplx y = x[(int64_t)(first + c0 + tid) * NR + r];
+      tv[tid][r] = cdiv(csub(y, red[tid][r]), sc);
+    }
+  }
+  __syncthreads();
+  // x_c = t_c + sum_{i>c} X[i][c] t_i ; 4 threads per column, shuffle-reduced
+  {
+    const int c = tid >> 2, k = tid & 3;
+    cplx xv[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) xv[r] = cmk(0.0, 0.0);
+    if (c < ncol) {
+#pragma unroll 4
+      for (int i = c + 1 + k; i < ncol; i += 4) {
+        const cplx w = Xs[i * (PB + 1) + c];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) xv[r] = cfma(w, tv[i][r], xv[r]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+      double a = xv[r].x, b = xv[r].y;
+#pragma unroll
+      for (int o = 1; o < 4; o <<= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, o);
+        b += __shfl_xor_sync(0xffffffffu, b, o);
+      }
+      xv[r] = cmk(a, b);
+    }
+    if (c < ncol && k == 0) {
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        x[(int64_t)(first + c0 + c) * NR + r] = cadd(tv[c][r], xv[r]);
+      __threadfence();
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    st_release(flags + cb, epoch);
+    if (dep.fused) atomicAdd(sb.done[slot] + s, 1);
+  }
+}
+
+// Small fronts (npiv <= 64), NR = 4: one warp per (front, pole), up to 8
+// column groups of 8 with one accumulator fragment each.
+__global__ void __launch_bounds__(256) k_bwd_small_mma4(const int32_t* __restrict__ fronts, int nfr,
+                                                        int nslots, FrontsDev F, SolveBatchDev sb) {
+  constexpr int NR = 4;
+  extern __shared__ cplx dsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int item = blockIdx.x * 8 + warp;
+  if (item >= nfr * nslots) return;
+  const int slot = item % nslots;
+  const int s = fronts[item / nslots];
+  cplx(*tv)[NR] = reinterpret_cast<cplx(*)[NR]>(dsm + warp * PB * NR);
+  const int p = F.npiv[s], nf = F.nf[s], first = F.first[s];
+  const cplx* panel = sb.factor[slot] + F.panel_off[s];
+  cplx* x = sb.x[slot];
+  const int* rows = F.rows + F.rows_off[s];
+  const int kq = lane & 3, cq = lane >> 2;
+  const int rhs = cq & 3;
+  const bool hi = cq >= 4;
+  const int ncg = (p + 7) >> 3;
+  BwdFrag acc[8];
+  const cplx* colp = panel + (int64_t)cq * nf;      // column cq of group 0
+#pragma unroll 2
+  for (int r0 = p; r0 < nf; r0 += 4) {
+    const int rho = r0 + kq;
+    const bool ron = rho < nf;
+    const int g = ron ? __ldg(rows + rho) : 0;
+    cplx l[8];
+#pragma unroll
+    for (int cg = 0; cg < 8; ++cg)
+      l[cg] = (cg < ncg && ron && cg * 8 + cq < p) ? __ldg(colp + (int64_t)cg * 8 * nf + rho) : cmk(0.0, 0.0);
+    const cplx xv = ron ? x[(int64_t)g * NR + rhs] : cmk(0.0, 0.0);
+#pragma unroll
+    for (int cg = 0; cg < 8; ++cg)
+      if (cg < ncg) acc[cg].mac(l[cg], xv, hi);
+  }
+  // tv[c] = sum (before the diagonal solve)
+#pragma unroll
+  for (int cg = 0; cg < 8; ++cg) {
+    const int col = cg * 8 + cq;
+    if (cg < ncg && col < p) {
+      double* rd = reinterpret_cast<double*>(&tv[col][0]);
+      const int n0 = 2 * kq;
+      rd[2 * (n0 & 3) + (n0 >> 2)] = acc[cg].c0;
+      rd[2 * ((n0 + 1) & 3) + ((n0 + 1) >> 2)] = acc[cg].c1;
+    }
+  }
+  __syncwarp();
+  // t = (y - sum) / s, then x = X^T t  (X[i][c] at (row c, col i), i > c)
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+    if (c < p) {
+      const cplx sc = panel[(int64_t)c * nf + c];   // s_c = sqrt(d_c)
+#pragma unroll
+      for (int r = 0; r < NR; ++r)
+        tv[c][r] = cdiv(csub(x[(int64_t)(first + c) * NR + r], tv[c][r]), sc);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int c = lane + 32 * h;
+    if (c < p) {
+      cplx xv[NR];
+#pragma unroll
+      for (int r = 0; r < NR; ++r) xv[r] = tv[c][r];
+      for (int i = c + 1; i < p; ++i) {
+        const cplx w = __ldg(panel + (int64_t)i * nf + c);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) xv[r] = cfma(w, tv[i][r], xv[r]);
+      }
+#pragma unroll
+      for (int r = 0; r < NR; ++r) x[(int64_t)(first + c) * NR + r] = xv[r];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Small fronts (one pivot block, npiv <= 64): one WARP per (front, pole) does
 // the whole front -- no tickets, flags or block barriers.  The bottom levels
 // of the tree (C4: levels 0-4, ~20k fronts per pole) are all of this kind.
@@ -650,6 +912,22 @@ __global__ void __launch_bounds__(256) k_bwd_small(const int32_t* __restrict__ f
   }
 }
 
+// RBA_BWD_MMA: 0 = scalar (DFMA) backward kernels for 4 right-hand sides too,
+// 1 (default) = tensor-core kernel for the small fronts (C4 levels 0-4:
+// 8.5 -> 6.6 ms per 16-pole sweep), 2 = also for the large fronts (measured
+// slower, 27 -> 32 ms: the 8 x 64 B segments of an A fragment load keep fewer
+// bytes in flight per register than the scalar kernel's 512 B row segments;
+// it needs a TMA-fed shared-memory ring to pay)
+static int bwd_mma_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("RBA_BWD_MMA");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+static bool bwd_mma_on() { return bwd_mma_mode() >= 1; }
+
 template <int NR>
 static void small_nr(cudaStream_t st, bool forward, const int32_t* fronts, int nfr, int nslots,
                      const FrontsDev& F, const SolveBatchDev& sb, int mb) {
@@ -673,6 +951,8 @@ static void small_nr(cudaStream_t st, bool forward, const int32_t* fronts, int n
       }
       k_fwd_small<NR, 2><<<grid, 256, smem, st>>>(fronts, nfr, nslots, F, sb);
     }
+  } else if (NR == 4 && mb <= 1 && bwd_mma_on()) {   // one pivot block per front
+    k_bwd_small_mma4<<<grid, 256, 8 * PB * NR * sizeof(cplx), st>>>(fronts, nfr, nslots, F, sb);
   } else {
     const size_t smem = (16 * 32 * NR + 8 * PB * NR) * sizeof(cplx);
     static bool attr = false;
@@ -739,6 +1019,16 @@ template <int NR>
 static void bwd_nr(cudaStream_t st, const SolveTask* tasks, int ntasks, int nslots,
                    const FrontsDev& F, const SolveBatchDev& sb, int* ticket, int epoch,
                    const SweepDeps& dep) {
+  if (NR == 4 && bwd_mma_mode() >= 2) {
+    const size_t smem = (2 * PB * NR + PB * (PB + 1) + BCH * NR) * sizeof(cplx);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_bwd_mma4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    k_bwd_mma4<<<ntasks * nslots, 256, smem, st>>>(tasks, nslots, F, sb, ticket, dep);
+    return;
+  }
   if (g_bwd_nw < 0) {
     const char* e = getenv("RBA_BWD_NW");
     g_bwd_nw = (e && atoi(e) == 32) ? 32 : 16;

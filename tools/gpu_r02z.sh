@@ -1,6 +1,5 @@
 #!/bin/bash
 cd "$GRAFT_REPO_ROOT" || exit 1
 mkdir -p gpurun_out
-run() { tag=$1; shift; env "$@" RBA_OZ_STAGES=4 timeout 600 python tools/oz_check.py > gpurun_out/r02z_oz_$tag.log 2>&1; echo "== $tag: $@"; grep -h "oz_prof\|factor 16\|classes" gpurun_out/r02z_oz_$tag.log; }
-run a RBA_OZ_TRAIL=1 RBA_PANEL=4 RBA_OZ_MINROWS=256 RBA_OZ_MINK=128
-run g RBA_OZ_TRAIL=1 RBA_PANEL=4 RBA_OZ_MINROWS=512 RBA_OZ_MINK=256
+timeout 900 python -m pytest -x -q -m gpu tests/test_gpu_parity.py tests/test_gpu_verify.py 2>&1 | tail -4
+for v in 0 1; do echo "BWD_MMA=$v"; RBA_BWD_MMA=$v timeout 300 python tools/solve_check.py 3 2>&1 | tail -4; done
