@@ -124,6 +124,24 @@ def measured_traffic():
         return {}
 
 
+def oz_roles(pr):
+    """The Ozaki GEMM's own cycle counters over the timed region
+    (rba_oz_prof): where its MMA-issuing thread spent its time, the SM clock it
+    ran at (the INT8 phases run under the power cap) and the tensor-pipe
+    occupancy they imply (28 MMAs of 128x64x32 = 896 clk per k step at peak)."""
+    loop = pr.get("mma_loop", 0.0)
+    if loop <= 0:
+        return {}
+    per_k = loop / max(pr["ksteps"], 1.0)
+    return {"sm_mhz": round(1e3 * loop / max(pr["mma_loop_ns"], 1.0)),
+            "clk_per_kstep": round(per_k, 1),
+            "tensor_busy_frac": round(896.0 / per_k, 3),
+            "wait_data_frac": round(pr["mma_wait_data"] / loop, 3),
+            "wait_tmem_frac": round(pr["mma_wait_tmem"] / loop, 3),
+            "ksteps_per_tile": round(pr["ksteps"] / max(pr["tiles"], 1.0), 1),
+            "epilogue_clk_per_tile": round((pr["epi_drain"] + pr["epi_rmw"]) / max(pr["tiles"], 1.0))}
+
+
 def measured_peaks():
     peaks = {}
     try:
@@ -201,6 +219,7 @@ def run_ours(args, world, rank):
     nu_snap = nu
     # ---- timed region: K GN iterations, inputs resident in HBM ------------
     eng.set_timing(2)                     # reset the launch counter; events stay off
+    eng.oz_prof(True)                     # reset the Ozaki GEMM's role counters
     clocks = Clocks()
     barrier()
     torch.cuda.synchronize()
@@ -219,6 +238,7 @@ def run_ours(args, world, rank):
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
     launches = int(eng.timings()["launches"])
+    oz_prof = eng.oz_prof(True)           # cycle counters of the timed region (not a profiler)
     n_fact = cache.counters.factorizations - fac0
     n_solve = cache.counters.solves - sol0
     if world > 1:
@@ -373,7 +393,7 @@ def run_ours(args, world, rank):
         "counts": {"factorizations": n_fact, "solves": n_solve},
         "roofline": roof,
         "rooflines": rooflines,
-        "ozaki": oz,
+        "ozaki": dict(oz, timed_region=oz_roles(oz_prof)),
         "clocks": clk,
         "e2e": {"value": e2e_ms / 1e3, "unit": "s/GN-iteration",
                 "h2d_bytes_per_step": bytes_in, "d2h_bytes_per_step": bytes_out},
