@@ -56,6 +56,7 @@ struct Step {
   int64_t oz_tile_off = 0;  // ST_OZ: offset of the step's tile list
 };
 constexpr int64_t OZ_BLK_BYTES = 7 * 2 * 192 * 16;  // kernels_ozaki.cu OZ_BLK (A_big + B)
+constexpr int64_t OZ_BLK2_BYTES = 7 * 2 * 128 * 16 + 2 * 12288;  // OZ_BLK2 (A_big + two B arrangements)
 
 int nr_pad(int s) { return s <= 1 ? 1 : s <= 2 ? 2 : s <= 4 ? 4 : 8; }
 }  // namespace
@@ -104,6 +105,7 @@ struct rba_ctx {
   double oz_int8_ops = 0, oz_flops = 0;   // per pole factorisation: executed int8 ops,
                                           // FP64-equivalent (4-multiply) flops
   int oz_sub = 1;              // poles per Ozaki launch (digit-buffer budget)
+  int oz_pair = 0;             // RBA_OZ_2CTA=1: cluster-pair GEMM (cta_group::2, M = 256)
   int oz_wide = 1;             // RBA_OZ_WIDE=0: one N = 64 MMA per digit pair (28 per k step)
                                // instead of 10 wide ones (same integer sums, bitwise equal)
   unsigned char* oz_buf = nullptr;
@@ -351,6 +353,17 @@ int build_plans(rba_ctx* c) {
     // blocks in L2
     constexpr int SB = 12;
     int nt = 0;
+    if (c->oz_pair) {
+      // cluster pairs own two row tiles (2 i, 2 i + 1) x one column tile
+      const int np = (nrt + 1) / 2;
+      for (int I = 0; I < np; I += SB / 2)
+        for (int J = 0; J < ntc && J <= 2 * (I + SB / 2) - 1; J += SB)
+          for (int j = J; j < std::min(J + SB, ntc); ++j)
+            for (int i = std::max(I, j / 2); i < std::min(I + SB / 2, np); ++i) {
+              ozt.push_back(make_int2(i, j));
+              ++nt;
+            }
+    } else
     for (int I = 0; I < nrt; I += SB)
       for (int J = 0; J < ntc && J <= I + SB - 1; J += SB)
         for (int j = J; j < std::min(J + SB, ntc); ++j)
@@ -360,10 +373,10 @@ int build_plans(rba_ctx* c) {
           }
     o.tiles += nt;
     o.rt += nrt;
-    o.bytes += (int64_t)nrt * nks * OZ_BLK_BYTES;
+    o.bytes += c->oz_pair ? (int64_t)((nrt + 1) / 2 * 2) * nks * OZ_BLK2_BYTES : (int64_t)nrt * nks * OZ_BLK_BYTES;
     o.rows += nf - clo;
     const double w = chi - clo;
-    c->oz_int8_ops += 2.0 * 28 * (128.0 * 64 * 32) * nks * nt;
+    c->oz_int8_ops += 2.0 * 28 * ((c->oz_pair ? 256.0 : 128.0) * 64 * 32) * nks * nt;
     c->oz_flops += 8.0 * (w * (nf - clo) - 0.5 * w * (w - 1)) * (t1 - t0);
   };
   auto oz_end = [&](OzStep& o, int level) {
@@ -677,7 +690,7 @@ int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
           rba::launch_oz_schur(c->st, c->oz_tasks + s.off, s.n, c->oz_tiles + s.oz_tile_off, s.schur,
                                s.ntiles, c->F, sub,
                                c->oz_buf, s.oz_split, c->oz_exp, s.oz_rows,
-                               c->oz_wide ? (c->oz_stages == 5 ? 2 : 1) : 0);
+                               c->oz_pair ? 3 : (c->oz_wide ? (c->oz_stages == 5 ? 2 : 1) : 0));
         }
         break;
       }
@@ -1155,6 +1168,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   if (const char* e = getenv("RBA_OZ_MINK")) c->oz_min_k = std::max(16, atoi(e));
   if (const char* e = getenv("RBA_OZ_TRAIL")) c->oz_trail = std::string(e) != "0";
   if (const char* e = getenv("RBA_OZ_KMAX")) c->oz_kmax = std::max(64, atoi(e) / 16 * 16);
+  if (const char* e = getenv("RBA_OZ_2CTA")) c->oz_pair = std::string(e) == "1";
   if (const char* e = getenv("RBA_OZ_WIDE")) c->oz_wide = std::string(e) != "0";
   if (const char* e = getenv("RBA_OZ_STAGES")) c->oz_stages = atoi(e) == 4 ? 4 : 5;
   if (const char* e = getenv("RBA_OZ_MINROWS")) c->oz_min_rows = std::max(64, atoi(e));

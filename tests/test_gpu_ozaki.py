@@ -107,8 +107,9 @@ def test_ozaki_c1_parity(gpu, ozaki):
     assert ef <= 1e-9 and ej <= 1e-8 and et <= 1e-8
 
 
-def _factor_bytes(monkeypatch, n, wide):
+def _factor_bytes(monkeypatch, n, wide, pair=False):
     monkeypatch.setenv("RBA_OZ_WIDE", "1" if wide else "0")
+    monkeypatch.setenv("RBA_OZ_2CTA", "1" if pair else "0")
     prob, _ = rb.build_config("C4", n=n)
     approx = rb.config_approximant("C4")
     eng = Engine(prob, None)
@@ -135,5 +136,17 @@ def test_ozaki_wide_mma_bitwise(gpu, ozaki, monkeypatch):
     for n in (10, 20):
         a = _factor_bytes(monkeypatch, n, False)
         b = _factor_bytes(monkeypatch, n, True)
+        for x, y in zip(a, b):
+            assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
+
+
+def test_ozaki_cluster_pair_bitwise(gpu, ozaki, monkeypatch):
+    """The cluster-pair GEMM (RBA_OZ_2CTA=1: tcgen05.mma.cta_group::2, M = 256,
+    each CTA streams its half of every MMA's B rows) sums the same exact int32
+    products: factors bitwise equal to the one-SM kernel (odd and even
+    row-tile counts, fronts wider than one super-block)."""
+    for n in (10, 20):
+        a = _factor_bytes(monkeypatch, n, True, False)
+        b = _factor_bytes(monkeypatch, n, True, True)
         for x, y in zip(a, b):
             assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
