@@ -344,15 +344,22 @@ def run_ours(args, world, rank):
     rooflines = {}
     if oz["on"] and cls.get("ozaki", 0) > 0:
         try:
-            int8_peak = json.load(open(os.path.join(ROOT, "profiles", "int8_peak_r02.json")))["peak_tops"]
-            int8_src = "measured tcgen05 kind::i8 microbenchmark (profiles/int8_peak_r02.json)"
+            pk = json.load(open(os.path.join(ROOT, "profiles", "int8_peak_r02.json")))
+            # a kernel timed inside a long step: the SUSTAINED peak (same MMA loop run
+            # for seconds with random operand bytes: the board power cap holds the SMs
+            # at ~1.55 GHz); the burst figure is reported beside it
+            int8_peak = pk.get("sustained_tops", pk["peak_tops"])
+            int8_burst = pk["peak_tops"]
+            int8_src = ("measured tcgen05 kind::i8 microbenchmark, sustained (power-capped) rate "
+                        "(profiles/int8_peak_r02.json; burst %.0f TOPS)" % int8_burst)
         except OSError:
-            int8_peak = 2.0 * peaks.get("bf16_tflops", 2250.0)
+            int8_peak = int8_burst = 2.0 * peaks.get("bf16_tflops", 2250.0)
             int8_src = "2 x MEASURED_PEAKS.json bf16_tflops (dense INT8 = 2 x BF16 on sm_100)"
         ach = oz["int8_ops_per_pole"] * n_local_fact / (cls["ozaki"] * 1e-3) / 1e12
         rooflines["ozaki_int8_schur"] = {
             "bound": "tensor", "achieved": ach, "peak": int8_peak, "unit": "TOPS (int8)",
-            "frac": ach / int8_peak, "ms_per_step": cls["ozaki"],
+            "frac": ach / int8_peak, "peak_burst": int8_burst, "frac_of_burst": ach / int8_burst,
+            "ms_per_step": cls["ozaki"],
             "fp64_equiv_tflops": oz["flops_per_pole"] * n_local_fact / (cls["ozaki"] * 1e-3) / 1e12,
             "peak_source": int8_src,
             "per_unit": "2*28*(128*64*32)*ksteps*tiles int8 ops per pole (7 digits, 28 pairs, "

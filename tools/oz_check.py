@@ -28,7 +28,8 @@ if pr["mma_loop"] > 0:
           "clk per k step", round(pr["mma_loop"] / max(pr["ksteps"], 1), 1),
           "k steps per tile", round(pr["ksteps"] / max(pr["tiles"], 1), 1),
           "clk per tile: drain", round(pr["epi_drain"] / max(pr["tiles"], 1)),
-          "rmw", round(pr["epi_rmw"] / max(pr["tiles"], 1)))
+          "rmw", round(pr["epi_rmw"] / max(pr["tiles"], 1)),
+          "GEMM busy ms (issuer loops / 148 SMs)", round(pr["mma_loop_ns"] / 148e6, 1))
 print("factor_by_level", [round(x, 1) for x in lev["factor_by_level"][:15]])
 print("gemm_by_level", [round(x, 1) for x in lev["gemm_by_level"][:15]])
 print("classes", {k: round(v, 1) for k, v in cls.items()})

@@ -193,6 +193,80 @@ __global__ void k_rateN(int iters, int32_t* sink) {
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" :: "r"(tb));
 }
+// Sustained rate: the same N = 256 loop with pseudo-random operand bytes (the
+// burst loop above uses 3-bit values), launched back to back for several
+// seconds; SM clock from %globaltimer against clock64 inside the kernel.  This
+// is the roofline denominator for an INT8 kernel timed inside a long step:
+// the board power cap, not the issue rate, sets it.
+template <int N, int NACC>
+__global__ void k_rateS(int iters, int32_t* sink, unsigned long long* clk) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  int8_t* As = (int8_t*)sm;
+  int8_t* Bs = As + 4 * 32 * 128;
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int e = tid; e < 4 * 32 * 128 + 4 * 32 * N; e += blockDim.x) {
+    uint32_t h = (uint32_t)e * 2654435761u + blockIdx.x * 40503u;
+    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+    As[e] = (int8_t)(h & 0xFF);
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" :: "r"(smem_u32(&tbase)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  if (tid == 0) mbar_init(&bar, 1);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tb = tbase;
+  unsigned long long n0 = 0, n1 = 0;
+  long long c0 = 0, c1 = 0;
+  if (tid == 0) {
+    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(n0));
+    c0 = clock64();
+    const uint32_t idesc = idesc_i8(128, N);
+    for (int it = 0; it < iters; ++it)
+      for (int q = 0; q < 28; ++q) {
+        const uint64_t da = make_desc(smem_u32(As + (q % 4) * 32 * 128), 128 * 16, 128);
+        const uint64_t db = make_desc(smem_u32(Bs + ((q / 4) % 4) * 32 * N), N * 16, 128);
+        mma_i8(tb + (q % NACC) * N, da, db, idesc, it > 0 || q >= NACC);
+      }
+    mma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  if (tid == 0) {
+    c1 = clock64();
+    asm volatile("mov.u64 %0, %%globaltimer;\n" : "=l"(n1));
+    if (blockIdx.x == 0) { clk[0] = (unsigned long long)(c1 - c0); clk[1] = n1 - n0; }
+  }
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  int32_t v[16];
+  tmem_ld16(tb + ((uint32_t)((warp & 3) * 32) << 16), v);
+  if (v[0] == 123456789) sink[0] = v[1];
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" :: "r"(tb));
+}
+void sustained(int32_t* sink) {
+  CK(cudaFuncSetAttribute(k_rateS<256, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
+  unsigned long long* clk;
+  CK(cudaMalloc(&clk, 16));
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int iters = 100000, ctas = 148;      // ~0.2 s per launch
+  for (int rep = 0; rep < 30; ++rep) {
+    cudaEventRecord(e0); k_rateS<256, 2><<<ctas, 128, 120 * 1024>>>(iters, sink, clk); cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms; cudaEventElapsedTime(&ms, e0, e1);
+    unsigned long long h[2];
+    CK(cudaMemcpy(h, clk, 16, cudaMemcpyDeviceToHost));
+    if (rep % 3 == 2 || rep == 0)
+      printf("sustained rep %2d: %.1f ms, %.1f TOPS, SM clock %.0f MHz\n", rep, ms,
+             2.0 * ctas * iters * 28.0 * 128 * 256 * 32 / (ms * 1e-3) / 1e12, 1e3 * (double)h[0] / (double)h[1]);
+  }
+}
+
 template <int N, int NACC>
 void rateN(int32_t* sink) {
   CK(cudaFuncSetAttribute(k_rateN<N, NACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 120 * 1024));
@@ -205,7 +279,13 @@ void rateN(int32_t* sink) {
   printf("N=%d acc=%d: %.1f TOPS\n", N, NACC, 2.0 * ctas * iters * 28.0 * 128 * N * 32 / (ms * 1e-3) / 1e12);
 }
 
-int main() {
+int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 's') {
+    int32_t* sk;
+    CK(cudaMalloc(&sk, 4));
+    sustained(sk);
+    return 0;
+  }
   constexpr int K = 128;
   const int nlev = 7;
   std::vector<int8_t> A(128 * K), B(64 * K);
