@@ -1164,6 +1164,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   if (const char* e = getenv("RBA_DIAG")) c->diag_v1 = std::string(e) == "v1";
   if (const char* e = getenv("RBA_BWD_GEMM")) c->bwd_gemm = atoi(e) ? 1 : 0;
   if (const char* e = getenv("RBA_FWD_GEMM")) c->fwd_gemm = atoi(e) ? 1 : 0;
+  rba::solve_env_refresh();
   if (const char* e = getenv("RBA_OZAKI")) c->ozaki = std::string(e) != "0";
   if (const char* e = getenv("RBA_OZ_MINK")) c->oz_min_k = std::max(16, atoi(e));
   if (const char* e = getenv("RBA_OZ_TRAIL")) c->oz_trail = std::string(e) != "0";

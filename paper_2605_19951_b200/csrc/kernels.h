@@ -61,6 +61,7 @@ void launch_solve_level(cudaStream_t st, bool forward, int nr, const SolveTask* 
                         int ntasks, int nslots, const FrontsDev& F, const SolveBatch& b,
                         int* ticket, int epoch, const int32_t* parent, const int32_t* need_u,
                         bool fused, bool stagex = false);
+void solve_env_refresh();
 void launch_solve_small(cudaStream_t st, bool forward, int nr, const int32_t* fronts, int nfr,
                         int nslots, const FrontsDev& F, const SolveBatch& b, int mb);
 // receiver-Green build: backward sweep over Z (N x Mr) as DMMA GEMMs

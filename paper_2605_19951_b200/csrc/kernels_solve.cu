@@ -918,14 +918,16 @@ __global__ void __launch_bounds__(256) k_bwd_small(const int32_t* __restrict__ f
 // slower, 27 -> 32 ms: the 8 x 64 B segments of an A fragment load keep fewer
 // bytes in flight per register than the scalar kernel's 512 B row segments;
 // it needs a TMA-fed shared-memory ring to pay)
+static int g_bwd_mma = -1;
 static int bwd_mma_mode() {
-  static int v = -1;
-  if (v < 0) {
+  if (g_bwd_mma < 0) {
     const char* e = getenv("RBA_BWD_MMA");
-    v = e ? atoi(e) : 1;
+    g_bwd_mma = e ? atoi(e) : 1;
   }
-  return v;
+  return g_bwd_mma;
 }
+// re-read the environment (every rba_ctx_create: the tests switch variants per context)
+void solve_env_refresh() { g_bwd_mma = -1; }
 static bool bwd_mma_on() { return bwd_mma_mode() >= 1; }
 
 template <int NR>

@@ -150,3 +150,29 @@ def test_ozaki_cluster_pair_bitwise(gpu, ozaki, monkeypatch):
         b = _factor_bytes(monkeypatch, n, True, True)
         for x, y in zip(a, b):
             assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
+
+
+def test_ozaki_ring_depth_and_passes(gpu, ozaki, monkeypatch):
+    """RBA_OZ_STAGES=5 (deeper load ring) gives the same bits; RBA_OZ_KMAX=128
+    (Schur updates in passes of <= 128 pivots, each with its own row scaling)
+    rounds differently but keeps SuperLU's backward error."""
+    a = _factor_bytes(monkeypatch, 10, True)
+    monkeypatch.setenv("RBA_OZ_STAGES", "5")
+    b = _factor_bytes(monkeypatch, 10, True)
+    for x, y in zip(a, b):
+        assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
+    monkeypatch.setenv("RBA_OZ_KMAX", "128")
+    prob, _ = rb.build_config("C4", n=10)
+    approx = rb.config_approximant("C4")
+    eng = Engine(prob, approx)
+    eng.set_model(prob.m_true)
+    eng.factor()
+    M = orc.assemble_M(prob, prob.m_true)
+    rng = np.random.default_rng(5)
+    rhs = rng.standard_normal(eng.N) + 1j * rng.standard_normal(eng.N)
+    for i in (0, 9):
+        A = (prob.K.astype(complex) - approx.poles[i] * M.astype(complex)).tocsr()
+        e = _bwd(A, eng.solve(i, rhs), rhs)
+        print(f"RBA_OZ_KMAX=128 pole {i}: backward error {e:.2e}")
+        assert e <= 1e-15
+    eng.close()

@@ -278,6 +278,34 @@ def test_eight_rhs_solves_vs_splu(gpu):
         assert err <= 1e-9
 
 
+@pytest.mark.parametrize("mode", ["0", "1", "2"])
+def test_four_rhs_backward_kernels(gpu, monkeypatch, mode):
+    """4 right-hand sides (C3/C4's 4 sources): the backward sweep's variants --
+    scalar kernels (RBA_BWD_MMA=0), FP64 tensor-core kernel for the small
+    fronts (1, default) and for the large fronts too (2) -- all agree with
+    SuperLU column by column (n = 12 with air layers: fronts of several pivot
+    blocks, borders longer than one shared-memory chunk are covered by the C4
+    tests)."""
+    monkeypatch.setenv("RBA_BWD_MMA", mode)
+    prob, _ = rb.build_config("C4", n=12)
+    approx = rb.config_approximant("C4")
+    model = rb.Model(prob.m_true, prob.m_true)
+    cache = rb.ShiftedFactorCache()
+    rb.factorize_all_poles(prob, model, approx, cache)
+    assert cache.engine.S == 4
+    M = orc.assemble_M(prob, model.m)
+    rng = np.random.default_rng(4)
+    B = rng.standard_normal((prob.dof_count, 4)) + 1j * rng.standard_normal((prob.dof_count, 4))
+    for i in (0, 9):
+        A = (prob.K.astype(complex) - approx.poles[i] * M.astype(complex)).tocsc()
+        X = cache.solve(i, B)
+        r = max(np.linalg.norm(A @ X[:, k] - B[:, k]) /
+                (abs(A).sum(axis=1).max() * np.linalg.norm(X[:, k]) + np.linalg.norm(B[:, k])) for k in range(4))
+        print(f"RBA_BWD_MMA={mode} pole {i}: normwise backward error {r:.2e}")
+        assert r <= 1e-15           # (with 1e-8 S/m air the forward error is cond(A) x this)
+    cache.engine.close()
+
+
 def _c1_true():
     z = golden("ref3d_C1_true.npz")
     prob, _ = rb.build_config("C1", n=int(z["n"]))
