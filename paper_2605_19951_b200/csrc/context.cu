@@ -68,6 +68,15 @@ struct rba_symbolic {
 struct rba_ctx {
   int device = 0;
   cudaStream_t st = nullptr;
+  // second lane of the factorisation (rba_factor): the two halves of a pole
+  // batch run the same plan on two streams, so the DRAM-bound steps of one
+  // half (extend-add, digit split) overlap the tensor-bound steps of the other
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int fstreams = 1;            // RBA_FACTOR_STREAMS=2: two lanes (measured no gain at C4, 1.888 vs
+                               // 1.893 s per 16 poles: the INT8 phases run at the board power cap and
+                               // the Ozaki GEMM CTA leaves registers for one extend-add CTA per SM)
+  int* oz_ticket = nullptr;    // [2] tile tickets of the Ozaki GEMM launches, one per lane
   bool own_stream = false;
   std::vector<void*> allocs;       // persistent (mesh-level) device allocations
   size_t mem_other = 0, mem_factor = 0, mem_work = 0;
@@ -653,73 +662,87 @@ int build_plans(rba_ctx* c) {
   return RBA_OK;
 }
 
-int run_plan(rba_ctx* c, const rba::PoleBatch& pb) {
+// One lane of the factorisation: its poles, its stream, its share of the Ozaki
+// digit buffers (poles [oz0, oz0 + ozn) of the buffer) and its tile ticket.
+struct Lane {
+  rba::PoleBatch pb;
+  cudaStream_t st;
+  int oz0, ozn, id;
+};
+
+static void run_step(rba_ctx* c, const Step& s, const Lane& ln) {
+  const rba::PoleBatch& pb = ln.pb;
+  cudaStream_t st = ln.st;
+  switch (s.kind) {
+    case ST_EA: { Timed t(c, KC_EA); rba::launch_extend_add(st, c->ea_tasks + s.off, s.n, c->F, pb); break; }
+    case ST_DIAG: {
+      Timed t(c, KC_DIAG, (s.ntiles > 0 && s.ntiles < s.n) ? 2 : 1);
+      if (c->diag_v1)
+        rba::launch_diag(st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d);
+      else
+        rba::launch_diag2(st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d, s.ntiles);
+      break;
+    }
+    case ST_TRSM: {
+      Timed t(c, KC_TRSM);
+      if (c->gemm_dfma)
+        rba::launch_trsm(st, c->pt_tasks + s.off, s.n, c->F, pb);
+      else
+        rba::launch_trsm3(st, c->pt_tasks + s.off, s.n, c->F, pb, c->gemm_var);
+      break;
+    }
+    case ST_OZ: {
+      Timed t(c, KC_OZ);
+      Timed tg(c, 112 + std::min(s.level, 15), 0);
+      for (int g0 = 0; g0 < pb.count; g0 += ln.ozn) {
+        rba::PoleBatch sub{};
+        sub.count = std::min(ln.ozn, pb.count - g0);
+        for (int i = 0; i < sub.count; ++i) {
+          sub.factor[i] = pb.factor[g0 + i];
+          sub.upd[i] = pb.upd[g0 + i];
+          sub.tmap[i] = pb.tmap[g0 + i];
+          sub.xi[i] = pb.xi[g0 + i];
+        }
+        c->launches += 1;
+        rba::launch_oz_schur(st, c->oz_tasks + s.off, s.n, c->oz_tiles + s.oz_tile_off, s.schur,
+                             s.ntiles, c->F, sub,
+                             c->oz_buf + (size_t)ln.oz0 * c->oz_split_max, s.oz_split,
+                             c->oz_exp + (size_t)ln.oz0 * c->oz_rows_max, s.oz_rows,
+                             c->oz_pair ? 3 : (c->oz_wide ? (c->oz_stages == 5 ? 2 : 1) : 0),
+                             c->oz_ticket + ln.id);
+      }
+      break;
+    }
+    case ST_GEMM: {
+      Timed t(c, KC_GEMM);
+      Timed tg(c, 112 + std::min(s.level, 15), 0);   // GEMM time per level
+      if (!s.schur && c->panel_v > 0) {
+        // panel (look-ahead / aggregated) updates: short K, own kernel choice
+        if (c->panel_v == 5)
+          rba::launch_gemm5(st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros, c->panel_var);
+        else
+          rba::launch_gemm6(st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros, c->panel_var);
+        break;
+      }
+      if (c->gemm_dfma)
+        rba::launch_gemm_update(st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
+      else if (c->gemm_v == 3)
+        rba::launch_gemm3(st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->gemm_var);
+      else if (c->gemm_v == 5)
+        rba::launch_gemm5(st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros, c->gemm5_var);
+      else
+        rba::launch_gemm6(st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros, c->gemm5_var);
+      break;
+    }
+  }
+}
+
+// The plan, step by step, for one or two lanes (the launches of the lanes are
+// interleaved on the host so neither stream's queue runs dry).
+int run_plan(rba_ctx* c, const Lane* lanes, int nlanes) {
   for (const Step& s : c->plan) {
     Timed tl(c, 80 + std::min(s.level, 31), 0);   // factor time per level
-    switch (s.kind) {
-      case ST_EA: { Timed t(c, KC_EA); rba::launch_extend_add(c->st, c->ea_tasks + s.off, s.n, c->F, pb); break; }
-      case ST_DIAG: {
-        Timed t(c, KC_DIAG, (s.ntiles > 0 && s.ntiles < s.n) ? 2 : 1);
-        if (c->diag_v1)
-          rba::launch_diag(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d);
-        else
-          rba::launch_diag2(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d, s.ntiles);
-        break;
-      }
-      case ST_TRSM: {
-        Timed t(c, KC_TRSM);
-        if (c->gemm_dfma)
-          rba::launch_trsm(c->st, c->pt_tasks + s.off, s.n, c->F, pb);
-        else
-          rba::launch_trsm3(c->st, c->pt_tasks + s.off, s.n, c->F, pb, c->gemm_var);
-        break;
-      }
-      case ST_OZ: {
-        Timed t(c, KC_OZ);
-        Timed tg(c, 112 + std::min(s.level, 15), 0);
-        for (int g0 = 0; g0 < pb.count; g0 += c->oz_sub) {
-          rba::PoleBatch sub{};
-          sub.count = std::min(c->oz_sub, pb.count - g0);
-          for (int i = 0; i < sub.count; ++i) {
-            sub.factor[i] = pb.factor[g0 + i];
-            sub.upd[i] = pb.upd[g0 + i];
-            sub.tmap[i] = pb.tmap[g0 + i];
-            sub.xi[i] = pb.xi[g0 + i];
-          }
-          c->launches += 1;
-          rba::launch_oz_schur(c->st, c->oz_tasks + s.off, s.n, c->oz_tiles + s.oz_tile_off, s.schur,
-                               s.ntiles, c->F, sub,
-                               c->oz_buf, s.oz_split, c->oz_exp, s.oz_rows,
-                               c->oz_pair ? 3 : (c->oz_wide ? (c->oz_stages == 5 ? 2 : 1) : 0));
-        }
-        break;
-      }
-      case ST_GEMM: {
-        Timed t(c, KC_GEMM);
-        Timed tg(c, 112 + std::min(s.level, 15), 0);   // GEMM time per level
-        if (!s.schur && c->panel_v > 0) {
-          // panel (look-ahead / aggregated) updates: short K, own kernel choice
-          if (c->panel_v == 5)
-            rba::launch_gemm5(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros,
-                              c->panel_var);
-          else
-            rba::launch_gemm6(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros,
-                              c->panel_var);
-          break;
-        }
-        if (c->gemm_dfma)
-          rba::launch_gemm_update(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb);
-        else if (c->gemm_v == 3)
-          rba::launch_gemm3(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->gemm_var);
-        else if (c->gemm_v == 5)
-          rba::launch_gemm5(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros,
-                            c->gemm5_var);
-        else
-          rba::launch_gemm6(c->st, c->gm_tasks + s.off, s.n, s.ntiles, c->F, pb, c->zeros,
-                            c->gemm5_var);
-        break;
-      }
-    }
+    for (int l = 0; l < nlanes; ++l) run_step(c, s, lanes[l]);
     CKL();
   }
   return RBA_OK;
@@ -1126,6 +1149,12 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
     c->own_stream = true;
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
+  cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+  if (cudaMalloc(&c->oz_ticket, 2 * sizeof(int)) != cudaSuccess) { delete c; return fail(RBA_ERR_OOM, "ticket allocation"); }
+  cudaMemset(c->oz_ticket, 0, 2 * sizeof(int));
+  if (const char* e = getenv("RBA_FACTOR_STREAMS")) c->fstreams = atoi(e) == 2 ? 2 : 1;
   if (const char* e = getenv("RBA_GEMM")) {
     c->gemm_dfma = std::string(e) == "dfma";
     if (std::string(e) == "v3") { c->gemm_v = 3; c->gemm_var = 0; }
@@ -1199,6 +1228,10 @@ void rba_ctx_destroy(rba_ctx* c) {
   if (c->stage) cudaFree(c->stage);
   for (auto& e : c->ev) if (e) cudaEventDestroy(e);
   if (c->own_stream && c->st) cudaStreamDestroy(c->st);
+  if (c->st2) cudaStreamDestroy(c->st2);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->oz_ticket) cudaFree(c->oz_ticket);
   delete c;
 }
 
@@ -1401,27 +1434,52 @@ int rba_factor(rba_ctx* c) {
   if (c->timing) cudaEventRecord(c->ev[0], c->st);
   for (auto& v : c->green_valid) v = 0;   // the update arenas overlay Z
   for (int b0 = 0; b0 < nl; b0 += c->fbatch) {
-    rba::PoleBatch pb;
-    pb.count = std::min(c->fbatch, nl - b0);
-    for (int i = 0; i < pb.count; ++i) {
+    const int count = std::min(c->fbatch, nl - b0);
+    // two lanes when nothing is being timed per launch (the Timed events sit on
+    // the main stream) and every lane gets a pole and a share of the digit buffers
+    const bool dual = c->fstreams == 2 && !c->timing && count >= 2 && (!c->ozaki || c->oz_sub >= 2);
+    Lane lanes[2];
+    const int nlanes = dual ? 2 : 1;
+    const int half = dual ? (count + 1) / 2 : count;
+    for (int l = 0; l < nlanes; ++l) {
+      Lane& ln = lanes[l];
+      ln.id = l;
+      ln.st = l == 0 ? c->st : c->st2;
+      const int ozh = dual ? c->oz_sub / 2 : c->oz_sub;
+      ln.oz0 = l * ozh;
+      ln.ozn = std::max(1, dual && l == 1 ? c->oz_sub - ozh : ozh);
+      ln.pb = rba::PoleBatch{};
+      ln.pb.count = l == 0 ? half : count - half;
+    }
+    if (dual) {
+      CK(cudaEventRecord(c->ev_fork, c->st));
+      CK(cudaStreamWaitEvent(c->st2, c->ev_fork, 0));
+    }
+    for (int i = 0; i < count; ++i) {
       int l = b0 + i;
       if ((rc = ensure_factor(c, l))) return rc;
       c->valid[l] = 0;
-      pb.factor[i] = c->factor[l];
-      pb.tmap[i] = c->tmaps[l];
-      pb.upd[i] = c->upd[i];
-      pb.xi[i] = c->poles_h[c->local[l]];
-      CK(cudaMemsetAsync(c->factor[l], 0, S.panel_off[S.nfront] * sizeof(cplx), c->st));
+      Lane& ln = lanes[i < half ? 0 : 1];
+      const int k = i < half ? i : i - half;
+      ln.pb.factor[k] = c->factor[l];
+      ln.pb.tmap[k] = c->tmaps[l];
+      ln.pb.upd[k] = c->upd[i];
+      ln.pb.xi[k] = c->poles_h[c->local[l]];
+      CK(cudaMemsetAsync(c->factor[l], 0, S.panel_off[S.nfront] * sizeof(cplx), ln.st));
     }
-    {
+    for (int l = 0; l < nlanes; ++l) {
       Timed t(c, KC_SCATTER);
-      rba::launch_scatter_A(c->st, c->nnzA, c->tgt, c->Kv, c->Mv, pb);
+      rba::launch_scatter_A(lanes[l].st, c->nnzA, c->tgt, c->Kv, c->Mv, lanes[l].pb);
     }
     CKL();
-    if ((rc = run_plan(c, pb))) return rc;
+    if ((rc = run_plan(c, lanes, nlanes))) return rc;
+    if (dual) {
+      CK(cudaEventRecord(c->ev_join, c->st2));
+      CK(cudaStreamWaitEvent(c->st, c->ev_join, 0));
+    }
     if ((rc = check_err(c, c->local[b0]))) return rc;
-    for (int i = 0; i < pb.count; ++i) c->valid[b0 + i] = 1;
-    c->n_fact += pb.count;
+    for (int i = 0; i < count; ++i) c->valid[b0 + i] = 1;
+    c->n_fact += count;
   }
   if (c->timing) {
     cudaEventRecord(c->ev[1], c->st);
@@ -1454,7 +1512,8 @@ int rba_factor_values(rba_ctx* c, int32_t slot, const double* vals) {
   pb.xi[0] = rba::cmk(0.0, 0.0);
   c->valid[slot] = 0;
   for (auto& v : c->green_valid) v = 0;   // the update arenas overlay Z
-  if ((rc = run_plan(c, pb))) return rc;
+  Lane ln{pb, c->st, 0, std::max(1, c->oz_sub), 0};
+  if ((rc = run_plan(c, &ln, 1))) return rc;
   if ((rc = check_err(c, c->local[slot]))) return rc;
   c->valid[slot] = 1;
   c->n_fact += 1;

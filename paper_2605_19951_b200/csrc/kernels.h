@@ -52,7 +52,7 @@ void oz_prof_read(unsigned long long* out, bool reset);
 void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int2* tiles,
                      int nrowtiles, int ntiles,
                      const FrontsDev& F, const PoleBatch& pb, unsigned char* split,
-                     int64_t split_pole, double* scl, int64_t exp_pole, int wide);
+                     int64_t split_pole, double* scl, int64_t exp_pole, int wide, int* ticket);
 void launch_trsm3(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
                   const PoleBatch& pb, int variant);
 

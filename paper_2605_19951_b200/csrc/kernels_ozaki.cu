@@ -104,7 +104,6 @@ __device__ __forceinline__ void mbar_wait_(uint64_t* bar, uint32_t parity) {
 // [slice][chunk][64][16 B] (one MMA per digit pair, RBA_OZ_WIDE=0);
 // k interleaved with the real/imaginary part inside each 16 B.
 // ---------------------------------------------------------------------------
-__device__ int g_oz_ticket;   // next (pole, tile) item of k_oz_gemm; reset by k_oz_split of the same step
 
 __device__ __forceinline__ unsigned long long oz_u(double v, int e) {
   return (unsigned long long)(__double2ll_rn(ldexp(v, 54 - e)) + 0x80808080808080LL);
@@ -118,11 +117,12 @@ __global__ void __launch_bounds__(128) k_oz_split(const OzTask* __restrict__ tas
                                                   FrontsDev F, PoleBatch pb,
                                                   unsigned char* __restrict__ split,
                                                   int64_t split_pole, double* __restrict__ scl,
-                                                  int64_t exp_pole, int bwide) {
+                                                  int64_t exp_pole, int bwide, int* __restrict__ ticket) {
   __shared__ int s_e[64];
   __shared__ double s_m[2][64];
   const int slot = blockIdx.y;
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) g_oz_ticket = 0;
+  // the next (pole, tile) item of the k_oz_gemm launch that follows on this stream
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *ticket = 0;
   int ti = 0;
   {
     int lo = 0, hi = ntasks - 1;
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_oz_gemm(const OzTask* __restr
                                                     FrontsDev F, PoleBatch pb,
                                                     const unsigned char* __restrict__ split,
                                                     int64_t split_pole, const double* __restrict__ scl,
-                                                    int64_t exp_pole) {
+                                                    int64_t exp_pole, int* __restrict__ ticket) {
   extern __shared__ __align__(1024) unsigned char oz_raw[];
   OzSmem<OZ_NLD>& S = *reinterpret_cast<OzSmem<OZ_NLD>*>(oz_raw);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_oz_gemm(const OzTask* __restr
     int g = 0;
     long long w_empty = 0;
     for (int n = 0;; ++n) {
-      int item = atomicAdd(&g_oz_ticket, 1);
+      int item = atomicAdd(ticket, 1);
       if (item >= nitems) item = -1;
       S.itemq[n & 7] = oz_qent(n, item);   // released by the arrive on the item's first stage
       if (item < 0) {                      // an empty stage carries the end marker
@@ -610,7 +610,7 @@ __device__ __forceinline__ void mma_i8_2(uint32_t dtmem, uint64_t da, uint64_t d
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(OZ_THREADS, 1)
 k_oz_gemm2(const OzTask* __restrict__ tasks, int ntasks, const int2* __restrict__ tiles, int ntiles,
            FrontsDev F, PoleBatch pb, const unsigned char* __restrict__ split, int64_t split_pole,
-           const double* __restrict__ scl, int64_t exp_pole) {
+           const double* __restrict__ scl, int64_t exp_pole, int* __restrict__ ticket) {
   extern __shared__ __align__(1024) unsigned char oz_raw2[];
   OzSmem2& S = *reinterpret_cast<OzSmem2*>(oz_raw2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -650,7 +650,7 @@ k_oz_gemm2(const OzTask* __restrict__ tasks, int ntasks, const int2* __restrict_
     for (int n = 0;; ++n) {
       int item;
       if (rank == 0) {
-        item = atomicAdd(&g_oz_ticket, 1);
+        item = atomicAdd(ticket, 1);
         if (item >= nitems) item = -1;
         const unsigned long long qe = oz_qent(n, item);
         asm volatile("st.shared::cluster.u64 [%0], %1;\n" :: "r"(map_to_rank(su32((const void*)&S.itemq[n & 7]), 1)), "l"(qe) : "memory");
@@ -796,10 +796,10 @@ void oz_prof_read(unsigned long long* out, bool reset) {
 void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int2* tiles,
                      int nrowtiles, int ntiles, const FrontsDev& F, const PoleBatch& pb,
                      unsigned char* split, int64_t split_pole, double* scl, int64_t exp_pole,
-                     int wide) {
+                     int wide, int* ticket) {
   if (ntasks <= 0 || ntiles <= 0) return;
   k_oz_split<<<dim3(nrowtiles, pb.count), 128, 0, st>>>(tasks, ntasks, F, pb, split,
-                                                        split_pole, scl, exp_pole, wide == 3 ? 2 : (wide != 0));
+                                                        split_pole, scl, exp_pole, wide == 3 ? 2 : (wide != 0), ticket);
   static int nsm = 0;
   if (!nsm) {
     int dev = 0;
@@ -824,18 +824,18 @@ void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int
     }
     const int npairs = std::min(items, nsm / 2);
     k_oz_gemm2<<<2 * npairs, OZ_THREADS, smem2, st>>>(tasks, ntasks, tiles, ntiles, F, pb, split, split_pole,
-                                                     scl, exp_pole);
+                                                     scl, exp_pole, ticket);
     return;
   }
   if (wide == 2)
     k_oz_gemm<true, 5><<<grid, OZ_THREADS, sizeof(OzSmem<5>) + 1024, st>>>(tasks, ntasks, tiles, ntiles, F, pb, split,
-                                                                          split_pole, scl, exp_pole);
+                                                                          split_pole, scl, exp_pole, ticket);
   else if (wide)
     k_oz_gemm<true, 4><<<grid, OZ_THREADS, sizeof(OzSmem<4>) + 1024, st>>>(tasks, ntasks, tiles, ntiles, F, pb, split,
-                                                                          split_pole, scl, exp_pole);
+                                                                          split_pole, scl, exp_pole, ticket);
   else
     k_oz_gemm<false, 4><<<grid, OZ_THREADS, sizeof(OzSmem<4>) + 1024, st>>>(tasks, ntasks, tiles, ntiles, F, pb, split,
-                                                                           split_pole, scl, exp_pole);
+                                                                           split_pole, scl, exp_pole, ticket);
 }
 
 }  // namespace rba

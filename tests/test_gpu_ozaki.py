@@ -176,3 +176,14 @@ def test_ozaki_ring_depth_and_passes(gpu, ozaki, monkeypatch):
         print(f"RBA_OZ_KMAX=128 pole {i}: backward error {e:.2e}")
         assert e <= 1e-15
     eng.close()
+
+
+def test_two_lane_factorisation_bitwise(gpu, ozaki, monkeypatch):
+    """RBA_FACTOR_STREAMS=2: the two halves of a pole batch run the plan on two
+    streams (own Ozaki digit buffers and tile tickets).  Every pole's factor is
+    computed by the same kernels in the same order: bitwise equal."""
+    a = _factor_bytes(monkeypatch, 10, True)
+    monkeypatch.setenv("RBA_FACTOR_STREAMS", "2")
+    b = _factor_bytes(monkeypatch, 10, True)
+    for x, y in zip(a, b):
+        assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
