@@ -20,6 +20,8 @@ collectives; every arithmetic step runs in libdrba.so kernels.
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import scipy.sparse as sp
 import torch
@@ -77,7 +79,7 @@ class Engine:
         ki = np.ascontiguousarray(K.indices, dtype=np.int32)
         kx = np.ascontiguousarray(K.data, dtype=np.float64)
         check(self.lib.rba_set_mesh(self.ctx, self.N, self.P, k, ptr(cd), ptr(ml), ptr(kp),
-                                    ptr(ki), ptr(kx), ptr(coords), int(leaf)))
+                                    ptr(ki), ptr(kx), ptr(coords), int(os.environ.get("RBA_LEAF", leaf))))
         Q = sp.csr_matrix(problem.Q)
         self.Mr = int(Q.shape[0])
         qp = np.ascontiguousarray(Q.indptr, dtype=np.int64)
