@@ -377,8 +377,13 @@ def run_ours(args, world, rank):
     rooflines["factorisation"] = {k: roof[k] for k in ("achieved", "unit", "peak", "frac")}
     if rooflines.get("ozaki_int8_schur") and rooflines.get("dmma_gemm"):
         dom = max(("ozaki_int8_schur", "dmma_gemm"), key=lambda k: rooflines[k]["ms_per_step"])
-        roof = dict(rooflines[dom], kernel=dom, traffic=None,
-                    traffic_unit="see profiles/ for the ncu capture of this kernel",
+        try:
+            oz_traffic = json.load(open(os.path.join(ROOT, "profiles", "dram_r02.json")))["ozaki_gemm_launches"]
+        except (OSError, KeyError):
+            oz_traffic = None
+        roof = dict(rooflines[dom], kernel=dom,
+                    traffic=oz_traffic if dom == "ozaki_int8_schur" else None,
+                    traffic_unit="DRAM bytes of single k_oz_gemm launches (ncu --set full, profiles/dram_r02.json)",
                     units_per_step=n_local_fact)
     value = ms_step / 1e3
     line = {
