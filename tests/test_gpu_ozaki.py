@@ -187,3 +187,24 @@ def test_two_lane_factorisation_bitwise(gpu, ozaki, monkeypatch):
     b = _factor_bytes(monkeypatch, 10, True)
     for x, y in zip(a, b):
         assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
+
+
+def test_ozaki_role_counters(gpu, ozaki):
+    """rba_oz_prof: the GEMM's own cycle counters are consistent -- k steps and
+    tiles counted, waits inside the issuer loop, an SM clock in the B200's
+    range (measured with %globaltimer against clock64 inside the kernel)."""
+    prob, _ = rb.build_config("C4", n=12)
+    approx = rb.config_approximant("C4")
+    eng = Engine(prob, approx)
+    eng.set_model(prob.m_true)
+    eng.oz_prof(True)
+    eng.factor()
+    pr = eng.oz_prof(True)
+    assert pr["tiles"] > 0 and pr["ksteps"] >= pr["tiles"]
+    assert 0 <= pr["mma_wait_data"] + pr["mma_wait_tmem"] <= pr["mma_loop"]
+    mhz = 1e3 * pr["mma_loop"] / pr["mma_loop_ns"]
+    print(f"Ozaki GEMM: {pr['tiles']:.0f} tiles, {pr['ksteps']:.0f} k steps, SM clock {mhz:.0f} MHz")
+    assert 500 <= mhz <= 2500
+    again = eng.oz_prof(False)
+    assert again["tiles"] == 0          # reset by the previous read
+    eng.close()
