@@ -114,6 +114,9 @@ struct rba_ctx {
   double oz_int8_ops = 0, oz_flops = 0;   // per pole factorisation: executed int8 ops,
                                           // FP64-equivalent (4-multiply) flops
   int oz_sub = 1;              // poles per Ozaki launch (digit-buffer budget)
+  int oz_ts = 0;               // RBA_OZ_TS=1: A digits staged in TMEM (tcgen05.cp), wide MMAs read A from TMEM
+                               // (bitwise equal; 981 clk per k step alone, tools/umma_i8_ts_probe.cu, but
+                               // 1,380 vs 1,189 in the kernel: off)
   int oz_pair = 0;             // RBA_OZ_2CTA=1: cluster-pair GEMM (cta_group::2, M = 256)
   int oz_wide = 1;             // RBA_OZ_WIDE=0: one N = 64 MMA per digit pair (28 per k step)
                                // instead of 10 wide ones (same integer sums, bitwise equal)
@@ -708,7 +711,7 @@ static void run_step(rba_ctx* c, const Step& s, const Lane& ln) {
                              s.ntiles, c->F, sub,
                              c->oz_buf + (size_t)ln.oz0 * c->oz_split_max, s.oz_split,
                              c->oz_exp + (size_t)ln.oz0 * c->oz_rows_max, s.oz_rows,
-                             c->oz_pair ? 3 : (c->oz_wide ? (c->oz_stages == 5 ? 2 : 1) : 0),
+                             c->oz_pair ? 3 : (c->oz_wide ? (c->oz_ts ? (c->oz_stages == 5 ? 5 : 4) : (c->oz_stages == 5 ? 2 : 1)) : 0),
                              c->oz_ticket + ln.id);
       }
       break;
@@ -1198,6 +1201,7 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   if (const char* e = getenv("RBA_OZ_MINK")) c->oz_min_k = std::max(16, atoi(e));
   if (const char* e = getenv("RBA_OZ_TRAIL")) c->oz_trail = std::string(e) != "0";
   if (const char* e = getenv("RBA_OZ_KMAX")) c->oz_kmax = std::max(64, atoi(e) / 16 * 16);
+  if (const char* e = getenv("RBA_OZ_TS")) c->oz_ts = std::string(e) == "1";
   if (const char* e = getenv("RBA_OZ_2CTA")) c->oz_pair = std::string(e) == "1";
   if (const char* e = getenv("RBA_OZ_WIDE")) c->oz_wide = std::string(e) != "0";
   if (const char* e = getenv("RBA_OZ_STAGES")) c->oz_stages = atoi(e) == 4 ? 4 : 5;

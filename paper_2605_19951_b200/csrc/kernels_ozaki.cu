@@ -380,7 +380,20 @@ __device__ __forceinline__ void oz_tile_epilogue(const OzTask& tk, int slot, int
 __device__ unsigned long long g_oz_prof[10];
 
 constexpr int OZ_THREADS = 320;
-template <bool WIDE, int OZ_NLD>
+// TS = true: the A digit of each (k step, t) is copied once from shared memory
+// into one of 8 TMEM slots of 8 columns (448..511, beside the 7 level
+// accumulators) by tcgen05.cp and its 1-2 wide MMAs read A from TMEM: per k
+// step the shared-memory port then carries 56 KB of B reads + 28 KB of copy
+// reads + 42 KB of bulk-copy writes = 126 KB instead of 138 KB, and -- what
+// matters -- only 86 B/clk while the MMAs run, which leaves the bulk copies the
+// 42 B/clk they need (with A from shared memory the MMAs take 104 of the 128
+// B/clk and the copies starve: 15 % of the issuer's time went into waiting
+// for data).  tcgen05.cp and tcgen05.mma of one thread execute in issue order
+// (one pipeline), so the copy that rewrites a slot 8 digits later runs after
+// the MMAs that read it: no barrier (with a commit + wait per digit the
+// issuer lost its run-ahead and the k step took 2,660 clocks).  Same integer
+// sums: bitwise equal.
+template <bool WIDE, int OZ_NLD, bool TS = false>
 __global__ void __launch_bounds__(OZ_THREADS, 1) k_oz_gemm(const OzTask* __restrict__ tasks, int ntasks,
                                                     const int2* __restrict__ tiles, int ntiles,
                                                     FrontsDev F, PoleBatch pb,
@@ -480,7 +493,25 @@ __global__ void __launch_bounds__(OZ_THREADS, 1) k_oz_gemm(const OzTask* __restr
         }
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         const uint32_t abase = su32(S.st[q]), bbase = abase + OZ_ABYTES;
-        if constexpr (WIDE) {
+        if constexpr (WIDE && TS) {
+#pragma unroll
+          for (int t = 1; t <= OZ_S; ++t) {
+            const int n = g * OZ_S + (t - 1);          // global A digit counter
+            const int sl = n & 7;
+            const uint32_t ta = tb + 448 + sl * 8;
+            asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;\n"
+                         :: "r"(ta), "l"(umma_desc(abase + (t - 1) * 2 * 128 * 16, 128 * 16, 128)));
+#pragma unroll
+            for (int u0 = 1; u0 <= 8 - t; u0 += 4) {
+              const int nu = (8 - t - u0 + 1) < 4 ? (8 - t - u0 + 1) : 4;
+              const uint64_t db = umma_desc(bbase + (u0 - 1) * 64 * 16, OZ_S * 64 * 16, 128);
+              asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                           " tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n}\n"
+                           :: "r"(tb + (uint32_t)((t + u0 - 2) * 64)), "r"(ta), "l"(db), "r"(oz_idesc(64 * nu)),
+                              "r"((ks > 0 || t > 1) ? 1 : 0));
+            }
+          }
+        } else if constexpr (WIDE) {
           // A digit t x B digits u0..u1 -> levels t + u0 .. t + u1 (TMEM columns
           // 64 (t + u0 - 2) ...): integer sums, so the order does not matter
 #pragma unroll
@@ -812,6 +843,8 @@ void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int
     cudaFuncSetAttribute(k_oz_gemm<false, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(OzSmem<4>) + 1024);
     cudaFuncSetAttribute(k_oz_gemm<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(OzSmem<4>) + 1024);
     cudaFuncSetAttribute(k_oz_gemm<true, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(OzSmem<5>) + 1024);
+    cudaFuncSetAttribute(k_oz_gemm<true, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(OzSmem<4>) + 1024);
+    cudaFuncSetAttribute(k_oz_gemm<true, 5, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(OzSmem<5>) + 1024);
     attr = true;
   }
   const int grid = std::min(items, nsm);
@@ -827,7 +860,13 @@ void launch_oz_schur(cudaStream_t st, const OzTask* tasks, int ntasks, const int
                                                      scl, exp_pole, ticket);
     return;
   }
-  if (wide == 2)
+  if (wide == 4)
+    k_oz_gemm<true, 4, true><<<grid, OZ_THREADS, sizeof(OzSmem<4>) + 1024, st>>>(tasks, ntasks, tiles, ntiles, F, pb,
+                                                                                split, split_pole, scl, exp_pole, ticket);
+  else if (wide == 5)
+    k_oz_gemm<true, 5, true><<<grid, OZ_THREADS, sizeof(OzSmem<5>) + 1024, st>>>(tasks, ntasks, tiles, ntiles, F, pb,
+                                                                                split, split_pole, scl, exp_pole, ticket);
+  else if (wide == 2)
     k_oz_gemm<true, 5><<<grid, OZ_THREADS, sizeof(OzSmem<5>) + 1024, st>>>(tasks, ntasks, tiles, ntiles, F, pb, split,
                                                                           split_pole, scl, exp_pole, ticket);
   else if (wide)

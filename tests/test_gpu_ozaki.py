@@ -107,8 +107,10 @@ def test_ozaki_c1_parity(gpu, ozaki):
     assert ef <= 1e-9 and ej <= 1e-8 and et <= 1e-8
 
 
-def _factor_bytes(monkeypatch, n, wide, pair=False):
+def _factor_bytes(monkeypatch, n, wide, pair=False, ts=None):
     monkeypatch.setenv("RBA_OZ_WIDE", "1" if wide else "0")
+    if ts is not None:
+        monkeypatch.setenv("RBA_OZ_TS", "1" if ts else "0")
     monkeypatch.setenv("RBA_OZ_2CTA", "1" if pair else "0")
     prob, _ = rb.build_config("C4", n=n)
     approx = rb.config_approximant("C4")
@@ -208,3 +210,14 @@ def test_ozaki_role_counters(gpu, ozaki):
     again = eng.oz_prof(False)
     assert again["tiles"] == 0          # reset by the previous read
     eng.close()
+
+
+def test_ozaki_tmem_a_bitwise(gpu, ozaki, monkeypatch):
+    """RBA_OZ_TS: the A digits staged in TMEM by tcgen05.cp (8 rotating slots
+    beside the level accumulators), wide MMAs with A from TMEM -- the same
+    exact int32 sums as with A from shared memory: factors bitwise equal."""
+    for n in (10, 20):
+        a = _factor_bytes(monkeypatch, n, True, False, ts=False)
+        b = _factor_bytes(monkeypatch, n, True, False, ts=True)
+        for x, y in zip(a, b):
+            assert np.array_equal(x.view(np.uint64), y.view(np.uint64))
