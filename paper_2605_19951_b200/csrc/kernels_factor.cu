@@ -98,12 +98,14 @@ __global__ void __launch_bounds__(256) k_extend_add(const int2* __restrict__ tas
       const int rc = F.nf[ch] - F.npiv[ch];
       const int32_t* rm = F.relmap + F.rel_off[ch];
       const cplx* U = pb.upd[slot] + F.upd_off[ch];
-      for (int j = 0; j < rc; ++j) {
-        const cplx* Uc = U + ucol(j, rc);
-        const int tc = rm[j];
-        for (int i = j + threadIdx.x; i < rc; i += blockDim.x) {
-          cplx* dst = faddr(panel, upd, p, nf, rm[i], tc);
-          *dst = cadd(*dst, Uc[i - j]);
+      // all (column, row) pairs of the child's block at once: a small child has
+      // fewer rows than the CTA has threads (each parent entry still receives
+      // exactly one addend per child, children in order: same sums)
+      for (int q = threadIdx.x; q < rc * rc; q += blockDim.x) {
+        const int j = q / rc, i = q - j * rc;
+        if (i >= j) {
+          cplx* dst = faddr(panel, upd, p, nf, rm[i], rm[j]);
+          *dst = cadd(*dst, U[ucol(j, rc) + (i - j)]);
         }
       }
       __syncthreads();
