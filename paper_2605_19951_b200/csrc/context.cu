@@ -42,7 +42,7 @@ int fail(int code, const std::string& msg) {
       return fail(RBA_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
   } while (0)
 
-enum StepKind { ST_EA = 0, ST_DIAG = 1, ST_TRSM = 2, ST_GEMM = 3, ST_OZ = 4 };
+enum StepKind { ST_EA = 0, ST_DIAG = 1, ST_TRSM = 2, ST_GEMM = 3, ST_OZ = 4, ST_SSCHUR = 5 };
 struct Step {
   int kind;
   int64_t off;
@@ -99,6 +99,9 @@ struct rba_ctx {
   int2* ea_tasks = nullptr;
   rba::PanelTask* pt_tasks = nullptr;
   rba::GemmTask* gm_tasks = nullptr;
+  int32_t* ss_fronts = nullptr;   // ST_SSCHUR: small fronts (one pivot block) per level
+  bool schur_small = true;        // RBA_SCHUR_SMALL=0: k_gemm6 tiles for the small fronts too
+  int schur_small_b = 288;        // largest border of a front taken by k_schur_small (RBA_SCHUR_SMALL_B)
   // Ozaki-scheme INT8 tensor-core Schur updates (RBA_OZAKI, kernels_ozaki.cu)
   bool ozaki = true;           // RBA_OZAKI=0: DMMA for every Schur update
   int oz_stages = 4;           // RBA_OZ_STAGES: load-ring depth of the wide GEMM (4 or 5; 5 measured
@@ -345,6 +348,7 @@ int build_plans(rba_ctx* c) {
   std::vector<rba::PanelTask> pt;
   std::vector<rba::GemmTask> gm;
   std::vector<rba::OzTask> oz;
+  std::vector<int32_t> ssf;
   std::vector<int2> ozt;
   c->plan.clear();
   c->oz_split_max = c->oz_rows_max = 0;
@@ -484,6 +488,7 @@ int build_plans(rba_ctx* c) {
     // Schur complement of each front with a border: large fronts on the INT8
     // tensor cores (Ozaki scheme), the rest with the DMMA GEMM
     int64_t goff = gm.size();
+    const int64_t ssoff = ssf.size();
     int tiles = 0;
     // the pivots of a wide front are taken in passes of at most oz_kmax (one
     // plan step per pass): the digit streams of the ~148 tiles in flight
@@ -506,11 +511,16 @@ int build_plans(rba_ctx* c) {
         if (opass == 1) oz_add(osc[0], s, nf, p, nf, 0, p);
         continue;
       }
+      if (c->schur_small && p <= rba::PB && nf - p <= c->schur_small_b) {   // one pivot block: fragment-exact kernel
+        ssf.push_back(s);
+        continue;
+      }
       int ntr = (nf - p + rba::GT - 1) / rba::GT;
       gm.push_back({s, 0, p, p, nf, tiles, ntr, 0});
       tiles += ntr * (ntr + 1) / 2;
     }
     if ((int64_t)gm.size() > goff) c->plan.push_back({ST_GEMM, goff, (int)(gm.size() - goff), tiles, 1});
+    if ((int64_t)ssf.size() > ssoff) c->plan.push_back({ST_SSCHUR, ssoff, (int)(ssf.size() - ssoff), 0});
     oz_end(osc[0], L);
     // tasks of one plan step are contiguous in `oz`, so the passes of a
     // multi-pass level are built one after the other
@@ -533,6 +543,7 @@ int build_plans(rba_ctx* c) {
   if ((rc = upload(c, c->allocs, &c->ea_tasks, ea.data(), ea.size()))) return rc;
   if ((rc = upload(c, c->allocs, &c->pt_tasks, pt.data(), pt.size()))) return rc;
   if ((rc = upload(c, c->allocs, &c->gm_tasks, gm.data(), gm.size()))) return rc;
+  if (!ssf.empty() && (rc = upload(c, c->allocs, &c->ss_fronts, ssf.data(), ssf.size()))) return rc;
   if (!oz.empty() && (rc = upload(c, c->allocs, &c->oz_tasks, oz.data(), oz.size()))) return rc;
   if (!ozt.empty() && (rc = upload(c, c->allocs, &c->oz_tiles, ozt.data(), ozt.size()))) return rc;
 
@@ -714,6 +725,12 @@ static void run_step(rba_ctx* c, const Step& s, const Lane& ln) {
                              c->oz_pair ? 3 : (c->oz_wide ? (c->oz_ts ? (c->oz_stages == 5 ? 5 : 4) : (c->oz_stages == 5 ? 2 : 1)) : 0),
                              c->oz_ticket + ln.id);
       }
+      break;
+    }
+    case ST_SSCHUR: {
+      Timed t(c, KC_GEMM);
+      Timed tg(c, 112 + std::min(s.level, 15), 0);
+      rba::launch_schur_small(st, c->ss_fronts + s.off, s.n, c->F, pb);
       break;
     }
     case ST_GEMM: {
@@ -1201,6 +1218,8 @@ int rba_ctx_create(int device, void* stream, rba_ctx** out) {
   if (const char* e = getenv("RBA_OZ_MINK")) c->oz_min_k = std::max(16, atoi(e));
   if (const char* e = getenv("RBA_OZ_TRAIL")) c->oz_trail = std::string(e) != "0";
   if (const char* e = getenv("RBA_OZ_KMAX")) c->oz_kmax = std::max(64, atoi(e) / 16 * 16);
+  if (const char* e = getenv("RBA_SCHUR_SMALL")) c->schur_small = std::string(e) != "0";
+  if (const char* e = getenv("RBA_SCHUR_SMALL_B")) c->schur_small_b = std::max(8, atoi(e));
   if (const char* e = getenv("RBA_OZ_TS")) c->oz_ts = std::string(e) == "1";
   if (const char* e = getenv("RBA_OZ_2CTA")) c->oz_pair = std::string(e) == "1";
   if (const char* e = getenv("RBA_OZ_WIDE")) c->oz_wide = std::string(e) != "0";

@@ -45,6 +45,8 @@ void launch_gemm3(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
                   const FrontsDev& F, const PoleBatch& pb, int variant);
 void launch_gemm5(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
                   const FrontsDev& F, const PoleBatch& pb, const cplx* zeros, int variant);
+void launch_schur_small(cudaStream_t st, const int32_t* fronts, int nfr, const FrontsDev& F,
+                        const PoleBatch& pb);
 void launch_gemm6(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
                   const FrontsDev& F, const PoleBatch& pb, const cplx* zeros, int variant);
 // Schur update of large fronts on the INT8 tensor cores (Ozaki scheme)

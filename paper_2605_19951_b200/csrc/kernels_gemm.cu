@@ -712,4 +712,72 @@ void launch_gemm6(cudaStream_t st, const GemmTask* tasks, int ntasks, int nctas,
   else launch_g6<16, 4, 32>(st, grid, tasks, ntasks, F, pb, zeros);
 }
 
+// ---------------------------------------------------------------------------
+// Schur update of the small fronts (one pivot block, p <= 64): one CTA of 4
+// warps per (front, pole); a warp takes 16 x 8 blocks of the lower triangle of
+// C (b x b, b = nf - p) and accumulates C -= L' L'^T over the p pivots with
+// mma.sync m8n8k4 on exact 8 x 8 x 4 fragments (4 real MMAs per complex
+// product).  The 64 x 32 tiles of k_gemm6 are mostly padding on these fronts
+// (C4 level 0: b ~ 70, p ~ 33 -> ~20 % useful MMAs).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_schur_small(const int32_t* __restrict__ fronts, FrontsDev F,
+                                                     PoleBatch pb) {
+  const int slot = blockIdx.y;
+  const int s = fronts[blockIdx.x];
+  const int nf = F.nf[s], p = F.npiv[s];
+  const int b = nf - p;
+  const cplx* __restrict__ panel = pb.factor[slot] + F.panel_off[s];
+  cplx* upd = pb.upd[slot] + F.upd_off[s];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int kq = lane & 3, mq = lane >> 2;
+  const int nb8 = (b + 7) >> 3, nb16 = (b + 15) >> 4;
+  const int p4 = (p + 3) & ~3;
+  // blocks (I16, J8): rows 16 I16 .. +15, columns 8 J8 .. +7, J8 <= 2 I16 + 1
+  int q = warp;
+  for (int I = 0; I < nb16; ++I) {
+    const int jmax = min(2 * I + 1, nb8 - 1);
+    for (int J = 0; J <= jmax; ++J, ++q) {
+      if ((q & 3) != 0) continue;          // round-robin over the 4 warps (q starts at warp)
+      double re[2][2] = {{0.0, 0.0}, {0.0, 0.0}}, im[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      const int r0 = p + 16 * I + mq, r1 = r0 + 8;       // A rows of this lane (two fragments)
+      const int cr = p + 8 * J + mq;                       // B row (= C column) of this lane
+#pragma unroll 2
+      for (int k0 = 0; k0 < p4; k0 += 4) {
+        const int k = k0 + kq;
+        const bool kon = k < p;
+        const cplx* col = panel + (int64_t)k * nf;
+        const cplx a0 = (kon && r0 < nf) ? __ldg(col + r0) : cmk(0.0, 0.0);
+        const cplx a1 = (kon && r1 < nf) ? __ldg(col + r1) : cmk(0.0, 0.0);
+        const cplx bb = (kon && cr < nf) ? __ldg(col + cr) : cmk(0.0, 0.0);
+        dmma(re[0][0], re[0][1], a0.x, bb.x);
+        dmma(re[1][0], re[1][1], a1.x, bb.x);
+        dmma(im[0][0], im[0][1], a0.x, bb.y);
+        dmma(im[1][0], im[1][1], a1.x, bb.y);
+        dmma(re[0][0], re[0][1], -a0.y, bb.y);
+        dmma(re[1][0], re[1][1], -a1.y, bb.y);
+        dmma(im[0][0], im[0][1], a0.y, bb.x);
+        dmma(im[1][0], im[1][1], a1.y, bb.x);
+      }
+      // fragment element (row mq, columns 2 kq, 2 kq + 1)
+#pragma unroll
+      for (int f = 0; f < 2; ++f)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int r = 16 * I + 8 * f + mq, c = 8 * J + 2 * kq + h;
+          if (r < b && c <= r) {
+            cplx* dst = upd + ucol(c, b) + (r - c);
+            const cplx v = *dst;
+            *dst = cmk(v.x - re[f][h], v.y - im[f][h]);
+          }
+        }
+    }
+  }
+}
+
+void launch_schur_small(cudaStream_t st, const int32_t* fronts, int nfr, const FrontsDev& F,
+                        const PoleBatch& pb) {
+  if (nfr <= 0) return;
+  k_schur_small<<<dim3(nfr, pb.count), 128, 0, st>>>(fronts, F, pb);
+}
+
 }  // namespace rba
