@@ -49,6 +49,7 @@ struct Step {
   int n;
   int ntiles;
   int schur;   // ST_GEMM: 1 = Schur-complement update (K = npiv), 0 = panel update;
+               // ST_DIAG: blocks of 33..48 pivots (after the ntiles blocks of <= 32);
                // ST_OZ: row tiles of the step (digit-split CTAs)
   int level;
   int64_t oz_split = 0;   // ST_OZ: digit-block bytes per pole
@@ -434,12 +435,19 @@ int build_plans(rba_ctx* c) {
         if (S.npiv[s] > k0 && S.npiv[s] - k0 <= 32) pt.push_back({s, k0, k0, 0});
       }
       const int nsmall = (int)(pt.size() - doff);
+      // then the blocks of 33..48 pivots (k_diag2<48>: 52 KB, 4 CTAs per SM instead of 2)
       for (int q = q0; q < q1; ++q) {
         int s = S.level_fronts[q];
-        if (S.npiv[s] - k0 > 32) pt.push_back({s, k0, k0, 0});
+        if (S.npiv[s] - k0 > 32 && S.npiv[s] - k0 <= 48) pt.push_back({s, k0, k0, 0});
+      }
+      const int nmid = (int)(pt.size() - doff) - nsmall;
+      for (int q = q0; q < q1; ++q) {
+        int s = S.level_fronts[q];
+        if (S.npiv[s] - k0 > 48) pt.push_back({s, k0, k0, 0});
       }
       if ((int64_t)pt.size() > doff)
-        c->plan.push_back({ST_DIAG, doff, (int)(pt.size() - doff), c->diag_v1 ? 0 : nsmall});
+        c->plan.push_back({ST_DIAG, doff, (int)(pt.size() - doff), c->diag_v1 ? 0 : nsmall,
+                           c->diag_v1 ? 0 : nmid});
       int64_t toff = pt.size();
       for (int q = q0; q < q1; ++q) {
         int s = S.level_fronts[q];
@@ -690,11 +698,11 @@ static void run_step(rba_ctx* c, const Step& s, const Lane& ln) {
   switch (s.kind) {
     case ST_EA: { Timed t(c, KC_EA); rba::launch_extend_add(st, c->ea_tasks + s.off, s.n, c->F, pb); break; }
     case ST_DIAG: {
-      Timed t(c, KC_DIAG, (s.ntiles > 0 && s.ntiles < s.n) ? 2 : 1);
+      Timed t(c, KC_DIAG, (s.ntiles > 0) + (s.schur > 0) + (s.ntiles + s.schur < s.n));
       if (c->diag_v1)
         rba::launch_diag(st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d);
       else
-        rba::launch_diag2(st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d, s.ntiles);
+        rba::launch_diag2(st, c->pt_tasks + s.off, s.n, c->F, pb, c->err_d, s.ntiles, s.schur);
       break;
     }
     case ST_TRSM: {

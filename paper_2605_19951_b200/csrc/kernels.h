@@ -36,7 +36,7 @@ void launch_extend_add(cudaStream_t st, const int2* tasks, int ntasks, const Fro
 void launch_diag(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
                  const PoleBatch& pb, int* err);
 void launch_diag2(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
-                  const PoleBatch& pb, int* err, int nsmall = 0);
+                  const PoleBatch& pb, int* err, int nsmall = 0, int nmid = 0);
 void launch_trsm(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
                  const PoleBatch& pb);
 void launch_gemm_update(cudaStream_t st, const GemmTask* tasks, int ntasks, int ntiles,

@@ -215,7 +215,7 @@ constexpr int SB = 16;
 
 template <int BK>   // maximum block size: 64 (PB), or 32 (small fronts: 128 threads,
                    // 4x less shared memory, several more CTAs per SM)
-__global__ void __launch_bounds__(BK == 32 ? 128 : 256) k_diag2(const PanelTask* __restrict__ tasks, FrontsDev F,
+__global__ void __launch_bounds__(BK <= 48 ? 128 : 256) k_diag2(const PanelTask* __restrict__ tasks, FrontsDev F,
                                                PoleBatch pb, int* err) {
   // Dg holds L (lower) and, transposed in the free upper triangle, X = L^{-1}
   // (X[i][j], i > j, at Dg[j][i]) -- exactly the panel layout written back.
@@ -342,14 +342,15 @@ static void diag2_go(cudaStream_t st, const PanelTask* tasks, int ntasks, const 
     attr = true;
   }
   dim3 grid(ntasks, pb.count);
-  k_diag2<BK><<<grid, BK == 32 ? 128 : 256, smem, st>>>(tasks, F, pb, err);
+  k_diag2<BK><<<grid, BK <= 48 ? 128 : 256, smem, st>>>(tasks, F, pb, err);
 }
 
-// the first nsmall tasks have blocks of at most 32 pivots (build_plans)
+// the first nsmall tasks have blocks of at most 32 pivots, the next nmid of 33..48 (build_plans)
 void launch_diag2(cudaStream_t st, const PanelTask* tasks, int ntasks, const FrontsDev& F,
-                  const PoleBatch& pb, int* err, int nsmall) {
+                  const PoleBatch& pb, int* err, int nsmall, int nmid) {
   diag2_go<32>(st, tasks, nsmall, F, pb, err);
-  diag2_go<PB>(st, tasks + nsmall, ntasks - nsmall, F, pb, err);
+  diag2_go<48>(st, tasks + nsmall, nmid, F, pb, err);
+  diag2_go<PB>(st, tasks + nsmall + nmid, ntasks - nsmall - nmid, F, pb, err);
 }
 
 // K4a': panel TRSM  L_r = F_r L_kk^{-T} D^{-1}  for one 64-row tile per CTA
